@@ -1,0 +1,402 @@
+"""Pins of the CPU oracle against things other than itself (runs without a GPU).
+
+Each test names the passage / closed form / brute force it pins.  A plausible
+mistake in the oracle (dropped term, wrong sign/index, transposed operand, wrong
+link direction, wrong memory timing) fails at least one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from tests.helpers_independent import brute_force_opt, bubble, fp_simulate, random_valid_plan
+from workloads import configs as K
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def inst(p, m, n_dc, f, d, w, **kw):
+    return K.uniform_instance(p, m, n_dc, f, d, w, **kw).item(0)
+
+
+# --------------------------------------------------------------------------- SPEC worked examples
+def test_spec_simulate_p2_m1(oracle_lib):
+    g = gold("spec_examples.json")["simulate_p2_m1_unit"]
+    d = inst(2, 1, 1, 1, 1, 1, m_f=1, m_d=0, m_w=-1)
+    r = oracle_lib.simulate(d, g["plan"])
+    assert r["status"] == 0 and r["makespan"] == g["makespan"]
+
+
+def test_spec_1f1b_p4_m8_and_bubble(oracle_lib):
+    g = gold("spec_examples.json")["simulate_1f1b_p4_m8"]
+    d = inst(4, 8, 1, 1, 1, 1)
+    r = oracle_lib.simulate(d, *oracle_lib.build_static("1f1b", 4, 8))
+    assert r["makespan"] == g["makespan"]
+    loc, glo = bubble(r["first_start"][0], r["last_end"][0], r["busy"][0], r["makespan"])
+    assert abs(loc - g["stage0_bubble_num"] / g["stage0_bubble_den"]) < 1e-9
+    assert abs(glo - g["stage0_bubble_num"] / g["stage0_bubble_den"]) < 1e-9
+
+
+def test_spec_greedy_p2_m1(oracle_lib):
+    g = gold("spec_examples.json")["greedy_p2_m1_unit"]
+    d = inst(2, 1, 1, 1, 1, 1, m_f=1, m_d=0, m_w=-1)
+    assert oracle_lib.greedy(d)["makespan"] == g["makespan"]
+
+
+def test_reserve_window_spec(oracle_lib):
+    for c in gold("spec_examples.json")["reserve_window"]["cases"]:
+        assert list(oracle_lib.reserve_window(c["intervals"], c["t_ready"], c["width"])) == c["window"]
+
+
+def test_reserve_window_vs_exhaustive_gap_scan(oracle_lib):
+    """first-fit equals an exhaustive scan on 1000 random interval sets."""
+    rng = np.random.default_rng(1)
+    for _ in range(1000):
+        k = int(rng.integers(0, 8))
+        pts = np.sort(rng.choice(200, size=2 * k, replace=False))
+        ivs = [(int(pts[2 * i]), int(pts[2 * i + 1])) for i in range(k)]
+        t, w = int(rng.integers(0, 200)), int(rng.integers(1, 30))
+        x = t
+        while any(not (x + w <= a or x >= b) for a, b in ivs):
+            x += 1
+        assert oracle_lib.reserve_window(ivs, t, w) == (x, x + w)
+
+
+def test_two_simultaneous_messages_serialize(oracle_lib):
+    """SPEC.md:551 / fig:comm_model: second ends at first_end + width."""
+    assert oracle_lib.reserve_window([(3, 10)], 3, 7) == (10, 17)
+
+
+# --------------------------------------------------------------------------- closed forms
+@pytest.mark.parametrize("kind", ["1f1b", "gpipe"])
+def test_Z1_zero_delay(oracle_lib, kind):
+    """Z1: (m + p - 1)(f + b) at zero delay, including m < p (reading Q23)."""
+    rng = np.random.default_rng(2)
+    for _ in range(60):
+        p, m = int(rng.integers(1, 12)), int(rng.integers(1, 20))
+        f, dd, w = (int(x) for x in rng.integers(1, 50, size=3))
+        d = inst(p, m, 2, f, dd, w, mlim_x1000=10**6)
+        r = oracle_lib.simulate(d, *oracle_lib.build_static(kind, p, m))
+        assert r["makespan"] == (m + p - 1) * (f + dd + w)
+
+
+def test_Z2_gpipe_with_delays(oracle_lib):
+    """Z2: p(f+b) + k(T_f+L_f+T_b+L_b) + (m-1)(max(f,T_f) + max(b,T_b)), k >= 1 boundaries."""
+    rng = np.random.default_rng(3)
+    for _ in range(80):
+        n_dc = int(rng.integers(2, 5))
+        p = int(rng.integers(n_dc, 12))
+        m = int(rng.integers(1, 16))
+        f, dd, w = (int(x) for x in rng.integers(1, 60, size=3))
+        Lf, Tf, Lb, Tb = (int(x) for x in rng.integers(0, 120, size=4))
+        d = inst(p, m, n_dc, f, dd, w, lat=Lf, bw=Tf, lat_b=Lb, bw_b=Tb, mlim_x1000=10**6)
+        k = min(n_dc, p) - 1                     # contiguous even split: one boundary per DC pair
+        b = dd + w
+        want = p * (f + b) + k * (Tf + Lf + Tb + Lb) + (m - 1) * (max(f, Tf) + max(b, Tb))
+        r = oracle_lib.simulate(d, *oracle_lib.build_static("gpipe", p, m))
+        assert r["makespan"] == want, (p, m, n_dc, f, b, Lf, Tf, Lb, Tb)
+
+
+def test_Z3_1f1b_two_stages(oracle_lib):
+    """Z3: 1F1B, p=2, one boundary, T <= min(f,b), m >= 2: (m+1)(f+b) + 2*ceil(m/2)*(L+T)."""
+    rng = np.random.default_rng(4)
+    for _ in range(80):
+        m = int(rng.integers(2, 30))
+        f, dd, w = (int(x) for x in rng.integers(1, 60, size=3))
+        b = dd + w
+        L = int(rng.integers(0, 200))
+        T = int(rng.integers(0, min(f, b) + 1))
+        d = inst(2, m, 2, f, dd, w, lat=L, bw=T, mlim_x1000=10**6)
+        r = oracle_lib.simulate(d, *oracle_lib.build_static("1f1b", 2, m))
+        assert r["makespan"] == (m + 1) * (f + b) + 2 * math.ceil(m / 2) * (L + T)
+
+
+def test_Z5_1f1b_peak_memory(oracle_lib):
+    """Z5: 1F1B peak on stage s = min(p - s, m) * m_f."""
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        p, m = int(rng.integers(1, 16)), int(rng.integers(1, 20))
+        mf = int(rng.integers(1, 5))
+        md = -int(rng.integers(0, mf + 1))
+        d = inst(p, m, 2, 3, 4, 5, m_f=mf, m_d=md, m_w=-mf - md, mlim_x1000=10**6)
+        r = oracle_lib.simulate(d, *oracle_lib.build_static("1f1b", p, m))
+        assert list(r["peak"]) == [min(p - s, m) * mf for s in range(p)]
+
+
+def test_Z6_greedy_matches_zbh1_closed_form(oracle_lib):
+    """Z6: greedy, zero delay, f=t_d=t_w, m_lim = p*m_f, m >= p: (3m + p - 1) f; this equals
+    ZB-H1's m(f+d+w) + (p-1)(f+d-w) and backs PAPER.md:443 ("Equivalent performance to ZB-H1")."""
+    rng = np.random.default_rng(6)
+    for _ in range(60):
+        p = int(rng.integers(1, 12))
+        m = int(rng.integers(p, 3 * p + 1))
+        f = int(rng.integers(4, 60))
+        ns = int(rng.choice([1, 2, 4]))
+        d = inst(p, m, 2, f, f, f, n_sub=ns)
+        r = oracle_lib.greedy(d)
+        assert r["status"] == 0 and r["makespan"] == (3 * m + p - 1) * f
+
+
+def test_dp_tail_and_zero1_shift(oracle_lib):
+    """DP overlap: AR after the last W/B -> 1F1B zero delay ends at Z1 + T_dp;
+    ZeRO-1 AG before the first F shifts everything by T_ag (uniform); zero volume = no change."""
+    p, m, f, dd, w = 4, 8, 10, 7, 5
+    Z1 = (m + p - 1) * (f + dd + w)
+    c, ln = oracle_lib.build_static("1f1b", p, m)
+    assert oracle_lib.simulate(inst(p, m, 1, f, dd, w, t_dp=0), c, ln)["makespan"] == Z1
+    assert oracle_lib.simulate(inst(p, m, 1, f, dd, w, t_dp=37), c, ln)["makespan"] == Z1 + 37
+    assert oracle_lib.simulate(inst(p, m, 1, f, dd, w, zero1=1, t_ag=11), c, ln)["makespan"] == Z1 + 11
+
+
+def test_appendix_c_bubble_strides(oracle_lib):
+    """App. C + SPEC.md:479: 1F1B delay accumulates (> 1.5 T_F extra), zero-delay = Z1."""
+    g = gold("spec_examples.json")["appendix_c_bubble_strides"]
+    p, m, TF = g["p"], g["m"], g["T_F"]
+    c, ln = oracle_lib.build_static("1f1b", p, m)
+    r0 = oracle_lib.simulate(inst(p, m, 2, TF, TF, TF, mlim_x1000=1000), c, ln)
+    r1 = oracle_lib.simulate(inst(p, m, 2, TF, TF, TF, lat=g["lat"], mlim_x1000=1000), c, ln)
+    assert r0["makespan"] == (m + p - 1) * 3 * TF
+    assert r1["makespan"] - r0["makespan"] > 1.5 * TF
+    gr0 = oracle_lib.greedy(inst(p, m, 2, TF, TF, TF))
+    gr1 = oracle_lib.greedy(inst(p, m, 2, TF, TF, TF, lat=g["lat"]))
+    assert gr0["makespan"] == (3 * m + p - 1) * TF                  # Z6
+    assert gr1["makespan"] - gr0["makespan"] < r1["makespan"] - r0["makespan"]
+    reg = gold("survey_check_tiny.json")["appendix_c"]                # regression (survey check)
+    assert (r0["makespan"], r1["makespan"], gr0["makespan"], gr1["makespan"]) == (
+        reg["1f1b_zero"], reg["1f1b_lat"], reg["greedy1_zero"], reg["greedy1_lat"])
+
+
+def test_Z7_monotone_and_convex_in_latency(oracle_lib):
+    """Z7 + SPEC.md:289: fixed-plan makespan is non-decreasing in every lat/bw entry and
+    convex piecewise-linear with integer slopes in a uniform boundary latency."""
+    rng = np.random.default_rng(7)
+    for _ in range(25):
+        d = K.random_instances(1, seed=int(rng.integers(1 << 30)), max_p=6, max_m=6).item(0)
+        if d["p"] < 2:
+            continue
+        codes = random_valid_plan(d, rng)
+        base = oracle_lib.simulate(d, codes)["makespan"]
+        for fld in ("lat_f", "bw_f", "lat_b", "bw_b"):
+            e = dict(d)
+            e[fld] = d[fld].copy()
+            e[fld][int(rng.integers(d["p"] - 1))] += int(rng.integers(1, 50))
+            assert oracle_lib.simulate(e, codes)["makespan"] >= base
+        vals = []
+        for L in range(0, 60, 3):
+            e = dict(d)
+            e["lat_f"] = np.full(d["p"] - 1, L)
+            e["lat_b"] = np.full(d["p"] - 1, L)
+            vals.append(oracle_lib.simulate(e, codes)["makespan"])
+        sec = np.diff(vals, 2)
+        assert np.all(sec >= 0)
+
+
+# --------------------------------------------------------------------------- independent formulation
+def test_simulate_equals_fixed_point_formulation(oracle_lib):
+    """SPEC.md:292 brute-force equivalence: the oracle's Kahn/first-fit evaluation equals the
+    least fixed point of the §3.5 equations with FIFO links (App. X1 equivalence under UD)."""
+    rng = np.random.default_rng(8)
+    batch = K.random_instances(150, seed=9, max_p=6, max_m=6, intra_delay=True)
+    for i in range(len(batch)):
+        d = batch.item(i)
+        codes = random_valid_plan(d, rng)
+        r = oracle_lib.simulate(d, codes, timeline=True)
+        fp = fp_simulate(d, codes)
+        assert not fp["deadlock"]
+        assert r["makespan"] == fp["makespan"]
+        for s in range(d["p"]):
+            assert list(r["t_start"][s, :len(codes[s])]) == fp["start"][s]
+
+
+def test_deadlock_matches_fixed_point_divergence(oracle_lib):
+    """Plans with swapped entries: oracle DEADLOCK <=> the fixed-point iteration diverges."""
+    rng = np.random.default_rng(10)
+    batch = K.random_instances(80, seed=11, max_p=5, max_m=5)
+    seen = deadlocks = 0
+    for i in range(len(batch)):
+        d = batch.item(i)
+        d["m_lim"] = d["m_lim"] * 100
+        codes = random_valid_plan(d, rng)
+        s = int(rng.integers(d["p"]))
+        if len(codes[s]) < 2:
+            continue
+        k = int(rng.integers(len(codes[s]) - 1))
+        codes[s][k], codes[s][k + 1] = codes[s][k + 1], codes[s][k]
+        st = oracle_lib.check_plan(d, codes)
+        r = oracle_lib.simulate(d, codes)
+        if st:
+            assert r["status"] == st
+            continue
+        fp = fp_simulate(d, codes)
+        assert (r["status"] & 1 == 1) == fp["deadlock"]
+        deadlocks += fp["deadlock"]
+        if not fp["deadlock"]:
+            assert r["makespan"] == fp["makespan"]
+        seen += 1
+    assert seen > 20 and deadlocks >= 3
+
+
+def test_bad_plan_rules(oracle_lib):
+    """Reading Q29: counts, W prefix, B mixed with D/W."""
+    d = inst(2, 2, 1, 1, 1, 1)
+    good = [[0, 0, 2, 3, 2, 3], [0, 2, 3, 0, 2, 3]]
+    assert oracle_lib.check_plan(d, good) == 0
+    assert oracle_lib.check_plan(d, [[0, 0, 3, 2, 2, 3], good[1]]) == 4     # W before its D
+    assert oracle_lib.check_plan(d, [[0, 0, 2, 2, 3], good[1]]) == 4        # missing W
+    assert oracle_lib.check_plan(d, [[0, 0, 0, 2, 3, 2, 3], good[1]]) == 4  # extra F
+    assert oracle_lib.check_plan(d, [[0, 0, 1, 2, 3], good[1]]) == 4        # B mixed with D/W
+    assert oracle_lib.check_plan(d, [[0, 0, 1, 1], [0, 1, 0, 1]]) == 0      # all combined
+
+
+# --------------------------------------------------------------------------- greedy properties
+def test_greedy_properties(oracle_lib):
+    """Alg. 1 pins: iteration count 3*n_mb*n_sub*n_PP; re-simulating the plan
+    reproduces the greedy timeline; peak <= M_L; determinism."""
+    batch = K.random_instances(200, seed=12, max_p=10, max_m=12)
+    for i in range(len(batch)):
+        d = batch.item(i)
+        g = oracle_lib.greedy(d, timeline=True)
+        assert g["status"] == 0
+        assert g["iterations"] == 3 * d["m"] * d["n_sub"] * d["p"]
+        assert np.all(g["peak"] <= d["m_lim"])
+        r = oracle_lib.simulate(d, g["codes"], g["len"], timeline=True)
+        assert r["status"] == 0 and r["makespan"] == g["makespan"]
+        assert np.array_equal(r["t_start"], g["t_start"])
+        fp = fp_simulate(d, [list(g["codes"][s, :g["len"][s]]) for s in range(d["p"])])
+        assert fp["makespan"] == g["makespan"]
+        g2 = oracle_lib.greedy(d)
+        assert np.array_equal(g2["codes"], g["codes"])
+
+
+def test_greedy_priority_examples(oracle_lib):
+    """SPEC.md:348-350 select_op examples, observed on a 1-stage instance:
+    warm-up prefers F; after an F the D is preferred; memory-blocked F -> W sub-block."""
+    d = inst(1, 3, 1, 2, 2, 2, m_f=2, m_d=-1, m_w=-1, mlim_x1000=2000)   # m_lim = 4: two F in flight
+    g = oracle_lib.greedy(d)
+    seq = list(g["codes"][0, :g["len"][0]])
+    assert seq[0] == 0                       # warm-up: F first
+    assert seq[1] == 2                       # after F, D (local F -> D on last stage)
+    d2 = inst(1, 2, 1, 2, 2, 2, m_f=2, m_d=0, m_w=-2, mlim_x1000=1000)   # m_lim = 2
+    s2 = list(oracle_lib.greedy(d2)["codes"][0, :9])
+    assert s2[:4] == [0, 2, 3, 0]            # F blocked by memory until W releases
+
+
+# --------------------------------------------------------------------------- brute force
+def test_exhaustive_optimum_vs_python_brute_force(oracle_lib):
+    """§4.1 validity set: the oracle's enumeration optimum equals a Python brute force over all
+    per-stage permutations evaluated by the fixed-point formulation (SPEC.md:547 <= 14 ops)."""
+    rng = np.random.default_rng(13)
+    cases = [(2, 2), (2, 1), (3, 1), (1, 3), (2, 2), (4, 1)]
+    for p, m in cases:
+        d = K.random_instances(1, seed=int(rng.integers(1 << 30)), max_p=1, max_m=1).item(0)
+        d = inst(p, m, int(rng.integers(1, 3)), int(rng.integers(1, 9)), int(rng.integers(1, 9)),
+                 int(rng.integers(1, 9)), lat=int(rng.integers(0, 6)), bw=int(rng.integers(0, 6)),
+                 mlim_x1000=int(rng.choice([1000, 1500, 3000])))
+        e = oracle_lib.enumerate_opt(d)
+        assert e["evaluated"] > 0
+        assert e["makespan"] == brute_force_opt(d)
+
+
+def test_optimal_le_greedy_le_and_le_1f1b(oracle_lib):
+    """North star / Q25: optimal <= greedy(n_sub=1) (theorem, same space and budget) and
+    optimal <= 1F1B; greedy <= 1F1B is only reported (empirical), not asserted."""
+    rng = np.random.default_rng(14)
+    for _ in range(30):
+        p, m = [(2, 2), (2, 3), (3, 2), (4, 1), (3, 1)][int(rng.integers(5))]
+        f = int(rng.integers(1, 9))
+        d = inst(p, m, 2, f, int(rng.integers(1, 9)), int(rng.integers(1, 9)),
+                 lat=int(rng.integers(0, 12)), bw=int(rng.integers(0, 8)), mlim_x1000=1000)
+        e = oracle_lib.enumerate_opt(d)
+        g = oracle_lib.greedy(d)
+        s = oracle_lib.simulate(d, *oracle_lib.build_static("1f1b", p, m))
+        assert e["makespan"] <= g["makespan"]
+        assert e["makespan"] <= s["makespan"]
+
+
+def test_p1_optimum_is_total_work(oracle_lib):
+    """One stage: every valid order is gap-free, so optimum = greedy = m (f + d + w)."""
+    d = inst(1, 3, 1, 3, 4, 5, mlim_x1000=3000)
+    assert oracle_lib.enumerate_opt(d)["makespan"] == 3 * 12 == oracle_lib.greedy(d)["makespan"]
+
+
+# --------------------------------------------------------------------------- regression (survey check)
+def test_survey_check_tiny_config(oracle_lib):
+    """REGRESSION (SURVEY.md §8(c) survey-check table; same reading, not independent).
+    The (0,0) column is independently fixed by Z1 (3300) and Z6 (2700); GPipe at (1,.5) by Z2."""
+    for pt in gold("survey_check_tiny.json")["points"]:
+        d = K.tiny(pt["lat_ratio"], pt["bw_ratio"]).item(0)
+        assert oracle_lib.simulate(d, *oracle_lib.build_static("gpipe", 4, 8))["makespan"] == pt["gpipe"]
+        assert oracle_lib.simulate(d, *oracle_lib.build_static("1f1b", 4, 8))["makespan"] == pt["1f1b"]
+        for ns, want in zip((1, 2, 4), pt["greedy"]):
+            e = dict(d); e["n_sub"] = ns
+            assert oracle_lib.greedy(e)["makespan"] == want
+
+
+# --------------------------------------------------------------------------- quantization
+def test_quantize_grounding(oracle_lib):
+    """Q21 quantization pinned to PAPER.md:618 numbers: T_F = 0.038 s -> 38,000 ticks @1 us;
+    1 GB at 421 Gb/s -> 19.0024 ms -> 19,002 ticks; alpha 19 ms -> 19,000; half-away rounding."""
+    g = gold("spec_examples.json")["m70_grounding"]
+    spec = {"p": 2, "m": 4, "n_sub": 1, "zero1": 0, "n_dc": 2, "dc_of_stage": [0, 1],
+            "t_f": [0.038, 0.038], "t_d": [0.038, 0.038], "t_w": [2.5e-6, 0.0000015],
+            "m_f": [2e9, 2e9], "m_d": [-1e9, -1e9], "m_w": [-1e9, -1e9], "m_lim": [8.5e9, 8e9],
+            "t_dp": [0.0, 0.0], "t_ag": [0.0, 0.0],
+            "alpha": [[0, 0.019], [0.076, 0]], "beta": [[0, 8 / 421e9], [8 / 105e9, 0]],
+            "msg_f": [g["msg_bytes"]], "msg_b": [g["msg_bytes"]], "tick_s": 1e-6, "mem_unit": 1e9}
+    q = oracle_lib.quantize(spec)
+    assert q["status"] == 0
+    assert list(q["t_f"]) == [38000, 38000]
+    assert list(q["t_w"]) == [3, 2]                 # 2.5 -> 3 (half away from zero), 1.5 -> 2
+    assert list(q["lat_f"]) == [19000] and list(q["lat_b"]) == [76000]
+    assert list(q["bw_f"]) == [19002]               # 1e9*8/421e9 s = 19.0024 ms
+    assert list(q["bw_b"]) == [76190]               # 1e9*8/105e9 s = 76.190 ms
+    assert list(q["m_lim"]) == [8, 8]               # budgets floor: 8.5 -> 8
+    bad = dict(spec, dc_of_stage=[1, 0])
+    assert oracle_lib.quantize(bad)["status"] == 8  # non-contiguous DC assignment
+    bad2 = dict(spec, m_w=[-2e9, -1e9])
+    assert oracle_lib.quantize(bad2)["status"] == 8  # deltas do not sum to zero
+
+
+def test_message_size_and_presets():
+    """message size b*s*d*n_DP*2; preset beta = 8 / (Gb/s * 1e9) s/B."""
+    g = gold("spec_examples.json")
+    for b, s, dd, ndp, bpe, want in g["message_size"]["cases"]:
+        assert b * s * dd * ndp * bpe == want
+    assert K.bw_ticks(421.0)[()] == 19002 and K.bw_ticks(105.0)[()] == 76190
+
+
+# --------------------------------------------------------------------------- sweep synthesis
+def test_grid_instance_synthesis(oracle_lib):
+    """the oracle's grid point decode equals an instance built directly
+    (workloads.uniform_instance) for random points of the config-5 grid."""
+    g = K.full_sweep_grid()
+    rng = np.random.default_rng(15)
+    for k in rng.integers(0, g.n_points, size=40):
+        i_pp, i_mb, i_lat, i_bw, i_mem, i_dp = (int(x) for x in g.point_axes(int(k)))
+        p, m = g.pp_vals[i_pp], g.mb_vals[i_mb]
+        want = K.uniform_instance(p, m, g.n_dc, int(g.base.t_f[0, 0]), int(g.base.t_d[0, 0]), int(g.base.t_w[0, 0]),
+                                  lat=int(g.lat[i_lat]), bw=int(g.bw[i_bw]), mlim_x1000=int(g.mlim_x1000[i_mem]),
+                                  t_dp=int(g.tdp[i_dp]), tick_s=g.base.tick_s).item(0)
+        got = oracle_lib.grid_instance(g, int(k))
+        for key in want:
+            assert np.array_equal(np.asarray(got[key]), np.asarray(want[key])), key
+
+
+def test_sweep_point_tiny(oracle_lib):
+    """Sweep argmin on the tiny grid point (1, .5): GPipe infeasible (peak 16 > 8), so the
+    winner is greedy; candidate makespans match Z2 (GPipe) and direct evaluation."""
+    from workloads.core import Grid
+    base = K.tiny(0, 0)
+    g = Grid(base=base, n_dc=2, pp_vals=[4], mb_vals=[8], lat=np.array([100]), bw=np.array([50]),
+             mlim_x1000=np.array([1000]), tdp=np.array([0]), cand_mask=0b11111)
+    key, cm = oracle_lib.sweep_point(g, 0)
+    assert cm[0] == -1                                  # GPipe memory-infeasible at M_L = p*m_f
+    assert cm[1] == 4500 and cm[2] == cm[3] == cm[4] == 3300
+    assert key == (3300 << 8) | 2
