@@ -1,0 +1,199 @@
+/*
+ * crosspipe.h -- C ABI (v1) of the B200-native CrossPipe hot path (arXiv 2507.00217).
+ *
+ * What the calls compute (citations are PAPER.md line numbers):
+ *   cp_simulate    §3.5 pipeline performance model (:257-260): per-stage block order ->
+ *                  timeline (start = max(previous block end on the stage, dependency end +
+ *                  comm delay)), alpha-beta comm with link queuing (fig:comm_model :133,
+ *                  Alg. 1 :404-407, §4.2.3 :436-437), memory accounting (§4.1 :307-308,
+ *                  :341-345), DP-overlap tail and ZeRO-1 gate (:363), runtime App. A (:808).
+ *   cp_greedy      Alg. 1 "Greedy Generation for CrossUDSub" (:383-412) with the §4.2.2
+ *                  scheduling loop (:415-432); returns the schedule and its timeline.
+ *   cp_sweep_shard schedule selection "with the best simulation performance" (:535, :543)
+ *                  over a grid of instances; candidates GPipe, 1F1B (tab:ppschedules :470),
+ *                  greedy n_sub = 1, 2, 4.
+ *   cp_quantize    SI (seconds, bytes, s/byte) -> integer ticks / memory units (tab:symbols
+ *                  :98-115, Alg. 1 inputs :381).
+ * Every ambiguity is resolved by the readings Q1-Q30 listed in DESIGN.md.
+ *
+ * Conventions
+ *   - Pointers are DEVICE pointers unless marked (host).  The caller owns every buffer;
+ *     the library allocates nothing and keeps no global state (reentrant).
+ *   - Compute calls enqueue on `stream` and return without synchronizing.  Return codes
+ *     (cp_rc) are API-level and synchronous: bad descriptor, unsupported shape, workspace
+ *     too small, CUDA launch error.  Per-item problems never fail a call: they set the
+ *     item's cp_item status bits, visible once the stream has completed.
+ *   - All device arithmetic is int32 on integer ticks; an item whose conservative horizon
+ *     bound U (Q21) is >= 2^30, or whose sizes exceed the GPU limits below, gets
+ *     CPI_OVERFLOW and is not evaluated.
+ *   - Outputs are deterministic and bit-identical across runs, GPUs and world sizes.
+ */
+#ifndef CROSSPIPE_H
+#define CROSSPIPE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CP_ABI_VERSION 1u
+#define CP_MAX_STAGES 32      /* lane-per-stage design: p <= 32 */
+#define CP_MAX_MB 1024        /* microbatches per instance */
+#define CP_MAX_SUB 16         /* n_sub limit of the GPU path */
+
+/* op codes of a plan entry (2 bits) */
+#define CP_OP_F 0u            /* forward block */
+#define CP_OP_B 1u            /* combined backward block B = D + W (App. B :811-822) */
+#define CP_OP_D 2u            /* input-gradient block (DGrad) */
+#define CP_OP_W 3u            /* ONE weight-gradient sub-block (n_sub per W block) */
+
+typedef enum { CP_OK = 0, CP_EINVAL = -1, CP_EUNSUPPORTED = -2, CP_ECUDA = -3, CP_EWORKSPACE = -4 } cp_rc;
+
+typedef enum {                /* per-item status bitmask */
+  CPI_OK = 0,
+  CPI_DEADLOCK = 1,           /* plan cannot complete (cross-stage cycle / D_j before F_j) */
+  CPI_MEM_EXCEEDED = 2,       /* completed, but a stage's peak > m_lim */
+  CPI_BAD_PLAN = 4,           /* static plan check failed (reading Q29) */
+  CPI_BAD_INSTANCE = 8,       /* instance invariant violated (Q10, Q12) */
+  CPI_OVERFLOW = 16           /* exceeds int32 horizon (U >= 2^30) or GPU size limits */
+} cp_item;
+
+/* Instance record v1: 1792 B, 128-B aligned, int32 ticks / memory units.
+ * Per-stage arrays are indexed by stage s < n_pp.  Boundary arrays are indexed by
+ * boundary s < n_pp-1: *_f = link s -> s+1 (activations), *_b = link s+1 -> s (gradients).
+ * Invariants (else CPI_BAD_INSTANCE): 1 <= n_pp <= 32, n_mb >= 1, n_sub >= 1; t_f, t_d,
+ * t_w > 0; t_w >= n_sub; m_f > 0, m_d <= 0, m_w <= 0, m_f + m_d + m_w == 0; m_lim >= m_f;
+ * t_dp, t_ag >= 0; lat/bw >= 0.  flags bit0 = ZeRO-1 (t_ag gates the stage's F blocks). */
+typedef struct {
+  uint8_t n_pp, n_dc, n_sub, flags;
+  uint16_t n_mb, version;                          /* version = 1 */
+  int32_t tick_ns;                                 /* informational: tick length */
+  uint8_t dc_first_stage[4];                       /* informational: contiguous DC split */
+  uint8_t _pad0[16];
+  int32_t t_f[32], t_d[32], t_w[32];               /* ticks */
+  int32_t m_f[32], m_d[32], m_w[32], m_lim[32];    /* memory units */
+  int32_t t_dp[32], t_ag[32];                      /* DP allreduce / ZeRO-1 allgather, ticks */
+  int32_t lat_f[32], bw_f[32], lat_b[32], bw_b[32];/* per boundary, ticks (bw = beta * msg) */
+  uint8_t _tail[96];
+} cp_inst_v1;
+
+typedef struct {
+  int32_t n;                  /* number of instance records */
+  int32_t max_pp;             /* upper bound of n_pp over the batch: selects the lane segment width */
+  int32_t max_mb;             /* upper bound of n_mb: sizes the workspace of the overflow path */
+  int32_t ring_hint;          /* upper bound of in-flight F blocks per stage, usually
+                                 min(n_mb, floor(m_lim/m_f)); 0 -> max_mb.  Only a performance hint. */
+  const cp_inst_v1* inst;     /* [n] */
+} cp_instances;
+
+/* Plan batch.  Entry k of stage s of schedule i is the 2-bit code
+ *   (ops[(i*words + k/16)*stage_stride + s] >> (2*(k%16))) & 3        (LSB first)
+ * i.e. word-major / stage-minor, so a warp reads word k of all its stages in one
+ * coalesced transaction.  Microbatch indices are implied by per-type counters
+ * (microbatch order within stage and type, §4.1 :346-351); W entries are sub-blocks. */
+typedef struct {
+  int32_t n;                  /* number of schedules */
+  int32_t stage_stride;       /* >= max_pp */
+  int32_t words;              /* words per stage row: capacity 16*words entries */
+  int32_t _pad;
+  const int32_t* inst_of;     /* [n] instance of schedule i; NULL: instance i (or 0 if instances.n == 1) */
+  uint32_t* ops;              /* [n][words][stage_stride]; input of cp_simulate, output of cp_greedy */
+  uint16_t* len;              /* [n][stage_stride] entries per stage row */
+} cp_schedules;
+
+typedef struct {
+  int64_t* makespan;          /* [n] App.-A runtime in ticks (origin t = 0); -1 if not completed */
+  int32_t* peak_mem;          /* [n] max over stages, -1 if not completed (nullable) */
+  int32_t* status;            /* [n] cp_item bitmask */
+  int32_t* stage_stats;       /* [n][stage_stride][4] first_start, last_end, busy, peak (nullable) */
+  int32_t* t_start;           /* [n][stage_stride][len_stride] start tick of every entry (nullable) */
+  int32_t len_stride;
+  int32_t _pad;
+  uint64_t* best_key;         /* [1] nullable: atomic min of (makespan << 32 | i) over items with
+                                 status 0; the caller initializes it to INT64_MAX */
+} cp_results;
+
+#define CP_GRID_MAX_AXIS 128
+#define CP_GRID_MAX_SMALL 16
+/* (host) Sweep grid.  Point k decodes mixed-radix as
+ *   k = ((((i_pp*n_mb_n + i_mb)*n_lat + i_lat)*n_bw + i_bw)*n_mem + i_mem)*n_dp + i_dp.
+ * Instance of a point: base per-stage costs / memory deltas / t_ag / flags, p = n_pp_vals[i_pp],
+ * m = n_mb_vals[i_mb]; stages split contiguously over min(n_dc, p) DCs, dc(s) = s*n_dc/p;
+ * a cross-DC boundary carries (lat[i_lat], bw[i_bw]) both ways, intra-DC boundaries (0, 0);
+ * m_lim[s] = (mlim_x1000[i_mem]*p*m_f[s] + 500)/1000; t_dp[s] = tdp[i_dp].
+ * Candidates (cand_mask bits): 0 GPipe, 1 1F1B (combined B; n_sub ignored), 2/3/4 greedy with
+ * n_sub = 1/2/4.  key = (makespan << 8) | cand (int64 >= 0), INT64_MAX for a memory-infeasible
+ * candidate; the point's key is the minimum (ties -> lower candidate id), INT64_MAX if no candidate
+ * is feasible, INT64_MAX-1 if the point exceeds the GPU limits (CPI_OVERFLOW).  Signed keys let
+ * an int64 all-reduce(MIN) across ranks act as allgather + argmin in one collective. */
+typedef struct {
+  cp_inst_v1 base;
+  int32_t n_dc;
+  int32_t n_pp_vals[8], n_pp_n;
+  int32_t n_mb_vals[8], n_mb_n;
+  int32_t lat[CP_GRID_MAX_AXIS], n_lat;
+  int32_t bw[CP_GRID_MAX_AXIS], n_bw;
+  int32_t mlim_x1000[CP_GRID_MAX_SMALL], n_mem;
+  int32_t tdp[CP_GRID_MAX_SMALL], n_dp;
+  uint32_t cand_mask;
+} cp_grid;
+
+uint32_t    cp_abi_version(void);
+const char* cp_status_string(int32_t code);   /* cp_rc (<0) or cp_item bitmask (>=0) */
+
+/* Workspace bytes (device memory, caller-allocated, need not be initialized) for a call
+ * over n_items items: which = 0 cp_simulate (desc: cp_instances*, n_items = schedules),
+ * 1 cp_greedy (desc: cp_instances*, n_items = instances), 2 cp_sweep_shard (desc: cp_grid*).
+ * Holds the overflow list and the global arrival rings of the fix-up pass. */
+size_t cp_workspace_bytes(int32_t which, const void* desc, int64_t n_items);
+
+/* Evaluate sched->n fixed plans.  Errors: CP_EINVAL (NULL/inconsistent descriptors,
+ * stage_stride < max_pp, words < 1, len_stride < 0), CP_EUNSUPPORTED (max_pp > 32),
+ * CP_EWORKSPACE, CP_ECUDA (launch failure). */
+int32_t cp_simulate(const cp_instances* inst, const cp_schedules* sched, const cp_results* res,
+                    void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
+
+/* Generate one greedy schedule per instance (out->n must equal inst->n, out->inst_of NULL,
+ * 16*out->words >= (2+n_sub)*n_mb).  Writes out->ops / out->len and res (its timeline). */
+int32_t cp_greedy(const cp_instances* inst, const cp_schedules* out, const cp_results* res,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* Evaluate grid points [point_lo, point_hi): writes keys[k] for k in range only (the caller
+ * fills the rest with INT64_MAX; cp_sweep in python = fill + shard + all_reduce(MIN)).
+ * cand_makespan (nullable) [n_points][5] int32: makespan of each candidate, -1 if not run
+ * or memory-infeasible.  grid is a HOST pointer, passed to the kernel by value. */
+int32_t cp_sweep_shard(const cp_grid* grid, int64_t point_lo, int64_t point_hi,
+                       int64_t* keys, int32_t* cand_makespan, void* ws, size_t ws_bytes, void* stream);
+
+/* (host) Cost-balanced partition of the grid's points over `world` ranks: bounds[0..world]
+ * with bounds[r]..bounds[r+1] owned by rank r; cuts at equal prefix sums of the estimated
+ * cost p*m*sum_{cand}(2 + n_sub(cand)). */
+int32_t cp_sweep_partition(const cp_grid* grid, int32_t world, int64_t* bounds);
+
+/* (host) SI -> record quantization.  All arrays have n_pp entries (boundary arrays n_pp-1).
+ * ticks = llround(x / tick_s) (half away from zero, double); bw = llround(beta*msg/tick_s);
+ * memory = llround(bytes / mem_unit), m_lim = floor(m_lim / mem_unit).  Returns the item
+ * status (0 or CPI_BAD_INSTANCE, CPI_OVERFLOW if a value does not fit int32). */
+typedef struct {
+  int32_t n_pp, n_mb, n_sub, zero1, n_dc;
+  int32_t dc_of_stage[32];
+  double t_f[32], t_d[32], t_w[32];                /* seconds */
+  double m_f[32], m_d[32], m_w[32], m_lim[32];     /* bytes */
+  double t_dp[32], t_ag[32];                       /* seconds */
+  double alpha[4][4];                              /* seconds, [src dc][dst dc] */
+  double beta[4][4];                               /* seconds per byte */
+  double msg_f[32], msg_b[32];                     /* bytes per boundary */
+  double tick_s, mem_unit;
+} cp_spec_si;
+int32_t cp_quantize(const cp_spec_si* spec /*host*/, cp_inst_v1* out /*host*/);
+
+/* (host) Invariant check of one record; returns 0 or CPI_BAD_INSTANCE / CPI_OVERFLOW and,
+ * if msg != NULL, a NUL-terminated message naming the violated invariant. */
+int32_t cp_validate_instance(const cp_inst_v1* inst /*host*/, char* msg, size_t msg_len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CROSSPIPE_H */

@@ -1,0 +1,17 @@
+"""B200-native CrossPipe hot path (arXiv 2507.00217): batched pipeline-schedule
+evaluation (§3.5 performance model), greedy schedule generation (Alg. 1) and
+grid sweeps with NCCL argmin.  The compute is in libcrosspipe.so (sm_100a);
+this package is a thin binding.  Importing it loads the library and fails loudly
+if it is missing -- there is no CPU fallback.
+"""
+from . import _lib
+
+_lib.load()
+
+from .api import (  # noqa: E402,F401
+    KEY_NONE, KEY_OVER, Instances, decode_key, greedy, pack_instances, quantize, records_to_device, ring_hint,
+    simulate, sweep_partition, sweep_shard, to_cp_grid, validate_record,
+)
+
+__all__ = ["Instances", "simulate", "greedy", "sweep_shard", "sweep_partition", "quantize", "decode_key",
+           "pack_instances", "records_to_device", "ring_hint", "to_cp_grid", "validate_record"]

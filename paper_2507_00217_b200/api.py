@@ -1,0 +1,243 @@
+"""Thin Python binding of the CrossPipe C ABI (argument marshalling only).
+
+Every step of the hot path runs in libcrosspipe.so kernels; this module only packs
+records, allocates result tensors with torch (device memory / streams are torch's),
+and forwards raw pointers.  Names follow include/crosspipe.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+INT32_MAX = 2**31 - 1
+KEY_NONE = 2**63 - 1          # no feasible candidate / not owned (int64 max)
+KEY_OVER = 2**63 - 2          # point exceeds GPU limits (CPI_OVERFLOW)
+
+
+def _require_cuda(*tensors):
+    if not torch.cuda.is_available():
+        raise RuntimeError("CrossPipe hot path needs a CUDA device (sm_100a); there is no CPU fallback")
+    for t in tensors:
+        if t is not None and not t.is_cuda:
+            raise ValueError("device tensors expected")
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+# ---------------------------------------------------------------------------------------- records
+def pack_instances(batch) -> np.ndarray:
+    """workloads.InstanceBatch -> numpy array of cp_inst_v1 records (format conversion)."""
+    n = len(batch)
+    rec = np.zeros(n, dtype=L.INST_DTYPE)
+    for k in ("t_f", "t_d", "t_w", "m_f", "m_d", "m_w", "m_lim", "t_dp", "t_ag", "lat_f", "bw_f", "lat_b", "bw_b"):
+        v = np.asarray(getattr(batch, k))
+        if v.size and (v.max() > INT32_MAX or v.min() < -INT32_MAX - 1):
+            raise OverflowError(f"{k} does not fit int32")
+        rec[k] = v
+    rec["n_pp"] = batch.p
+    rec["n_mb"] = batch.m
+    rec["n_sub"] = batch.n_sub
+    rec["flags"] = np.asarray(batch.zero1) & 1
+    rec["n_dc"] = batch.n_dc if batch.n_dc is not None else 1
+    rec["version"] = 1
+    rec["tick_ns"] = int(round(batch.tick_s * 1e9))
+    return rec
+
+
+def records_to_device(rec: np.ndarray, device="cuda") -> torch.Tensor:
+    return torch.from_numpy(rec.view(np.uint8).reshape(len(rec), 1792).copy()).to(device)
+
+
+def ring_hint(batch) -> int:
+    """max over items of min(n_mb, max_s floor(m_lim/m_f)) -- in-flight F bound."""
+    mf = np.maximum(np.asarray(batch.m_f), 1)
+    bound = (np.asarray(batch.m_lim) // mf).max(axis=1)
+    return int(np.max(np.minimum(bound, np.asarray(batch.m)))) if len(batch) else 1
+
+
+class Instances:
+    """Device-resident instance batch + the host-side hints the launcher needs."""
+
+    def __init__(self, batch, device="cuda"):
+        self.rec = pack_instances(batch)
+        self.dev = records_to_device(self.rec, device)
+        self.n = len(batch)
+        self.max_pp = int(np.max(batch.p))
+        self.max_mb = int(np.max(batch.m))
+        self.ring = ring_hint(batch)
+        self.max_sub = int(np.max(batch.n_sub))
+
+    def desc(self, ring=None):
+        return L.CpInstances(self.n, self.max_pp, self.max_mb, int(ring if ring is not None else self.ring),
+                             self.dev.data_ptr())
+
+
+def _workspace(which, desc, n_items, device):
+    nb = L.load().cp_workspace_bytes(which, C.byref(desc), n_items)
+    return torch.empty(max(int(nb), 256), dtype=torch.uint8, device=device)
+
+
+def _results(n, stage_stride, stats, timeline, len_stride, device, best):
+    r = {"makespan": torch.empty(n, dtype=torch.int64, device=device),
+         "peak_mem": torch.empty(n, dtype=torch.int32, device=device),
+         "status": torch.empty(n, dtype=torch.int32, device=device)}
+    if stats:
+        r["stage_stats"] = torch.empty((n, stage_stride, 4), dtype=torch.int32, device=device)
+    if timeline:
+        r["t_start"] = torch.zeros((n, stage_stride, len_stride), dtype=torch.int32, device=device)
+    if best:
+        r["best_key"] = torch.full((1,), KEY_NONE, dtype=torch.int64, device=device)
+    cres = L.CpResults(r["makespan"].data_ptr(), r["peak_mem"].data_ptr(), r["status"].data_ptr(),
+                       r["stage_stats"].data_ptr() if stats else None,
+                       r["t_start"].data_ptr() if timeline else None, int(len_stride if timeline else 0), 0,
+                       r["best_key"].data_ptr() if best else None)
+    return r, cres
+
+
+# ---------------------------------------------------------------------------------------- calls
+def simulate(inst: Instances, ops: torch.Tensor, lens: torch.Tensor, inst_of: torch.Tensor = None, *,
+             stats=False, timeline=False, len_stride=None, best=False, ring=None, stream=None, ws=None,
+             out=None):
+    """cp_simulate: evaluate ops.shape[0] fixed plans.  ops uint32-as-int32 [n, words, stride], lens int16 [n, stride]."""
+    _require_cuda(ops, lens, inst_of)
+    n, words, stride = ops.shape
+    dev = ops.device
+    d = inst.desc(ring)
+    if out is None:
+        out = _results(n, stride, stats, timeline, len_stride or 16 * words, dev, best)
+    r, cres = out
+    if ws is None:
+        ws = _workspace(0, d, n, dev)
+    sc = L.CpSchedules(n, stride, words, 0, _ptr(inst_of), ops.data_ptr(), lens.data_ptr())
+    if best:
+        r["best_key"].fill_(KEY_NONE)
+    rc = L.load().cp_simulate(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(ws.data_ptr()), ws.numel(),
+                              _stream(stream))
+    L.check(rc, "cp_simulate")
+    return r
+
+
+def greedy(inst: Instances, *, stats=False, timeline=False, stage_stride=None, words=None, ring=None,
+           stream=None, ws=None, out=None):
+    """cp_greedy: one Alg.-1 schedule per instance -> dict(ops, len, makespan, peak_mem, status, ...)."""
+    _require_cuda(inst.dev)
+    dev = inst.dev.device
+    n = inst.n
+    stride = stage_stride or inst.max_pp
+    if words is None:
+        words = ((2 + inst.max_sub) * inst.max_mb + 15) // 16
+    d = inst.desc(ring)
+    if out is None:
+        r, cres = _results(n, stride, stats, timeline, 16 * words, dev, False)
+        r["ops"] = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
+        r["len"] = torch.empty((n, stride), dtype=torch.int16, device=dev)
+        out = (r, cres)
+    r, cres = out
+    if ws is None:
+        ws = _workspace(1, d, n, dev)
+    sc = L.CpSchedules(n, stride, words, 0, None, r["ops"].data_ptr(), r["len"].data_ptr())
+    rc = L.load().cp_greedy(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(ws.data_ptr()), ws.numel(),
+                            _stream(stream))
+    L.check(rc, "cp_greedy")
+    return r
+
+
+def to_cp_grid(grid) -> L.CpGrid:
+    """workloads.Grid -> cp_grid (host struct, passed to the kernel by value)."""
+    g = L.CpGrid()
+    rec = pack_instances(grid.base)
+    C.memmove(C.addressof(g.base), rec.ctypes.data, 1792)
+    g.n_dc = int(grid.n_dc)
+    if len(grid.pp_vals) > 8 or len(grid.mb_vals) > 8:
+        raise ValueError("at most 8 n_pp / n_mb values")
+    for i, v in enumerate(grid.pp_vals):
+        g.n_pp_vals[i] = int(v)
+    g.n_pp_n = len(grid.pp_vals)
+    for i, v in enumerate(grid.mb_vals):
+        g.n_mb_vals[i] = int(v)
+    g.n_mb_n = len(grid.mb_vals)
+    for name, cap in (("lat", L.GRID_MAX_AXIS), ("bw", L.GRID_MAX_AXIS), ("mlim_x1000", L.GRID_MAX_SMALL),
+                      ("tdp", L.GRID_MAX_SMALL)):
+        v = np.asarray(getattr(grid, name), dtype=np.int64)
+        if len(v) > cap or (len(v) and (v.max() > INT32_MAX or v.min() < 0)):
+            raise ValueError(f"grid axis {name}: at most {cap} int32 values >= 0")
+        arr = getattr(g, name)
+        for i, x in enumerate(v):
+            arr[i] = int(x)
+    g.n_lat, g.n_bw, g.n_mem, g.n_dp = len(grid.lat), len(grid.bw), len(grid.mlim_x1000), len(grid.tdp)
+    g.cand_mask = int(grid.cand_mask)
+    return g
+
+
+def sweep_shard(grid, lo=0, hi=None, *, keys=None, cand=False, stream=None, device="cuda", cgrid=None):
+    """cp_sweep_shard over points [lo, hi).  Returns (keys uint64-as-int64 [n_points], cand_ms or None).
+    Keys outside [lo, hi) are INT64_MAX when `keys` is allocated here."""
+    _require_cuda()
+    g = cgrid if cgrid is not None else to_cp_grid(grid)
+    npts = grid.n_points
+    hi = npts if hi is None else hi
+    if keys is None:
+        keys = torch.full((npts,), KEY_NONE, dtype=torch.int64, device=device)
+    cm = torch.full((npts, 5), -1, dtype=torch.int32, device=device) if cand is True else (cand if cand is not False and cand is not None else None)
+    rc = L.load().cp_sweep_shard(C.byref(g), int(lo), int(hi), C.c_void_p(keys.data_ptr()),
+                                 _ptr(cm), None, 0, _stream(stream))
+    L.check(rc, "cp_sweep_shard")
+    return keys, cm
+
+
+def sweep_partition(grid, world: int, cgrid=None):
+    g = cgrid if cgrid is not None else to_cp_grid(grid)
+    b = (C.c_int64 * (world + 1))()
+    L.check(L.load().cp_sweep_partition(C.byref(g), int(world), b), "cp_sweep_partition")
+    return [int(x) for x in b]
+
+
+def decode_key(k: int):
+    """packed sweep key -> (makespan, candidate) or None (no feasible candidate / overflow)."""
+    k = int(k)
+    if k >= KEY_OVER:
+        return None
+    return k >> 8, k & 0xFF
+
+
+def quantize(spec: dict) -> tuple:
+    """cp_quantize: SI spec dict -> (status, record numpy[1] of INST_DTYPE)."""
+    s = L.CpSpecSI()
+    for k, v in spec.items():
+        if k in ("alpha", "beta"):
+            arr = getattr(s, k)
+            for i in range(min(4, len(v))):
+                for j in range(min(4, len(v[i]))):
+                    arr[i][j] = float(v[i][j])
+        elif k == "dc_of_stage":
+            arr = getattr(s, k)
+            for i, x in enumerate(v):
+                arr[i] = int(x)
+        elif k in ("p", "m"):
+            setattr(s, "n_pp" if k == "p" else "n_mb", int(v))
+        elif isinstance(v, (list, tuple, np.ndarray)):
+            arr = getattr(s, k)
+            for i, x in enumerate(v):
+                arr[i] = float(x)
+        else:
+            setattr(s, k, v)
+    rec = np.zeros(1, dtype=L.INST_DTYPE)
+    st = L.load().cp_quantize(C.byref(s), C.c_void_p(rec.ctypes.data))
+    return int(st), rec
+
+
+def validate_record(rec) -> tuple:
+    buf = C.create_string_buffer(256)
+    st = L.load().cp_validate_instance(C.c_void_p(rec.ctypes.data), buf, 256)
+    return int(st), buf.value.decode()

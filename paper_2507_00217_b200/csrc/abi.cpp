@@ -1,0 +1,352 @@
+// abi.cpp -- host side of the C ABI declared in include/crosspipe.h.
+// Descriptor validation, launch geometry (lane-segment width, arrival-ring size,
+// occupancy-sized persistent grids), workspace layout, the overflow fix-up pass,
+// cost-balanced sweep partition, SI -> tick quantization and the host validator.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "crosspipe.h"
+#include "engine.h"
+
+using cpk::Args;
+
+namespace {
+
+constexpr size_t kCtrlBytes = 256;
+constexpr size_t kMaxSmemPerBlock = 227 * 1024;
+
+int lg2_ceil(long long x) {
+  int l = 0;
+  while ((1LL << l) < x) ++l;
+  return l;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Ring slots needed by items: min(n_mb, in-flight F bound); the memory argument
+// bounds every producer->consumer lead by floor(m_lim/m_f).
+int ring_lg_for(const cp_instances* in) {
+  long long r = in->ring_hint > 0 ? in->ring_hint : in->max_mb;
+  r = std::max(1LL, std::min<long long>(r, in->max_mb > 0 ? in->max_mb : r));
+  return lg2_ceil(r);
+}
+
+int big_ring_lg(const cp_instances* in) { return lg2_ceil(std::max(1, std::min(in->max_mb, CP_MAX_MB))); }
+
+size_t ring_bytes_per_warp(int ring_lg) { return size_t(2) << (ring_lg + 5 + 2); }   // 2 rings x R x 32 x 4 B
+
+size_t ws_sim_greedy(const cp_instances* in, long long n_items) {
+  return kCtrlBytes + align256(sizeof(int32_t) * (size_t)std::max(1LL, n_items)) +
+         (size_t)cpk::kFixWarps * ring_bytes_per_warp(big_ring_lg(in));
+}
+
+int check_instances(const cp_instances* in) {
+  if (!in || !in->inst || in->n < 1) return CP_EINVAL;
+  if (in->max_pp < 1 || in->max_mb < 1) return CP_EINVAL;
+  if (in->max_pp > CP_MAX_STAGES) return CP_EUNSUPPORTED;
+  if (in->max_mb > CP_MAX_MB) return CP_EUNSUPPORTED;
+  return CP_OK;
+}
+
+int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, const cp_results* res, void* ws,
+               size_t ws_bytes, void* stream) {
+  const long long n = sc->n;
+  if (ws_bytes < ws_sim_greedy(in, n) || !ws) return CP_EWORKSPACE;
+  Args a;
+  std::memset(&a, 0, sizeof(a));
+  a.inst = in->inst;
+  a.inst_of = sc->inst_of;
+  a.n_inst = in->n;
+  a.n_items = (int32_t)n;
+  a.seg_lg = lg2_ceil(in->max_pp);
+  a.ops = sc->ops;
+  a.len = sc->len;
+  a.stage_stride = sc->stage_stride;
+  a.words = sc->words;
+  a.makespan = res->makespan;
+  a.peak_mem = res->peak_mem;
+  a.status = res->status;
+  a.stage_stats = res->stage_stats;
+  a.t_start = res->t_start;
+  a.len_stride = res->len_stride;
+  a.best_key = reinterpret_cast<unsigned long long*>(res->best_key);
+  char* base = static_cast<char*>(ws);
+  a.ovf_count = reinterpret_cast<int32_t*>(base);
+  a.ovf_list = reinterpret_cast<int32_t*>(base + kCtrlBytes);
+  int32_t* rings = reinterpret_cast<int32_t*>(base + kCtrlBytes + align256(sizeof(int32_t) * (size_t)std::max(1LL, n)));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(a.ovf_count, 0, sizeof(int32_t), st) != cudaSuccess) return CP_ECUDA;
+
+  const int nseg = 32 >> a.seg_lg;
+  const int sms = cpk::device_sm_count();
+  int rlg = ring_lg_for(in);
+  const int blg = big_ring_lg(in);
+  int wpb = (int)std::min<size_t>(4, kMaxSmemPerBlock / ring_bytes_per_warp(rlg));
+  if (wpb >= 1) {
+    // fast pass: shared-memory rings, occupancy-sized persistent grid
+    a.ring_lg = rlg;
+    const size_t smem = ring_bytes_per_warp(rlg) * wpb;
+    const int threads = 32 * wpb;
+    const int bps = cpk::engine_blocks_per_sm(mode, false, threads, smem);
+    const long long need = (n + (long long)nseg * wpb - 1) / ((long long)nseg * wpb);
+    const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
+    if (cpk::launch_engine(mode, false, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+    // fix-up pass over the overflow list with global rings of n_mb slots
+    a.from_list = 1;
+    a.ring_lg = blg;
+    a.ring_g = rings;
+    if (cpk::launch_engine(mode, true, a, cpk::kFixWarps / 4, cpk::kThreads, 0, stream) != cudaSuccess) return CP_ECUDA;
+  } else {
+    // rings too large for shared memory: single global-ring pass
+    a.ring_lg = blg;
+    a.ring_g = rings;
+    if (cpk::launch_engine(mode, true, a, cpk::kFixWarps / 4, cpk::kThreads, 0, stream) != cudaSuccess) return CP_ECUDA;
+  }
+  return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
+}
+
+// grid helpers ---------------------------------------------------------------
+long long grid_points(const cp_grid* g) {
+  return (long long)g->n_pp_n * g->n_mb_n * g->n_lat * g->n_bw * g->n_mem * g->n_dp;
+}
+
+int check_grid(const cp_grid* g) {
+  if (!g) return CP_EINVAL;
+  if (g->n_pp_n < 1 || g->n_pp_n > 8 || g->n_mb_n < 1 || g->n_mb_n > 8) return CP_EINVAL;
+  if (g->n_lat < 1 || g->n_lat > CP_GRID_MAX_AXIS || g->n_bw < 1 || g->n_bw > CP_GRID_MAX_AXIS) return CP_EINVAL;
+  if (g->n_mem < 1 || g->n_mem > CP_GRID_MAX_SMALL || g->n_dp < 1 || g->n_dp > CP_GRID_MAX_SMALL) return CP_EINVAL;
+  for (int i = 0; i < g->n_pp_n; ++i) {
+    if (g->n_pp_vals[i] < 1) return CP_EINVAL;
+    if (g->n_pp_vals[i] > CP_MAX_STAGES) return CP_EUNSUPPORTED;
+  }
+  for (int i = 0; i < g->n_mb_n; ++i) {
+    if (g->n_mb_vals[i] < 1) return CP_EINVAL;
+    if (g->n_mb_vals[i] > CP_MAX_MB) return CP_EUNSUPPORTED;
+  }
+  return CP_OK;
+}
+
+// ring slots needed by the points of one p-class: max over (m, M_L) of
+// min(m, max_s floor(m_lim[s] / m_f[s])) -- greedy and feasible static plans never exceed it
+int sweep_ring_lg(const cp_grid* g, int p) {
+  long long r = 1;
+  for (int im = 0; im < g->n_mb_n; ++im)
+    for (int ix = 0; ix < g->n_mem; ++ix) {
+      long long need = 1;
+      for (int s = 0; s < p; ++s) {
+        const long long mf = std::max(1, g->base.m_f[s]);
+        const long long mlim = ((long long)g->mlim_x1000[ix] * p * mf + 500) / 1000;
+        need = std::max(need, mlim / mf);
+      }
+      r = std::max(r, std::min<long long>(need, g->n_mb_vals[im]));
+    }
+  return lg2_ceil(r);
+}
+
+long long point_cost(const cp_grid* g, int i_pp, int i_mb) {
+  static const int units[5] = {2, 2, 3, 4, 6};   // entries per microbatch: 2m static, (2+n_sub)m greedy
+  long long u = 0;
+  for (int c = 0; c < 5; ++c)
+    if ((g->cand_mask >> c) & 1u) u += units[c];
+  return (long long)g->n_pp_vals[i_pp] * g->n_mb_vals[i_mb] * std::max(1LL, u);
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t cp_abi_version(void) { return CP_ABI_VERSION; }
+
+const char* cp_status_string(int32_t code) {
+  switch (code) {
+    case CP_OK: return "ok";
+    case CP_EINVAL: return "invalid argument / descriptor";
+    case CP_EUNSUPPORTED: return "unsupported shape (p > 32 or n_mb > 1024)";
+    case CP_ECUDA: return "CUDA launch error";
+    case CP_EWORKSPACE: return "workspace too small";
+    case CPI_DEADLOCK: return "deadlock: plan cannot complete";
+    case CPI_MEM_EXCEEDED: return "memory limit exceeded";
+    case CPI_BAD_PLAN: return "bad plan";
+    case CPI_BAD_INSTANCE: return "bad instance";
+    case CPI_OVERFLOW: return "exceeds int32 horizon / GPU size limits";
+    default: return code > 0 ? "multiple item status bits" : "unknown error";
+  }
+}
+
+size_t cp_workspace_bytes(int32_t which, const void* desc, int64_t n_items) {
+  if (which == 2) return kCtrlBytes;
+  if (which != 0 && which != 1) return 0;
+  const cp_instances* in = static_cast<const cp_instances*>(desc);
+  if (!in || n_items < 0) return 0;
+  return ws_sim_greedy(in, n_items);
+}
+
+int32_t cp_simulate(const cp_instances* in, const cp_schedules* sc, const cp_results* res, void* ws, size_t ws_bytes,
+                    void* stream) {
+  int rc = check_instances(in);
+  if (rc) return rc;
+  if (!sc || !res || sc->n < 0 || !sc->ops || !sc->len || !res->makespan || !res->status) return CP_EINVAL;
+  if (sc->stage_stride < in->max_pp || sc->words < 1 || (res->t_start && res->len_stride < 1)) return CP_EINVAL;
+  if (!sc->inst_of && in->n != 1 && in->n < sc->n) return CP_EINVAL;
+  if (sc->n == 0) return CP_OK;
+  return run_engine(cpk::MODE_SIM, in, sc, res, ws, ws_bytes, stream);
+}
+
+int32_t cp_greedy(const cp_instances* in, const cp_schedules* out, const cp_results* res, void* ws, size_t ws_bytes,
+                  void* stream) {
+  int rc = check_instances(in);
+  if (rc) return rc;
+  if (!out || !res || out->n != in->n || out->inst_of || !out->ops || !out->len || !res->makespan || !res->status)
+    return CP_EINVAL;
+  if (out->stage_stride < in->max_pp || out->words < 1 || (res->t_start && res->len_stride < 1)) return CP_EINVAL;
+  return run_engine(cpk::MODE_GREEDY, in, out, res, ws, ws_bytes, stream);
+}
+
+int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, int32_t* cand_ms, void* ws,
+                       size_t ws_bytes, void* stream) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  const long long np = grid_points(g);
+  if (!keys || lo < 0 || hi < lo || hi > np) return CP_EINVAL;
+  (void)ws; (void)ws_bytes;
+  if (lo == hi) return CP_OK;
+  const long long per_pp = np / g->n_pp_n;        // p is the slowest axis: one contiguous block per p
+  const int sms = cpk::device_sm_count();
+  for (int ip = 0; ip < g->n_pp_n; ++ip) {
+    const long long a0 = std::max<long long>(lo, ip * per_pp), a1 = std::min<long long>(hi, (ip + 1) * per_pp);
+    if (a0 >= a1) continue;
+    Args a;
+    std::memset(&a, 0, sizeof(a));
+    a.grid = *g;
+    a.pt_lo = a0;
+    a.pt_hi = a1;
+    a.keys = reinterpret_cast<unsigned long long*>(keys);
+    a.cand_ms = cand_ms;
+    a.seg_lg = lg2_ceil(g->n_pp_vals[ip]);
+    a.ring_lg = sweep_ring_lg(g, g->n_pp_vals[ip]);
+    const int wpb = (int)std::min<size_t>(4, kMaxSmemPerBlock / ring_bytes_per_warp(a.ring_lg));
+    if (wpb < 1) return CP_EUNSUPPORTED;
+    const size_t smem = ring_bytes_per_warp(a.ring_lg) * wpb;
+    const int threads = 32 * wpb;
+    const int nseg = 32 >> a.seg_lg;
+    const int bps = cpk::engine_blocks_per_sm(cpk::MODE_SWEEP, false, threads, smem);
+    const long long need = (a1 - a0 + (long long)nseg * wpb - 1) / ((long long)nseg * wpb);
+    const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
+    if (cpk::launch_engine(cpk::MODE_SWEEP, false, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+  }
+  return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
+}
+
+int32_t cp_sweep_partition(const cp_grid* g, int32_t world, int64_t* bounds) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  if (world < 1 || !bounds) return CP_EINVAL;
+  const long long inner = (long long)g->n_lat * g->n_bw * g->n_mem * g->n_dp;   // equal-cost run
+  const int nblk = g->n_pp_n * g->n_mb_n;
+  std::vector<long long> pre(nblk + 1, 0);
+  for (int b = 0; b < nblk; ++b) pre[b + 1] = pre[b] + point_cost(g, b / g->n_mb_n, b % g->n_mb_n) * inner;
+  const long long total = pre[nblk];
+  bounds[0] = 0;
+  for (int r = 1; r < world; ++r) {
+    const long double target = (long double)total * r / world;
+    int b = 0;
+    while (b < nblk && pre[b + 1] <= target) ++b;
+    long long pt;
+    if (b >= nblk) pt = (long long)nblk * inner;
+    else {
+      const long long c = point_cost(g, b / g->n_mb_n, b % g->n_mb_n);
+      long long k = (long long)std::llround((double)((target - pre[b]) / c));
+      k = std::max(0LL, std::min(inner, k));
+      pt = (long long)b * inner + k;
+    }
+    bounds[r] = std::max<long long>(pt, bounds[r - 1]);
+  }
+  bounds[world] = (long long)nblk * inner;
+  return CP_OK;
+}
+
+int32_t cp_validate_instance(const cp_inst_v1* I, char* msg, size_t msg_len) {
+  auto fail = [&](int code, const char* what, int s) {
+    if (msg && msg_len) std::snprintf(msg, msg_len, "%s%s%d", what, s >= 0 ? " at stage/boundary " : "", s);
+    return code;
+  };
+  if (!I) return fail(CPI_BAD_INSTANCE, "null record", -1);
+  if (I->n_pp < 1 || I->n_pp > CP_MAX_STAGES) return fail(CPI_BAD_INSTANCE, "n_pp out of [1, 32]", -1);
+  if (I->n_mb < 1) return fail(CPI_BAD_INSTANCE, "n_mb < 1", -1);
+  if (I->n_sub < 1) return fail(CPI_BAD_INSTANCE, "n_sub < 1", -1);
+  for (int s = 0; s < I->n_pp; ++s) {
+    if (I->t_f[s] <= 0 || I->t_d[s] <= 0 || I->t_w[s] <= 0) return fail(CPI_BAD_INSTANCE, "durations must be > 0", s);
+    if (I->t_w[s] < I->n_sub) return fail(CPI_BAD_INSTANCE, "t_w < n_sub (integer sub-blocks)", s);
+    if (I->m_f[s] <= 0 || I->m_d[s] > 0 || I->m_w[s] > 0) return fail(CPI_BAD_INSTANCE, "memory delta signs", s);
+    if ((long long)I->m_f[s] + I->m_d[s] + I->m_w[s] != 0) return fail(CPI_BAD_INSTANCE, "memory deltas do not sum to zero", s);
+    if (I->m_lim[s] < I->m_f[s]) return fail(CPI_BAD_INSTANCE, "m_lim < m_f", s);
+    if (I->t_dp[s] < 0 || I->t_ag[s] < 0) return fail(CPI_BAD_INSTANCE, "negative DP time", s);
+    if (s < I->n_pp - 1 && (I->lat_f[s] < 0 || I->bw_f[s] < 0 || I->lat_b[s] < 0 || I->bw_b[s] < 0))
+      return fail(CPI_BAD_INSTANCE, "negative link delay", s);
+  }
+  if (I->n_mb > CP_MAX_MB || I->n_sub > CP_MAX_SUB) return fail(CPI_OVERFLOW, "n_mb/n_sub exceed GPU limits", -1);
+  long long U = 0;
+  for (int s = 0; s < I->n_pp; ++s) {
+    U += (long long)I->n_mb * ((long long)I->t_f[s] + I->t_d[s] + I->t_w[s]) + I->t_dp[s] + ((I->flags & 1) ? I->t_ag[s] : 0);
+    if (s < I->n_pp - 1) U += (long long)I->n_mb * ((long long)I->lat_f[s] + I->bw_f[s] + I->lat_b[s] + I->bw_b[s]);
+  }
+  if (U >= (1LL << 30)) return fail(CPI_OVERFLOW, "horizon bound U >= 2^30 ticks", -1);
+  if (msg && msg_len) msg[0] = 0;
+  return 0;
+}
+
+int32_t cp_quantize(const cp_spec_si* S, cp_inst_v1* o) {
+  if (!S || !o) return CPI_BAD_INSTANCE;
+  std::memset(o, 0, sizeof(*o));
+  if (S->n_pp < 1 || S->n_pp > CP_MAX_STAGES || S->n_dc < 1 || S->n_dc > 4 || !(S->tick_s > 0) || !(S->mem_unit > 0))
+    return CPI_BAD_INSTANCE;
+  if (S->n_mb < 1 || S->n_mb > 65535 || S->n_sub < 1 || S->n_sub > 255) return CPI_BAD_INSTANCE;
+  o->n_pp = (uint8_t)S->n_pp;
+  o->n_mb = (uint16_t)S->n_mb;
+  o->n_sub = (uint8_t)S->n_sub;
+  o->n_dc = (uint8_t)S->n_dc;
+  o->flags = S->zero1 ? 1 : 0;
+  o->version = 1;
+  o->tick_ns = (int32_t)std::llround(S->tick_s * 1e9);
+  bool over = false;
+  auto q = [&](double x, double unit) -> int32_t {
+    const long long v = std::llround(x / unit);
+    if (v > INT32_MAX || v < INT32_MIN) { over = true; return 0; }
+    return (int32_t)v;
+  };
+  for (int s = 0; s < S->n_pp; ++s) {
+    const int dc = S->dc_of_stage[s];
+    if (dc < 0 || dc >= S->n_dc) return CPI_BAD_INSTANCE;
+    if (s > 0 && dc < S->dc_of_stage[s - 1]) return CPI_BAD_INSTANCE;     // contiguous DC assignment
+    if (s == 0 || dc != S->dc_of_stage[s - 1]) o->dc_first_stage[dc] = (uint8_t)s;
+    o->t_f[s] = q(S->t_f[s], S->tick_s);
+    o->t_d[s] = q(S->t_d[s], S->tick_s);
+    o->t_w[s] = q(S->t_w[s], S->tick_s);
+    o->m_f[s] = q(S->m_f[s], S->mem_unit);
+    o->m_d[s] = q(S->m_d[s], S->mem_unit);
+    o->m_w[s] = q(S->m_w[s], S->mem_unit);
+    const double ml = std::floor(S->m_lim[s] / S->mem_unit);
+    if (ml > INT32_MAX) over = true; else o->m_lim[s] = (int32_t)ml;
+    o->t_dp[s] = q(S->t_dp[s], S->tick_s);
+    o->t_ag[s] = S->zero1 ? q(S->t_ag[s], S->tick_s) : 0;
+    if (s < S->n_pp - 1) {
+      const int a = S->dc_of_stage[s], b = S->dc_of_stage[s + 1];
+      o->lat_f[s] = q(S->alpha[a][b], S->tick_s);
+      const double wf = S->beta[a][b] * S->msg_f[s];
+      o->bw_f[s] = q(wf, S->tick_s);
+      o->lat_b[s] = q(S->alpha[b][a], S->tick_s);
+      const double wb = S->beta[b][a] * S->msg_b[s];
+      o->bw_b[s] = q(wb, S->tick_s);
+    }
+  }
+  const int32_t v = cp_validate_instance(o, nullptr, 0);
+  if (v == CPI_BAD_INSTANCE) return v;
+  return over ? CPI_OVERFLOW : 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,520 @@
+// engine.cu -- sm_100a kernels of the CrossPipe hot path (arXiv 2507.00217).
+//
+// One warp evaluates 32/W items at a time: lane = pipeline stage, W = pow2 >= p is
+// the lane-segment width (small-p items are packed several per warp; shuffles use
+// the `width` argument so segments never talk to each other).  Evaluation is
+// round-synchronous dataflow:
+//   * each lane holds its stage's clock, memory, per-type counters and the FIFO
+//     clocks of its two outgoing links in registers;
+//   * a finished F (resp. D/B) block pushes its message through the link clock
+//     (Alg. 1 :404-407: E_bw = BW_model(end), T_avail = E_bw + T_lat) and writes the
+//     arrival time into the consumer's shared-memory arrival ring (slot-major
+//     [R][32] layout: lane l always hits bank l -> conflict-free);
+//   * producer counts are exchanged with one __shfl_up / __shfl_down per round.
+// MODE_SIM    : plan-driven (cp_simulate): a lane executes its next plan entry as
+//               soon as the entry's input is known (the §3.5 max-plus recurrence).
+// MODE_GREEDY : Alg. 1 + §4.2.2 (cp_greedy): every lane computes its schedulable
+//               time t*_s; two min-plus warp scans give a causal horizon H_s and every
+//               lane with t*_s < H_s decides in the same round (DESIGN.md "round-
+//               parallel greedy"), which reproduces sequential Alg. 1 exactly.
+// MODE_SWEEP  : (cp_sweep_shard) grid point -> instance synthesis in registers ->
+//               GPipe / 1F1B plans generated arithmetically + greedy n_sub = 1, 2, 4 ->
+//               packed (makespan << 8 | cand) argmin per point.
+// No tensor cores: nothing here is a dense contraction.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "engine.h"
+
+namespace cpk {
+
+constexpr int32_t INF = 1 << 30;        // > every valid tick value (guard U < 2^30)
+constexpr unsigned FULL = 0xffffffffu;
+constexpr unsigned long long KEY_NONE = 0x7fffffffffffffffull;   // no feasible candidate (INT64_MAX)
+constexpr unsigned long long KEY_OVER = 0x7ffffffffffffffeull;   // point not evaluated (CPI_OVERFLOW)
+
+__device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
+__device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
+
+// Arithmetic static plans (Table tab:ppschedules :470; readings Q22/Q23).
+// GPipe: F x m, B x m.  1F1B: w = min(p-s-1, m) F, (F,B) x (m-w), B x w.
+__device__ __forceinline__ uint32_t static_code(int cand, int s, int p, int m, int pos) {
+  if (cand == 0) return pos < m ? CP_OP_F : CP_OP_B;
+  int w = imin(p - s - 1, m);
+  if (pos < w) return CP_OP_F;
+  int q = pos - w;
+  if (q < 2 * (m - w)) return (q & 1) ? CP_OP_B : CP_OP_F;
+  return CP_OP_B;
+}
+
+struct LaneCfg {       // per-lane (stage) instance fields
+  int p, m, nsub, tagate;
+  int tf, td, tw, wq, wr, mf, md, mw, mlim, tdp;
+  int latF, bwF, latB, bwB;
+  int P, Q;            // greedy lookahead: exclusive prefix of (tf+bwF+latF), inclusive prefix of (td+bwB+latB)
+};
+
+template <int kMode, bool kRingGlobal>
+__global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Args A) {
+  extern __shared__ int32_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int lgW = A.seg_lg;
+  const int W = 1 << lgW;
+  const int s = lane & (W - 1);
+  const int seg = lane >> lgW;
+  const int nseg = 32 >> lgW;
+  const unsigned segmask = (W == 32) ? FULL : (((1u << W) - 1u) << (seg * W));
+  const int RM = (1 << A.ring_lg) - 1;
+  const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  int32_t* ringF = kRingGlobal ? A.ring_g + gwarp * (2LL << (A.ring_lg + 5)) : smem + wib * (2 << (A.ring_lg + 5));
+  int32_t* ringD = ringF + ((RM + 1) << 5);
+
+  long long task = gwarp * nseg + seg;
+  const long long task_stride = nwarps * nseg;
+
+  LaneCfg c = {};
+  long long item = -1;
+  bool need_load = true;
+  int load_status = 0;
+  int zero1 = 0, valid_inst = 0;
+  // dynamic state of this lane's stage
+  int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0, linkF = 0, linkB = 0;
+  int first = 0, busy = 0, pos = 0, plen = 0, comb = 0, last_fd = 0;
+  uint32_t word = 0, nextword = 0;
+  bool ovf = false;
+  // sweep: current candidate (>= 0), or -(c+1) = "advance to the first candidate >= c"
+  int cand = 0;
+  bool cand_greedy = (kMode == MODE_GREEDY);
+  unsigned long long best = KEY_NONE;
+
+  for (;;) {
+    // ------------------------------------------------------------------ fetch + load (per segment)
+    bool just_loaded = false;
+    if (need_load) {
+      need_load = false;
+      item = -1;
+      if (kMode == MODE_SWEEP) {
+        const long long pt = A.pt_lo + task;
+        if (pt < A.pt_hi) item = pt;
+      } else if (A.from_list) {
+        const int cnt = *(volatile int32_t*)A.ovf_count;
+        if (task < cnt) item = A.ovf_list[task];
+      } else if (task < A.n_items) {
+        item = task;
+      }
+      task += task_stride;
+      if (item >= 0) {
+        just_loaded = true;
+        int lat_b_s = 0, bw_b_s = 0;   // lane s validates boundary s in both directions
+        c = LaneCfg{};
+        if (kMode == MODE_SWEEP) {
+          const cp_grid& G = A.grid;
+          long long k = item;
+          const int i_dp = (int)(k % G.n_dp); k /= G.n_dp;
+          const int i_mem = (int)(k % G.n_mem); k /= G.n_mem;
+          const int i_bw = (int)(k % G.n_bw); k /= G.n_bw;
+          const int i_lat = (int)(k % G.n_lat); k /= G.n_lat;
+          const int i_mb = (int)(k % G.n_mb_n); k /= G.n_mb_n;
+          const int i_pp = (int)k;
+          c.p = G.n_pp_vals[i_pp];
+          c.m = G.n_mb_vals[i_mb];
+          c.nsub = 1;
+          zero1 = G.base.flags & 1;
+          const int ndc = imin(G.n_dc, c.p);
+          if (s < c.p) {
+            c.tf = G.base.t_f[s]; c.td = G.base.t_d[s]; c.tw = G.base.t_w[s];
+            c.mf = G.base.m_f[s]; c.md = G.base.m_d[s]; c.mw = G.base.m_w[s];
+            c.mlim = (int)(((long long)G.mlim_x1000[i_mem] * c.p * c.mf + 500) / 1000);
+            c.tdp = G.tdp[i_dp];
+            c.tagate = G.base.t_ag[s];
+            const bool xf = (s < c.p - 1) && (s * ndc / c.p != (s + 1) * ndc / c.p);
+            const bool xb = (s > 0) && ((s - 1) * ndc / c.p != s * ndc / c.p);
+            c.latF = xf ? G.lat[i_lat] : 0; c.bwF = xf ? G.bw[i_bw] : 0;
+            c.latB = xb ? G.lat[i_lat] : 0; c.bwB = xb ? G.bw[i_bw] : 0;
+            lat_b_s = c.latF; bw_b_s = c.bwF;
+          }
+        } else {
+          const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
+          const cp_inst_v1* I = A.inst + ii;
+          c.p = I->n_pp; c.m = I->n_mb; c.nsub = I->n_sub;
+          zero1 = I->flags & 1;
+          if (s < c.p && s < CP_MAX_STAGES) {
+            c.tf = I->t_f[s]; c.td = I->t_d[s]; c.tw = I->t_w[s];
+            c.mf = I->m_f[s]; c.md = I->m_d[s]; c.mw = I->m_w[s]; c.mlim = I->m_lim[s];
+            c.tdp = I->t_dp[s];
+            c.tagate = I->t_ag[s];
+            c.latF = (s < c.p - 1) ? I->lat_f[s] : 0; c.bwF = (s < c.p - 1) ? I->bw_f[s] : 0;
+            c.latB = (s > 0) ? I->lat_b[s - 1] : 0; c.bwB = (s > 0) ? I->bw_b[s - 1] : 0;
+            lat_b_s = (s < c.p - 1) ? I->lat_b[s] : 0; bw_b_s = (s < c.p - 1) ? I->bw_b[s] : 0;
+          }
+        }
+        // instance invariants (readings Q10, Q12)
+        bool bad = c.p < 1 || c.p > CP_MAX_STAGES || c.m < 1 || c.nsub < 1;
+        if (!bad && s < c.p) {
+          bad = !(c.tf > 0 && c.td > 0 && c.tw > 0 && c.tw >= c.nsub && c.mf > 0 && c.md <= 0 && c.mw <= 0 &&
+                  (long long)c.mf + c.md + c.mw == 0 && c.mlim >= c.mf && c.tdp >= 0 && c.tagate >= 0 &&
+                  c.latF >= 0 && c.bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
+        }
+        if (!zero1) c.tagate = 0;
+        valid_inst = !bad;
+        load_status = bad ? CPI_BAD_INSTANCE : 0;
+        c.wq = c.tw / imax(c.nsub, 1);
+        c.wr = c.tw % imax(c.nsub, 1);
+        plen = 0; word = nextword = 0;
+        if (kMode == MODE_SIM && s < c.p && s < A.stage_stride) {
+          plen = A.len[item * A.stage_stride + s];
+          if (plen > 16 * A.words) {
+            if (!bad) load_status = CPI_BAD_PLAN;           // row longer than its capacity
+          } else {
+            if (plen > 0) word = A.ops[(item * A.words) * A.stage_stride + s];
+            if (plen > 16) nextword = A.ops[(item * A.words + 1) * A.stage_stride + s];
+          }
+        }
+        if (kMode == MODE_GREEDY && !bad && (long long)(2 + c.nsub) * c.m > 16LL * A.words)
+          load_status = CPI_BAD_PLAN;                          // output row capacity too small
+        if (!load_status && (c.p > W || c.m > CP_MAX_MB || c.nsub > CP_MAX_SUB)) load_status = CPI_OVERFLOW;
+        clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = 0;
+        first = busy = pos = comb = last_fd = 0;
+        word = (kMode == MODE_GREEDY) ? 0u : word;
+        ovf = false;
+        best = KEY_NONE;
+        cand = -1;
+        if (kMode == MODE_SWEEP && A.cand_ms && s == 0)
+          for (int cc = 0; cc < 5; ++cc) A.cand_ms[item * 5 + cc] = -1;
+      }
+    }
+    if (__all_sync(FULL, item < 0)) break;
+
+    // ------------------------------------------------------------------ warp-wide post-load
+    if (__any_sync(FULL, just_loaded)) {
+      const bool act = just_loaded && s < c.p && valid_inst;
+      const int cf = act ? c.tf + c.bwF + c.latF : 0;      // hop s -> s+1 (F)
+      const int cd = act ? c.td + c.bwB + c.latB : 0;      // hop s -> s-1 (D)
+      long long u = 0;                                      // horizon bound U (reading Q21)
+      if (act)
+        u = (long long)c.m * ((long long)c.tf + c.td + c.tw) + c.tagate + c.tdp +
+            (long long)c.m * ((long long)c.latF + c.bwF + c.latB + c.bwB);
+      int pf = cf, qd = cd;
+      for (int d = 1; d < W; d <<= 1) {
+        const int a = __shfl_up_sync(FULL, pf, d, W);
+        const int b = __shfl_up_sync(FULL, qd, d, W);
+        if (s >= d) { pf += a; qd += b; }
+      }
+      for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(FULL, u, d, W);
+      const unsigned b_inst = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_INSTANCE);
+      const unsigned b_plan = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_PLAN);
+      const unsigned b_over = __ballot_sync(FULL, just_loaded && load_status == CPI_OVERFLOW);
+      if (just_loaded) {
+        c.P = pf - cf;
+        c.Q = qd;
+        int st = (b_inst & segmask) ? CPI_BAD_INSTANCE
+                 : (b_plan & segmask) ? CPI_BAD_PLAN
+                 : (b_over & segmask) ? CPI_OVERFLOW : 0;
+        if (!st && u >= (long long)INF) st = CPI_OVERFLOW;     // int32 horizon guard
+        load_status = st;
+        if (kMode != MODE_SWEEP && st != 0) {
+          // per-item failure: report now, no evaluation
+          if (s == 0) {
+            A.makespan[item] = -1;
+            if (A.peak_mem) A.peak_mem[item] = -1;
+            A.status[item] = st;
+          }
+          if (A.stage_stats && s < A.stage_stride)
+            *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = make_int4(0, 0, 0, 0);
+          if (kMode == MODE_GREEDY && s < A.stage_stride) A.len[item * A.stage_stride + s] = 0;
+          need_load = true;
+        }
+      }
+    }
+
+    // ------------------------------------------------------------------ sweep: next candidate
+    if (kMode == MODE_SWEEP) {
+      const bool want = item >= 0 && cand < 0 && !need_load;
+      if (__any_sync(FULL, want)) {
+        const int from = -cand - 1;
+        int next = -1;
+        for (int cc = 0; cc < 5; ++cc) {
+          bool ok = true;       // statically memory-feasible / valid candidate on this stage
+          if (s < c.p) {
+            if (cc == 0) ok = (long long)c.m * c.mf <= c.mlim;                          // GPipe peak m*m_f
+            else if (cc == 1) ok = (long long)imin(c.p - s, c.m) * c.mf <= c.mlim;     // 1F1B peak (Z5)
+            else ok = c.tw >= (1 << (cc - 2));                                           // Q12 t_w >= n_sub
+          }
+          const unsigned nb = __ballot_sync(FULL, !ok);
+          if (want && next < 0 && cc >= from && ((A.grid.cand_mask >> cc) & 1u) && !(nb & segmask)) next = cc;
+        }
+        if (want) {
+          if (load_status != 0) {
+            if (s == 0) A.keys[item] = (load_status == CPI_OVERFLOW) ? KEY_OVER : KEY_NONE;
+            need_load = true;
+          } else if (next < 0) {
+            if (s == 0) A.keys[item] = best;
+            need_load = true;
+          } else {
+            cand = next;
+            cand_greedy = next >= 2;
+            c.nsub = cand_greedy ? (1 << (next - 2)) : 1;
+            c.wq = c.tw / c.nsub;
+            c.wr = c.tw % c.nsub;
+            clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = 0;
+            first = busy = pos = comb = last_fd = 0;
+            ovf = false;
+            plen = (s < c.p && !cand_greedy) ? 2 * c.m : 0;
+          }
+        }
+      }
+    }
+
+    // ------------------------------------------------------------------ one round
+    const bool in_round = item >= 0 && !need_load;
+    const bool is_greedy = (kMode == MODE_GREEDY) || (kMode == MODE_SWEEP && cand_greedy);
+    const bool act = in_round && s < c.p;
+    bool fin;
+    if (is_greedy) fin = !act || (nF == c.m && nD == c.m && nW == c.m);
+    else fin = !act || pos >= plen;
+    const bool live = act && !fin;
+
+    const int leftF = __shfl_up_sync(FULL, nF, 1, W);
+    const int rightD = __shfl_down_sync(FULL, nD, 1, W);
+    const int arrF = ringF[((nF & RM) << 5) + lane];
+    const int arrD = ringD[((nD & RM) << 5) + lane];
+    const bool knowF = nF < c.m && (s == 0 || leftF > nF);
+    const int availF = imax(s == 0 ? 0 : arrF, c.tagate);
+    const bool knowD = nD < c.m && (s == c.p - 1 ? nF > nD : rightD > nD);
+    const int availD = (s == c.p - 1) ? 0 : arrD;
+
+    int op = -1, start = 0;
+    bool badp = false;
+    if (kMode != MODE_GREEDY) {
+      if (live && !is_greedy) {
+        uint32_t code;
+        if (kMode == MODE_SIM) code = (word >> ((pos & 15) << 1)) & 3u;
+        else code = static_code(cand, s, c.p, c.m, pos);
+        if (kMode == MODE_SIM) {
+          // reading Q29: counts, W prefix <= n_sub * D, stage all-combined or all-split
+          const int wents = nW * c.nsub + wsub;
+          badp = (code == CP_OP_F && nF >= c.m) || ((code == CP_OP_D || code == CP_OP_B) && nD >= c.m) ||
+                 (code == CP_OP_W && wents >= c.nsub * nD) || (code == CP_OP_B && comb == 2) ||
+                 ((code == CP_OP_D || code == CP_OP_W) && comb == 1);
+        }
+        const bool ready = (code == CP_OP_F) ? knowF : (code == CP_OP_W ? true : knowD);
+        if (!badp && ready) {
+          op = (int)code;
+          start = imax(clk, code == CP_OP_F ? availF : (code == CP_OP_W ? 0 : availD));
+        }
+      }
+    }
+    if (kMode != MODE_SIM) {
+      int tstar = INF;
+      bool hasF = false, hasD = false;
+      if (live && is_greedy) {
+        hasF = knowF && mem + c.mf <= c.mlim;         // Q15: memory-infeasible F is not eligible
+        hasD = knowD;
+        const bool hasW = nW < nD;
+        int mn = INF;
+        if (hasF) mn = availF;
+        if (hasD) mn = imin(mn, availD);
+        if (hasW) mn = imin(mn, clk);                 // W avail = its D end <= clk
+        if (hasF || hasD || hasW) tstar = imax(clk, mn);   // §4.2.2 :419 schedulable time
+      }
+      if (kMode == MODE_GREEDY || __any_sync(FULL, is_greedy && act)) {
+        // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s
+        int x = tstar - c.P, y = tstar + c.Q;
+        for (int d = 1; d < W; d <<= 1) {
+          const int xu = __shfl_up_sync(FULL, x, d, W);
+          const int yd = __shfl_down_sync(FULL, y, d, W);
+          if (s >= d) x = imin(x, xu);
+          if (s + d < W) y = imin(y, yd);
+        }
+        const int xe = __shfl_up_sync(FULL, x, 1, W);
+        const int ye = __shfl_down_sync(FULL, y, 1, W);
+        const int Lh = (s == 0) ? INF : c.P + xe;
+        const int Rh = (s == W - 1) ? INF : ye - c.Q;
+        if (live && is_greedy && tstar < INF && tstar < imin(Lh, Rh)) {
+          // §4.2.2 operation selection (reading Q13): opposite of the last full F/D block,
+          // then the other, then a W sub-block
+          const bool cF = hasF && availF <= tstar, cD = hasD && availD <= tstar;
+          if (last_fd == 1) op = cD ? (int)CP_OP_D : (cF ? (int)CP_OP_F : (int)CP_OP_W);
+          else op = cF ? (int)CP_OP_F : (cD ? (int)CP_OP_D : (int)CP_OP_W);
+          start = tstar;
+        }
+      }
+    }
+    // ------------------------------------------------------------------ execute the chosen block
+    if (op >= 0) {
+      int dur;
+      if (op == (int)CP_OP_F) dur = c.tf;
+      else if (op == (int)CP_OP_D) dur = c.td;
+      else if (op == (int)CP_OP_B) dur = c.td + c.tw;
+      else dur = c.wq + (wsub < c.wr ? 1 : 0);       // Q12 integer sub-block durations
+      const int end = start + dur;
+      if (pos == 0) first = start;
+      busy += dur;
+      clk = end;
+      if (kMode != MODE_SWEEP && A.t_start && pos < A.len_stride)
+        A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
+      if (kMode == MODE_GREEDY) {
+        word |= (uint32_t)op << ((pos & 15) << 1);
+        if ((pos & 15) == 15) {
+          A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = word;
+          word = 0;
+        }
+      }
+      if (op == (int)CP_OP_F) {
+        mem += c.mf;
+        ++nF;
+        last_fd = 1;
+        if (s < c.p - 1) {
+          const int ws = imax(end, linkF);        // FIFO link clock = first fit under UD (App. X1)
+          linkF = ws + c.bwF;
+          ringF[(((nF - 1) & RM) << 5) + lane + 1] = linkF + c.latF;   // T_avail = E_bw + T_lat
+        }
+        if (!kRingGlobal && nF - nD > RM + 1) ovf = true;
+      } else if (op == (int)CP_OP_W) {
+        if (++wsub == c.nsub) { wsub = 0; ++nW; mem += c.mw; }     // W releases at its last sub-block
+        if (kMode == MODE_SIM) comb = 2;
+      } else {
+        mem += (op == (int)CP_OP_D) ? c.md : c.md + c.mw;
+        ++nD;
+        last_fd = 2;
+        if (kMode == MODE_SIM) comb = (op == (int)CP_OP_B) ? 1 : 2;
+        if (s > 0) {
+          const int ws = imax(end, linkB);
+          linkB = ws + c.bwB;
+          ringD[(((nD - 1) & RM) << 5) + lane - 1] = linkB + c.latB;
+        }
+      }
+      peak = imax(peak, mem);
+      ++pos;
+      if (kMode == MODE_SIM && (pos & 15) == 0) {
+        word = nextword;
+        const int kw = (pos >> 4) + 1;
+        nextword = (kw < A.words && kw * 16 < plen) ? A.ops[(item * A.words + kw) * A.stage_stride + s] : 0u;
+      }
+    }
+    __syncwarp();
+
+    // ------------------------------------------------------------------ completion (per segment)
+    bool fin2;
+    if (is_greedy) fin2 = !act || (nF == c.m && nD == c.m && nW == c.m);
+    else fin2 = !act || pos >= plen;
+    const unsigned b_unfin = __ballot_sync(FULL, in_round && !fin2);
+    const unsigned b_prog = __ballot_sync(FULL, op >= 0);
+    const unsigned b_bad = __ballot_sync(FULL, badp);
+    const unsigned b_ovf = __ballot_sync(FULL, ovf);
+    const bool seg_complete = in_round && !(b_unfin & segmask);
+    const bool seg_stuck = in_round && !seg_complete && !(b_prog & segmask);
+    const bool seg_bad = in_round && (b_bad & segmask);
+    const bool seg_ovf = in_round && (b_ovf & segmask);
+    const bool seg_end = seg_complete || seg_stuck || seg_bad || seg_ovf;
+    if (__any_sync(FULL, seg_end)) {
+      bool badc = false;
+      if (kMode == MODE_SIM && seg_complete && act)          // Q29 counts at the end of the walk
+        badc = nF != c.m || nD != c.m || (comb != 1 && nW * c.nsub + wsub != c.nsub * nD);
+      if (kMode == MODE_SIM && seg_stuck && !seg_bad && act) {
+        // cannot complete: a statically bad plan still reports BAD_PLAN -> scan the rest
+        int cF = nF, cD = nD, cW = nW * c.nsub + wsub, cb = comb;
+        for (int k = pos; k < plen && !badc; ++k) {
+          const uint32_t wv = A.ops[(item * A.words + (k >> 4)) * A.stage_stride + s];
+          const uint32_t code = (wv >> ((k & 15) << 1)) & 3u;
+          if (code == CP_OP_F) { badc = cF >= c.m; ++cF; }
+          else if (code == CP_OP_W) { badc = cW >= c.nsub * cD || cb == 1; ++cW; cb = 2; }
+          else { badc = cD >= c.m || (code == CP_OP_B ? cb == 2 : cb == 1); ++cD; cb = (code == CP_OP_B) ? 1 : 2; }
+        }
+        if (!badc) badc = cF != c.m || cD != c.m || (cb != 1 && cW != c.nsub * cD);
+      }
+      const unsigned b_badc = __ballot_sync(FULL, badc);
+      const unsigned b_mem = __ballot_sync(FULL, act && peak > c.mlim);
+      int ms = act ? imax(clk + c.tdp, c.tagate) : 0;   // App. A runtime incl. DP tail / AG
+      int pk = act ? peak : 0;
+      for (int d = 1; d < W; d <<= 1) {
+        ms = imax(ms, __shfl_xor_sync(FULL, ms, d, W));
+        pk = imax(pk, __shfl_xor_sync(FULL, pk, d, W));
+      }
+      if (seg_end) {
+        int st = 0;
+        bool completed = false;
+        if (seg_bad || (b_badc & segmask)) st = CPI_BAD_PLAN;
+        else if (seg_ovf) st = -1;
+        else if (seg_stuck) st = CPI_DEADLOCK;
+        else { completed = true; st = (b_mem & segmask) ? CPI_MEM_EXCEEDED : 0; }
+        if (st == -1) {
+          // an F lead exceeded the ring: the item is re-run by the global-ring fix-up pass
+          if (kMode == MODE_SWEEP) {
+            if (s == 0) A.keys[item] = KEY_OVER;                     // host sizes R so this never happens
+            need_load = true;
+          } else {
+            if (s == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
+            need_load = true;
+          }
+        } else if (kMode == MODE_SWEEP) {
+          const bool feas = completed && st == 0;
+          if (A.cand_ms && s == 0) A.cand_ms[item * 5 + cand] = feas ? ms : -1;
+          const unsigned long long key = feas ? (((unsigned long long)ms << 8) | (unsigned)cand) : KEY_NONE;
+          best = key < best ? key : best;
+          cand = -(cand + 2);                  // advance to the first candidate > cand
+          cand_greedy = false;
+        } else {
+          if (s == 0) {
+            A.makespan[item] = completed ? (long long)ms : -1LL;
+            if (A.peak_mem) A.peak_mem[item] = completed ? pk : -1;
+            A.status[item] = st;
+            if (A.best_key && st == 0)
+              atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
+          }
+          if (A.stage_stats && s < A.stage_stride) {
+            const int4 v = (completed && act) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
+            *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = v;
+          }
+          if (kMode == MODE_GREEDY && s < A.stage_stride) {
+            if (act && (pos & 15)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = word;
+            A.len[item * A.stage_stride + s] = (uint16_t)(act ? pos : 0);
+            word = 0;
+          }
+          need_load = true;
+        }
+      }
+    }
+  }
+}
+
+template <int kMode, bool kRG>
+static void* kernel_ptr() { return (void*)k_engine<kMode, kRG>; }
+
+static void* pick(Mode mode, bool rg) {
+  switch (mode) {
+    case MODE_SIM: return rg ? kernel_ptr<MODE_SIM, true>() : kernel_ptr<MODE_SIM, false>();
+    case MODE_GREEDY: return rg ? kernel_ptr<MODE_GREEDY, true>() : kernel_ptr<MODE_GREEDY, false>();
+    default: return rg ? kernel_ptr<MODE_SWEEP, true>() : kernel_ptr<MODE_SWEEP, false>();
+  }
+}
+
+int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int threads, size_t smem, void* stream) {
+  void* fn = pick(mode, ring_global);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  void* params[] = {(void*)&a};
+  cudaError_t e = cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
+  return (int)e;
+}
+
+int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem) {
+  void* fn = pick(mode, ring_global);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;
+  return n > 0 ? n : 1;
+}
+
+int device_sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return n;
+}
+
+}  // namespace cpk

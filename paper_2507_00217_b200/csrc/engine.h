@@ -1,0 +1,57 @@
+// engine.h -- internal interface between the C-ABI host layer (abi.cpp) and the
+// sm_100a kernels (engine.cu).  Not part of the public ABI (see include/crosspipe.h).
+#pragma once
+#include <stddef.h>
+#include <stdint.h>
+
+#include "crosspipe.h"
+
+namespace cpk {
+
+enum Mode : int32_t { MODE_SIM = 0, MODE_GREEDY = 1, MODE_SWEEP = 2 };
+
+// Kernel arguments, passed by value (__grid_constant__) -- the sweep grid rides along
+// in the kernel parameter space, so a sweep launch needs no host->device copy.
+struct Args {
+  // instances (SIM / GREEDY)
+  const cp_inst_v1* inst;
+  const int32_t* inst_of;
+  int32_t n_inst;
+  int32_t n_items;
+  // lane geometry
+  int32_t seg_lg;          // segment width W = 1 << seg_lg (>= p of every item)
+  int32_t ring_lg;         // arrival-ring slots R = 1 << ring_lg
+  int32_t* ring_g;         // global rings (ring_global launches): [warps][2][R][32]
+  // plans
+  uint32_t* ops;
+  uint16_t* len;
+  int32_t stage_stride;
+  int32_t words;
+  // results
+  int64_t* makespan;
+  int32_t* peak_mem;
+  int32_t* status;
+  int32_t* stage_stats;
+  int32_t* t_start;
+  int32_t len_stride;
+  int32_t from_list;       // items come from the overflow list (fix-up pass)
+  unsigned long long* best_key;
+  // overflow list (items whose lead exceeded R in the fast pass)
+  int32_t* ovf_count;
+  int32_t* ovf_list;
+  // sweep
+  int64_t pt_lo, pt_hi;
+  unsigned long long* keys;
+  int32_t* cand_ms;
+  cp_grid grid;
+};
+
+// launchers (return cudaError_t as int)
+int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int threads, size_t smem, void* stream);
+int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem);
+int device_sm_count();
+
+constexpr int kThreads = 128;          // 4 warps per block
+constexpr int kFixWarps = 148 * 4;     // warps of a global-ring (fix-up) launch
+
+}  // namespace cpk

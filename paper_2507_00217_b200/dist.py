@@ -1,0 +1,43 @@
+"""Multi-GPU sharding (one process per GPU, torch.distributed over NCCL).
+
+The hot path partitions naturally (independent grid points / schedules), so ranks
+share no data until the single final exchange: one all_reduce(MIN) over int64
+packed keys, which is an allgather + argmin in one collective.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import api
+
+
+def world():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def sweep(grid, *, cand=False, group=None, stream=None, bounds=None):
+    """cp_sweep(grid) = cost-balanced shard on every rank + all_reduce(MIN) of the keys.
+    Returns (keys [n_points] int64 on every rank, cand_ms of the local shard or None)."""
+    rank, ws = world()
+    cg = api.to_cp_grid(grid)
+    if bounds is None:
+        bounds = api.sweep_partition(grid, ws, cgrid=cg)
+    keys, cm = api.sweep_shard(grid, bounds[rank], bounds[rank + 1], cand=cand, stream=stream, cgrid=cg)
+    if ws > 1:
+        dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
+    return keys, cm
+
+
+def shard_range(n: int, rank: int, ws: int):
+    """Contiguous equal split of n uniform-cost items (schedules / instances)."""
+    return n * rank // ws, n * (rank + 1) // ws
+
+
+def best_schedule(best_key: torch.Tensor, group=None):
+    """all_reduce(MIN) of the (makespan << 32 | index) key of each rank's best schedule."""
+    if world()[1] > 1:
+        dist.all_reduce(best_key, op=dist.ReduceOp.MIN, group=group)
+    return best_key

@@ -1,0 +1,131 @@
+"""CPU-side checks of the product boundary (no GPU compute): the C-ABI library loads and
+exports every symbol include/crosspipe.h declares; host entry points (quantizer, validator,
+sweep partition) agree with the oracle / their definitions; format conversions round-trip."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2507_00217_b200 as cp
+from paper_2507_00217_b200 import _lib as L
+from workloads import configs as K, pack_plans, unpack_plans
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    syms = set()
+    for fn in os.listdir(os.path.join(ROOT, "include")):
+        if fn.endswith(".h"):
+            txt = open(os.path.join(ROOT, "include", fn)).read()
+            syms |= set(re.findall(r"^\s*(?:[A-Za-z_][\w\s\*]*?)\b(cp_\w+)\s*\(", txt, flags=re.M))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    syms = declared_symbols()
+    assert {"cp_simulate", "cp_greedy", "cp_sweep_shard", "cp_quantize"} <= syms
+    lib = C.CDLL(L.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(L.EXPORTS) == syms
+
+
+def test_abi_version_and_strings():
+    lib = L.load()
+    assert lib.cp_abi_version() == 1
+    assert b"workspace" in lib.cp_status_string(-4)
+    assert b"deadlock" in lib.cp_status_string(1)
+
+
+def test_record_layout():
+    assert L.INST_DTYPE.itemsize == 1792
+    assert C.sizeof(L.CpInstances) == 24 and C.sizeof(L.CpSchedules) == 40 and C.sizeof(L.CpResults) == 56
+    assert L.INST_DTYPE.fields["t_f"][1] == 32 and L.INST_DTYPE.fields["bw_b"][1] == 32 + 12 * 128
+
+
+def test_validator_matches_oracle(oracle_lib):
+    """cp_validate_instance (host) flags BAD_INSTANCE exactly when the oracle's validator does."""
+    rng = np.random.default_rng(3)
+    batch = K.random_instances(300, seed=4, max_p=8, max_m=6)
+    for i in range(len(batch)):
+        if rng.random() < 0.7:
+            k = int(rng.integers(7)); s = int(rng.integers(batch.p[i]))
+            fld = ["t_f", "t_d", "t_w", "m_f", "m_d", "m_lim", "t_ag"][k]
+            getattr(batch, fld)[i, s] += int(rng.integers(-3, 2))
+    recs = cp.pack_instances(batch)
+    for i in range(len(batch)):
+        st, msg = cp.validate_record(recs[i:i + 1])
+        want = oracle_lib.lib().or_validate_instance(C.byref(oracle_lib.to_or_inst(batch.item(i))))
+        assert (st == 8) == (want == 8), (i, st, want, msg)
+        if st == 8:
+            assert msg
+
+
+def test_quantizer_matches_oracle(oracle_lib):
+    """cp_quantize (product, C++) and or_quantize (oracle, C) agree bit for bit on random SI specs
+    (same double arithmetic, llround half away from zero; reading Q21)."""
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        p = int(rng.integers(1, 9)); n_dc = int(rng.integers(1, 5))
+        dc = sorted(int(x) for x in rng.integers(0, n_dc, size=p))
+        spec = {"p": p, "m": int(rng.integers(1, 40)), "n_sub": int(rng.integers(1, 4)), "zero1": int(rng.integers(2)),
+                "n_dc": n_dc, "dc_of_stage": dc,
+                "t_f": rng.uniform(1e-4, 0.1, p), "t_d": rng.uniform(1e-4, 0.1, p), "t_w": rng.uniform(1e-4, 0.1, p),
+                "m_f": [2e9] * p, "m_d": [-1e9] * p, "m_w": [-1e9] * p, "m_lim": rng.uniform(2e9, 4e10, p),
+                "t_dp": rng.uniform(0, 0.2, p), "t_ag": rng.uniform(0, 0.1, p),
+                "alpha": rng.uniform(0, 0.1, (4, 4)).tolist(), "beta": (8 / (rng.uniform(1, 800, (4, 4)) * 1e9)).tolist(),
+                "msg_f": [1e9] * p, "msg_b": [1e9] * p, "tick_s": 1e-6, "mem_unit": 1e9}
+        st, rec = cp.quantize(spec)
+        o = oracle_lib.quantize(spec)
+        assert (st == 8) == (o["status"] == 8)
+        if st == 0:
+            for k in ("t_f", "t_d", "t_w", "m_f", "m_d", "m_w", "m_lim", "t_dp", "t_ag"):
+                assert np.array_equal(rec[k][0, :p], o[k]), k
+            for k in ("lat_f", "bw_f", "lat_b", "bw_b"):
+                assert np.array_equal(rec[k][0, :p - 1], o[k]), k
+
+
+def test_sweep_partition_balances_cost():
+    """cp_sweep_partition cuts at equal prefix sums of p*m*sum(2+n_sub)."""
+    g = K.full_sweep_grid()
+    for world in (1, 2, 3, 4, 8):
+        b = cp.sweep_partition(g, world)
+        assert b[0] == 0 and b[-1] == g.n_points and all(x <= y for x, y in zip(b, b[1:]))
+        i_pp, i_mb, *_ = g.point_axes(np.arange(g.n_points))
+        cost = np.array(g.pp_vals)[i_pp] * np.array(g.mb_vals)[i_mb] * 17
+        shares = [cost[b[r]:b[r + 1]].sum() for r in range(world)]
+        assert max(shares) - min(shares) <= cost.max() + 1, (world, shares)
+
+
+def test_pack_unpack_roundtrip():
+    rng = np.random.default_rng(6)
+    codes = rng.integers(0, 4, size=(5, 7, 50)).astype(np.int8)
+    lens = rng.integers(0, 51, size=(5, 7)).astype(np.int32)
+    ops, ln = pack_plans(codes, lens, stage_stride=8)
+    c2, l2 = unpack_plans(ops, ln, p=7)
+    assert np.array_equal(l2, lens)
+    for i in range(5):
+        for s in range(7):
+            assert np.array_equal(c2[i, s, :lens[i, s]], codes[i, s, :lens[i, s]])
+
+
+def test_product_has_no_oracle_dependency():
+    """The product never imports / links the oracle (independence)."""
+    pkg = os.path.join(ROOT, "paper_2507_00217_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cpp", ".h", ".cuh", "Makefile")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert "oracle" not in txt.replace("no CPU fallback", ""), fn
+    assert b"or_simulate" not in open(L.LIB_PATH, "rb").read()
+
+
+def test_compute_entry_points_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(RuntimeError):
+        cp.sweep_shard(K.gpt16_grid())

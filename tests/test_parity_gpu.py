@@ -1,0 +1,321 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Bar: bit-exact on every integer output -- status, makespan, peak memory,
+per-stage stats, the full start-tick timeline, and greedy schedules byte for byte.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+import paper_2507_00217_b200 as cp  # noqa: E402
+from tests.gpu_util import codes_list_to_packed, compare_sim, plans_to_device, to_host  # noqa: E402
+from tests.helpers_independent import random_valid_plan  # noqa: E402
+from workloads import InstanceBatch, configs as K, pack_plans, plans as PL, unpack_plans  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def O():
+    from oracle import oracle
+    oracle.build()
+    return oracle
+
+
+def run_sim(batch, ops, ln, inst_of=None, stats=True, timeline=True, ring=None):
+    inst = cp.Instances(batch)
+    o, l_ = plans_to_device(ops, ln)
+    io = torch.from_numpy(np.asarray(inst_of, dtype=np.int32)).cuda() if inst_of is not None else None
+    r = cp.simulate(inst, o, l_, io, stats=stats, timeline=timeline, ring=ring)
+    torch.cuda.synchronize()
+    return to_host(r)
+
+
+# ------------------------------------------------------------------------------------- simulate
+@pytest.mark.parametrize("max_p,seed", [(32, 1), (8, 2), (4, 3), (16, 4)])
+def test_simulate_random_valid_plans(O, max_p, seed):
+    """Random instances (1..max_p stages, 1..24 mb, 1-4 DCs, n_sub 1-4, DP, ZeRO-1) x 4 random
+    valid plans each; several lane segments per warp when max_p <= 16; full timelines compared."""
+    batch = K.random_instances(120, seed=seed, max_p=max_p, max_m=24)
+    plans, inst_of = [], []
+    for i in range(len(batch)):
+        ops, ln = PL.plans_host(batch, 4, seed=seed * 1000 + i, i=i, q=int(i % 5), stride=32)
+        c, l_ = unpack_plans(ops, ln)
+        for k in range(4):
+            plans.append([list(c[k, s, :l_[k, s]]) for s in range(int(batch.p[i]))])
+            inst_of.append(i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(batch, ops, ln, inst_of)
+    codes, lens = unpack_plans(ops, ln)
+    for j, i in enumerate(inst_of):
+        compare_sim(O, batch.item(i), codes[j], lens[j], r, j, codes.shape[2])
+    assert np.all(r["status"] == 0)
+
+
+def test_simulate_static_plans_and_overflow_path(O):
+    """1F1B and GPipe (combined B) on random instances; GPipe exceeds the memory budget, which
+    also drives the lead past the shared-memory ring -> global-ring fix-up pass must agree."""
+    batch = K.random_instances(100, seed=5, max_p=32, max_m=30)
+    plans, inst_of = [], []
+    for i in range(len(batch)):
+        p, m = int(batch.p[i]), int(batch.m[i])
+        for kind in ("1f1b", "gpipe"):
+            c, l_ = O.build_static(kind, p, m)
+            plans.append([list(c[s, :l_[s]]) for s in range(p)])
+            inst_of.append(i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(batch, ops, ln, inst_of)
+    codes, lens = unpack_plans(ops, ln)
+    for j, i in enumerate(inst_of):
+        compare_sim(O, batch.item(i), codes[j], lens[j], r, j, codes.shape[2])
+    assert np.any(r["status"] == 2)          # memory-exceeded items present
+
+
+def test_simulate_invalid_plans(O):
+    """Deadlocks (adjacent swaps), BAD_PLAN (missing/extra entries, W before D, B mixed with
+    D/W), memory violations (budget cut after generation) -- status precedence included."""
+    rng = np.random.default_rng(6)
+    batch = K.random_instances(150, seed=7, max_p=12, max_m=10)
+    plans, inst_of, mlim_cut = [], [], []
+    for i in range(len(batch)):
+        d = batch.item(i)
+        base = random_valid_plan(d, rng)
+        for kind in range(5):
+            pl = [list(x) for x in base]
+            s = int(rng.integers(d["p"]))
+            if kind == 0 and len(pl[s]) > 1:                      # swap -> often deadlock
+                k = int(rng.integers(len(pl[s]) - 1)); pl[s][k], pl[s][k + 1] = pl[s][k + 1], pl[s][k]
+            elif kind == 1:                                        # drop an entry
+                pl[s].pop(int(rng.integers(len(pl[s]))))
+            elif kind == 2:                                        # extra F
+                pl[s].insert(int(rng.integers(len(pl[s]) + 1)), 0)
+            elif kind == 3:                                        # mix a B into a split stage
+                pl[s][int(rng.integers(len(pl[s])))] = 1
+            elif kind == 4:                                        # several random swaps
+                for _ in range(3):
+                    s2 = int(rng.integers(d["p"]))
+                    if len(pl[s2]) > 1:
+                        k = int(rng.integers(len(pl[s2]) - 1)); pl[s2][k], pl[s2][k + 1] = pl[s2][k + 1], pl[s2][k]
+            plans.append(pl)
+            inst_of.append(i)
+    # memory-violating but valid plans: same plan, instance with a halved budget
+    cut = InstanceBatch.concat([batch, batch.take(np.arange(len(batch)))])
+    n0 = len(batch)
+    cut.m_lim[n0:] = np.maximum(cut.m_f[n0:], cut.m_lim[n0:] // 3)
+    for i in range(n0):
+        plans.append(random_valid_plan(batch.item(i), rng))
+        inst_of.append(n0 + i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(cut, ops, ln, inst_of)
+    codes, lens = unpack_plans(ops, ln)
+    seen = set()
+    for j, i in enumerate(inst_of):
+        w = compare_sim(O, cut.item(i), codes[j], lens[j], r, j, codes.shape[2])
+        seen.add(w["status"])
+    assert {0, 1, 2, 4} <= seen, seen
+
+
+def test_simulate_edge_cases(O):
+    """p = 1, m = 1, n_sub = 16, zero delays everywhere, p = 32 with one huge-bandwidth
+    boundary, ZeRO-1 gate later than the pipeline start."""
+    parts = [
+        K.uniform_instance(1, 1, 1, 3, 4, 5),
+        K.uniform_instance(1, 7, 1, 3, 4, 5, mlim_x1000=7000),
+        K.uniform_instance(2, 1, 2, 1, 1, 1, lat=0, bw=0),
+        K.uniform_instance(32, 40, 4, 7, 9, 16, lat=500, bw=300, n_sub=16, mlim_x1000=2000),
+        K.uniform_instance(32, 3, 2, 5, 5, 5, lat=0, bw=100000, mlim_x1000=1000),
+        K.uniform_instance(6, 9, 3, 11, 13, 17, lat=40, bw=25, t_dp=333, zero1=1, t_ag=1000),
+    ]
+    batch = InstanceBatch.concat(parts)
+    plans, inst_of = [], []
+    for i in range(len(batch)):
+        ops, ln = PL.plans_host(batch, 3, seed=99 + i, i=i, stride=32)
+        c, l_ = unpack_plans(ops, ln)
+        for k in range(3):
+            plans.append([list(c[k, s, :l_[k, s]]) for s in range(int(batch.p[i]))])
+            inst_of.append(i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(batch, ops, ln, inst_of)
+    codes, lens = unpack_plans(ops, ln)
+    for j, i in enumerate(inst_of):
+        compare_sim(O, batch.item(i), codes[j], lens[j], r, j, codes.shape[2])
+
+
+def test_bad_instances_and_overflow_guard(O):
+    """Invalid records -> CPI_BAD_INSTANCE exactly when the oracle says so; a valid record
+    whose horizon bound U >= 2^30 -> CPI_OVERFLOW (GPU int32 guard, reading Q21)."""
+    batch = K.random_instances(60, seed=8, max_p=8, max_m=6)
+    rng = np.random.default_rng(9)
+    for i in range(len(batch)):
+        k = int(rng.integers(6))
+        s = int(rng.integers(batch.p[i]))
+        if k == 0: batch.t_f[i, s] = 0
+        elif k == 1: batch.m_w[i, s] -= 1
+        elif k == 2: batch.m_lim[i, s] = batch.m_f[i, s] - 1
+        elif k == 3: batch.t_w[i, s] = batch.n_sub[i] - 1 if batch.n_sub[i] > 1 else 0
+        elif k == 4 and batch.p[i] > 1: batch.lat_b[i, 0] = -1
+        elif k == 5: batch.t_dp[i, s] = -5
+    big = K.uniform_instance(4, 8, 2, 10**8, 10**8, 10**8)       # U = 9.6e9 >= 2^30
+    batch = InstanceBatch.concat([batch, big])
+    plans, inst_of = [], []
+    for i in range(len(batch)):
+        c, l_ = O.build_static("1f1b", int(batch.p[i]), int(batch.m[i]))
+        plans.append([list(c[s, :l_[s]]) for s in range(int(batch.p[i]))])
+        inst_of.append(i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(batch, ops, ln, inst_of)
+    codes, lens = unpack_plans(ops, ln)
+    for j, i in enumerate(inst_of[:-1]):
+        w = O.simulate(batch.item(i), codes[j][:int(batch.p[i])], lens[j][:int(batch.p[i])])
+        assert int(r["status"][j]) == w["status"], (j, int(r["status"][j]), w["status"])
+    assert int(r["status"][-1]) == 16 and int(r["makespan"][-1]) == -1
+
+
+def test_simulate_deterministic_and_ring_sizes(O):
+    """Identical results for every arrival-ring size (fast path vs fix-up) and across runs."""
+    batch = K.random_instances(40, seed=10, max_p=16, max_m=20)
+    plans, inst_of = [], []
+    for i in range(len(batch)):
+        ops, ln = PL.plans_host(batch, 2, seed=5 + i, i=i, stride=16)
+        c, l_ = unpack_plans(ops, ln)
+        for k in range(2):
+            plans.append([list(c[k, s, :l_[k, s]]) for s in range(int(batch.p[i]))])
+            inst_of.append(i)
+    ops, ln = codes_list_to_packed(plans, stride=16)
+    ref = run_sim(batch, ops, ln, inst_of)
+    for ring in (1, 2, 4, 64):
+        r = run_sim(batch, ops, ln, inst_of, ring=ring)
+        for k in ("makespan", "status", "peak_mem", "stage_stats", "t_start"):
+            assert np.array_equal(r[k], ref[k]), (ring, k)
+
+
+# ------------------------------------------------------------------------------------- greedy
+def check_greedy(O, batch, g, idx):
+    gc, gl = unpack_plans(g["ops"].view(np.uint32), g["len"].view(np.uint16))
+    for i in idx:
+        d = batch.item(i)
+        w = O.greedy(d, timeline=True)
+        p = d["p"]
+        assert int(g["status"][i]) == w["status"], (i, int(g["status"][i]), w["status"])
+        assert int(g["makespan"][i]) == w["makespan"], (i, int(g["makespan"][i]), w["makespan"])
+        assert int(g["peak_mem"][i]) == w["peak_mem"], i
+        assert np.array_equal(gl[i, :p], w["len"]), i
+        L = int(w["len"][0])
+        assert np.array_equal(gc[i, :p, :L], w["codes"][:, :L]), f"schedule differs at item {i}"
+        if "stage_stats" in g:
+            ss = g["stage_stats"][i]
+            assert np.array_equal(ss[:p, 0], w["first_start"]) and np.array_equal(ss[:p, 1], w["last_end"])
+            assert np.array_equal(ss[:p, 2], w["busy"]) and np.array_equal(ss[:p, 3], w["peak"])
+        if "t_start" in g:
+            assert np.array_equal(g["t_start"][i][:p, :L], w["t_start"][:, :L]), i
+
+
+@pytest.mark.parametrize("max_p,seed", [(32, 11), (8, 12), (16, 13), (2, 14)])
+def test_greedy_random_instances(O, max_p, seed):
+    """Round-parallel greedy (two min-plus warp scans) == sequential Alg. 1, byte for byte."""
+    batch = K.random_instances(300, seed=seed, max_p=max_p, max_m=20, intra_delay=True)
+    inst = cp.Instances(batch)
+    g = to_host(cp.greedy(inst, stats=True, timeline=True))
+    check_greedy(O, batch, g, range(len(batch)))
+
+
+def test_greedy_config3_sample(O):
+    """Config 3 (1e5 instances; memory limit, DP overlap, ZeRO-1, n_sub, jitter): a 3000-instance
+    slice end to end, every instance checked."""
+    batch = K.greedy_batch(3000)
+    inst = cp.Instances(batch)
+    g = to_host(cp.greedy(inst, stats=True))
+    check_greedy(O, batch, g, range(len(batch)))
+
+
+def test_greedy_plans_resimulate(O):
+    """Consistency: cp_simulate on cp_greedy's output reproduces its timeline."""
+    batch = K.random_instances(100, seed=15, max_p=32, max_m=16)
+    inst = cp.Instances(batch)
+    g = cp.greedy(inst, stats=True, timeline=True)
+    r = cp.simulate(inst, g["ops"], g["len"], stats=True, timeline=True, len_stride=g["t_start"].shape[2])
+    torch.cuda.synchronize()
+    for k in ("makespan", "status", "peak_mem", "stage_stats", "t_start"):
+        assert torch.equal(r[k], g[k]), k
+
+
+# ------------------------------------------------------------------------------------- sweep
+def check_sweep(O, grid, keys, cm, pts):
+    G, keep = O.to_or_grid(grid)
+    for k in pts:
+        key, cms = O.sweep_point(grid, int(k), G=G)
+        want_key = cp.KEY_NONE if key == 2**64 - 1 else key
+        assert int(keys[k]) == want_key, (k, int(keys[k]), want_key)
+        assert list(cm[k]) == cms, (k, list(cm[k]), cms)
+
+
+def test_sweep_tiny_grid(O):
+    """Config 1 grid {0,.5,1,2}^2 with all 5 candidates, every point."""
+    from workloads.core import Grid
+    base = K.tiny(0, 0)
+    r = [0, 50, 100, 200]
+    grid = Grid(base=base, n_dc=2, pp_vals=[4], mb_vals=[8], lat=np.array(r), bw=np.array(r),
+                mlim_x1000=np.array([1000, 2000]), tdp=np.array([0, 150]), cand_mask=0b11111)
+    keys, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
+
+
+def test_sweep_config2_sample(O):
+    """Config 2 (16 stages / 2 DCs / 32 mb, 64 x 64 latency x bandwidth): 300 sampled points,
+    each checked candidate by candidate."""
+    grid = K.gpt16_grid()
+    keys, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    pts = np.random.default_rng(16).choice(grid.n_points, 300, replace=False)
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), pts)
+
+
+def test_sweep_config5_sample_and_shards(O):
+    """Config 5 (4 DCs, p 8-32, m 8-128, memory grid): sampled points; shards over 1/2/4/8
+    cost-balanced ranges assembled with MIN give byte-identical keys."""
+    grid = K.full_sweep_grid()
+    full, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    full_h = full.cpu().numpy()
+    rng = np.random.default_rng(17)
+    pts = np.concatenate([rng.choice(grid.n_points, 120, replace=False)])
+    check_sweep(O, grid, full_h, cm.cpu().numpy(), pts)
+    for world in (2, 4, 8):
+        b = cp.sweep_partition(grid, world)
+        acc = torch.full((grid.n_points,), cp.KEY_NONE, dtype=torch.int64, device="cuda")
+        for rk in range(world):
+            kr, _ = cp.sweep_shard(grid, b[rk], b[rk + 1])
+            acc = torch.minimum(acc, kr)
+        assert torch.equal(acc.cpu(), torch.from_numpy(full_h)), world
+
+
+# ------------------------------------------------------------------------------------- config 4 at full size
+def test_config4_full_size_sampled(O):
+    """Config 4 at BASELINE size (1e6 perturbed valid schedules, p=32, 4 DCs, m=64) in the bench
+    launch configuration; 400 sampled schedules checked against the oracle, the GPU generator
+    checked against the host generator, and the argmin key checked for consistency."""
+    b = K.perturbed_instance()
+    n = 1_000_000
+    ops, ln = PL.plans_device(b, n, seed=K.PERTURB_SEED)
+    inst = cp.Instances(b)
+    r = cp.simulate(inst, ops, ln, best=True)
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(18).choice(n, 400, replace=False)
+    h_ops, h_ln = PL.plans_host(b, 1, seed=K.PERTURB_SEED, id0=int(idx[0]))
+    assert np.array_equal(ops[int(idx[0])].cpu().numpy().view(np.uint32), h_ops[0])
+    ms = r["makespan"].cpu().numpy()
+    st = r["status"].cpu().numpy()
+    assert np.all(st == 0)
+    sub_ops = ops[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint32)
+    sub_ln = ln[torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint16)
+    codes, lens = unpack_plans(sub_ops, sub_ln)
+    d = b.item(0)
+    for j, i in enumerate(idx):
+        w = O.simulate(d, codes[j], lens[j])
+        assert (int(ms[i]), int(st[i])) == (w["makespan"], w["status"]), i
+    bk = int(r["best_key"][0])
+    assert (bk >> 32) == ms.min() and ms[bk & 0xFFFFFFFF] == ms.min()

@@ -1,0 +1,114 @@
+// gen.cu -- seeded generator of random VALID plans (workloads module; input generation only).
+//
+// Holds none of the method's arithmetic: no times, no link model, no greedy rule.  A plan
+// is produced by a round-synchronous token game over the combinatorial dependency
+// structure of the UD pattern (F_j on s needs F_j produced on s-1; D_j on s needs D_j
+// produced on s+1, or F_j on the last stage; W sub-blocks of microbatch j need D_j) plus a
+// per-stage counter of activations held (F adds m_f, D adds m_d, a W block's last sub-block
+// adds m_w) that must stay <= m_lim.  Each round every stage appends at most one executable
+// op: with probability q/4 a uniformly random one, else by the fixed preference D > F > W.
+// Randomness is counter-based: u = splitmix64(seed ^ splitmix64(id ^ (s << 40) ^ (round << 8))),
+// so the host and device versions (same source) produce identical plans.
+// Output: the documented 2-bit plan format (word-major, stage-minor).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define GEN_MAXP 32
+
+__host__ __device__ static inline uint64_t gen_mix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// returns 0 on success, 1 if the token game got stuck (never observed), 2 on bad args
+__host__ __device__ static int gen_plan(int p, int m, int nsub, const int32_t* mf, const int32_t* md,
+                                        const int32_t* mw, const int32_t* mlim, uint64_t seed, uint64_t id,
+                                        int q, uint32_t* ops, uint16_t* len, int words, int stride) {
+  if (p < 1 || p > GEN_MAXP || m < 1 || nsub < 1 || (2 + nsub) * m > 16 * words) return 2;
+  int nF[GEN_MAXP], nD[GEN_MAXP], nW[GEN_MAXP], mem[GEN_MAXP], prevF[GEN_MAXP], prevD[GEN_MAXP];
+  uint32_t cur[GEN_MAXP];
+  for (int s = 0; s < p; ++s) { nF[s] = nD[s] = nW[s] = mem[s] = 0; cur[s] = 0; }
+  const int total = (2 + nsub) * m;
+  for (uint64_t r = 0;; ++r) {
+    for (int s = 0; s < p; ++s) { prevF[s] = nF[s]; prevD[s] = nD[s]; }
+    bool progress = false, done = true;
+    for (int s = 0; s < p; ++s) {
+      const int k = nF[s] + nD[s] + nW[s];
+      if (k == total) continue;
+      done = false;
+      const bool canF = nF[s] < m && (s == 0 || prevF[s - 1] > nF[s]) && mem[s] + mf[s] <= mlim[s];
+      const bool canD = nD[s] < m && (s == p - 1 ? nF[s] > nD[s] : prevD[s + 1] > nD[s]);
+      const bool canW = nW[s] < nsub * nD[s];
+      const int nx = (int)canF + (int)canD + (int)canW;
+      if (nx == 0) continue;
+      const uint64_t u = gen_mix(seed ^ gen_mix(id ^ ((uint64_t)s << 40) ^ (r << 8)));
+      int code;
+      if ((int)(u & 3u) < q) {
+        int pick = (int)((u >> 8) % (uint64_t)nx);
+        code = -1;
+        if (canF) { if (pick == 0) code = 0; --pick; }
+        if (code < 0 && canD) { if (pick == 0) code = 2; --pick; }
+        if (code < 0) code = 3;
+      } else {
+        code = canD ? 2 : (canF ? 0 : 3);
+      }
+      if (code == 0) { nF[s]++; mem[s] += mf[s]; }
+      else if (code == 2) { nD[s]++; mem[s] += md[s]; }
+      else { nW[s]++; if (nW[s] % nsub == 0) mem[s] += mw[s]; }
+      cur[s] |= (uint32_t)code << ((k & 15) * 2);
+      if ((k & 15) == 15 || k + 1 == total) { ops[(k >> 4) * stride + s] = cur[s]; cur[s] = 0; }
+      progress = true;
+    }
+    if (done) break;
+    if (!progress) return 1;
+  }
+  for (int s = 0; s < p; ++s) len[s] = (uint16_t)total;
+  return 0;
+}
+
+struct GenArgs {
+  int p, m, nsub, q, words, stride;
+  int32_t mf[GEN_MAXP], md[GEN_MAXP], mw[GEN_MAXP], mlim[GEN_MAXP];
+  uint64_t seed, id0;
+  long long n;
+};
+
+__global__ void k_gen(const __grid_constant__ GenArgs a, uint32_t* ops, uint16_t* len, int32_t* err) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.n) return;
+  const int e = gen_plan(a.p, a.m, a.nsub, a.mf, a.md, a.mw, a.mlim, a.seed, a.id0 + (uint64_t)i, a.q,
+                         ops + i * (long long)a.words * a.stride, len + i * (long long)a.stride, a.words, a.stride);
+  if (e) atomicAdd(err, 1);
+}
+
+extern "C" {
+
+// host: plans for ids id0 .. id0+n-1; returns number of failures
+int cpgen_plans_host(int p, int m, int nsub, const int32_t* mf, const int32_t* md, const int32_t* mw,
+                     const int32_t* mlim, uint64_t seed, uint64_t id0, int q, long long n, uint32_t* ops,
+                     uint16_t* len, int words, int stride) {
+  int err = 0;
+  for (long long i = 0; i < n; ++i)
+    err += gen_plan(p, m, nsub, mf, md, mw, mlim, seed, id0 + (uint64_t)i, q, ops + i * (long long)words * stride,
+                    len + i * (long long)stride, words, stride) != 0;
+  return err;
+}
+
+// device: same plans into device buffers (err: device int32, caller-zeroed)
+int cpgen_plans_device(int p, int m, int nsub, const int32_t* mf, const int32_t* md, const int32_t* mw,
+                       const int32_t* mlim, uint64_t seed, uint64_t id0, int q, long long n, uint32_t* ops,
+                       uint16_t* len, int words, int stride, int32_t* err, void* stream) {
+  GenArgs a;
+  a.p = p; a.m = m; a.nsub = nsub; a.q = q; a.words = words; a.stride = stride;
+  for (int s = 0; s < GEN_MAXP; ++s) {
+    a.mf[s] = s < p ? mf[s] : 0; a.md[s] = s < p ? md[s] : 0; a.mw[s] = s < p ? mw[s] : 0; a.mlim[s] = s < p ? mlim[s] : 0;
+  }
+  a.seed = seed; a.id0 = id0; a.n = n;
+  const int threads = 128;
+  const long long blocks = (n + threads - 1) / threads;
+  k_gen<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(a, ops, len, err);
+  return (int)cudaGetLastError();
+}
+}
