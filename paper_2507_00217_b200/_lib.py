@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcrosspipe.so")
+LIB_PATH = os.environ.get("CROSSPIPE_LIB") or os.path.join(_HERE, "libcrosspipe.so")   # override: debug build
 
 CP_OK, CP_EINVAL, CP_EUNSUPPORTED, CP_ECUDA, CP_EWORKSPACE = 0, -1, -2, -3, -4
 CPI_DEADLOCK, CPI_MEM_EXCEEDED, CPI_BAD_PLAN, CPI_BAD_INSTANCE, CPI_OVERFLOW = 1, 2, 4, 8, 16

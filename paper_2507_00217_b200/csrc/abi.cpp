@@ -13,7 +13,6 @@
 #include "crosspipe.h"
 #include "engine.h"
 
-using cpk::Args;
 
 namespace {
 
@@ -30,19 +29,29 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Ring slots needed by items: min(n_mb, in-flight F bound); the memory argument
 // bounds every producer->consumer lead by floor(m_lim/m_f).
-int ring_lg_for(const cp_instances* in) {
+int ring_slots_for(const cp_instances* in) {
   long long r = in->ring_hint > 0 ? in->ring_hint : in->max_mb;
-  r = std::max(1LL, std::min<long long>(r, in->max_mb > 0 ? in->max_mb : r));
-  return lg2_ceil(r);
+  r = std::max(1LL, std::min<long long>(r, in->max_mb));
+  return (int)r;
 }
 
-int big_ring_lg(const cp_instances* in) { return lg2_ceil(std::max(1, std::min(in->max_mb, CP_MAX_MB))); }
+int big_ring_slots(const cp_instances* in) { return std::max(1, std::min(in->max_mb, CP_MAX_MB)); }
 
-size_t ring_bytes_per_warp(int ring_lg) { return size_t(2) << (ring_lg + 5 + 2); }   // 2 rings x R x 32 x 4 B
+constexpr int kPlanCapWords = 64;        // plans up to 1024 entries per stage row are staged in smem
+
+size_t ring_bytes_per_warp(int slots) { return (size_t)2 * slots * 32 * 4; }
 
 size_t ws_sim_greedy(const cp_instances* in, long long n_items) {
   return kCtrlBytes + align256(sizeof(int32_t) * (size_t)std::max(1LL, n_items)) +
-         (size_t)cpk::kFixWarps * ring_bytes_per_warp(big_ring_lg(in));
+         (size_t)cpk::kFixWarps * ring_bytes_per_warp(big_ring_slots(in));
+}
+
+// per-warp shared memory (32-bit words): rings + plan buffers + 2 mbarriers
+int smem_words(bool ring_global, int slots, int plan_words, int nbuf, bool tma) {
+  int w = ring_global ? 0 : 2 * slots * 32;
+  w += nbuf * plan_words * 32;
+  if (tma) w += 4;
+  return (w + 3) & ~3;                       // 16-B aligned per warp
 }
 
 int check_instances(const cp_instances* in) {
@@ -53,11 +62,33 @@ int check_instances(const cp_instances* in) {
   return CP_OK;
 }
 
+int launch_pass(cpk::Mode mode, bool ring_global, cpk::Args& a, long long n_tasks, int nseg, void* stream) {
+  const int sms = cpk::device_sm_count();
+  const int nbuf = a.tma ? 2 : 1;
+  a.smem_words_per_warp = smem_words(ring_global, a.ring_slots, a.plan_words, nbuf, a.tma != 0);
+  const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
+  if (ring_global) {
+    const int wpb = 4;
+    const size_t smem = per_warp * wpb;
+    if (smem > kMaxSmemPerBlock) return CP_EUNSUPPORTED;
+    return cpk::launch_engine(mode, true, a, cpk::kFixWarps / wpb, 32 * wpb, smem, stream) == cudaSuccess ? CP_OK
+                                                                                                      : CP_ECUDA;
+  }
+  const int wpb = per_warp * 2 <= kMaxSmemPerBlock ? 2 : 1;
+  const size_t smem = per_warp * wpb;
+  if (smem > kMaxSmemPerBlock) return CP_EUNSUPPORTED;
+  const int threads = 32 * wpb;
+  const int bps = cpk::engine_blocks_per_sm(mode, false, threads, smem);
+  const long long need = (n_tasks + (long long)nseg * wpb - 1) / ((long long)nseg * wpb);
+  const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
+  return cpk::launch_engine(mode, false, a, blocks, threads, smem, stream) == cudaSuccess ? CP_OK : CP_ECUDA;
+}
+
 int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, const cp_results* res, void* ws,
                size_t ws_bytes, void* stream) {
   const long long n = sc->n;
   if (ws_bytes < ws_sim_greedy(in, n) || !ws) return CP_EWORKSPACE;
-  Args a;
+  cpk::Args a;
   std::memset(&a, 0, sizeof(a));
   a.inst = in->inst;
   a.inst_of = sc->inst_of;
@@ -83,30 +114,28 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
   if (cudaMemsetAsync(a.ovf_count, 0, sizeof(int32_t), st) != cudaSuccess) return CP_ECUDA;
 
   const int nseg = 32 >> a.seg_lg;
-  const int sms = cpk::device_sm_count();
-  int rlg = ring_lg_for(in);
-  const int blg = big_ring_lg(in);
-  int wpb = (int)std::min<size_t>(4, kMaxSmemPerBlock / ring_bytes_per_warp(rlg));
-  if (wpb >= 1) {
-    // fast pass: shared-memory rings, occupancy-sized persistent grid
-    a.ring_lg = rlg;
-    const size_t smem = ring_bytes_per_warp(rlg) * wpb;
-    const int threads = 32 * wpb;
-    const int bps = cpk::engine_blocks_per_sm(mode, false, threads, smem);
-    const long long need = (n + (long long)nseg * wpb - 1) / ((long long)nseg * wpb);
-    const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
-    if (cpk::launch_engine(mode, false, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
-    // fix-up pass over the overflow list with global rings of n_mb slots
-    a.from_list = 1;
-    a.ring_lg = blg;
+  a.plan_words = sc->words <= kPlanCapWords ? sc->words : 0;
+  // fast pass: shared-memory rings sized to the in-flight bound, occupancy-sized persistent grid
+  a.ring_slots = ring_slots_for(in);
+  a.tma = (mode == cpk::MODE_SIM && nseg == 1 && sc->stage_stride == 32 && a.plan_words > 0) ? 1 : 0;
+  int rc = launch_pass(mode, false, a, n, nseg, stream);
+  if (rc == CP_EUNSUPPORTED) {
+    // rings too large for shared memory: single global-ring pass over every item
+    a.tma = 0;
+    a.ring_slots = big_ring_slots(in);
     a.ring_g = rings;
-    if (cpk::launch_engine(mode, true, a, cpk::kFixWarps / 4, cpk::kThreads, 0, stream) != cudaSuccess) return CP_ECUDA;
-  } else {
-    // rings too large for shared memory: single global-ring pass
-    a.ring_lg = blg;
-    a.ring_g = rings;
-    if (cpk::launch_engine(mode, true, a, cpk::kFixWarps / 4, cpk::kThreads, 0, stream) != cudaSuccess) return CP_ECUDA;
+    rc = launch_pass(mode, true, a, n, nseg, stream);
+    if (rc) return rc;
+    return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
   }
+  if (rc) return rc;
+  // fix-up pass over the overflow list (items whose lead exceeded R) with n_mb-slot global rings
+  a.from_list = 1;
+  a.tma = 0;
+  a.ring_slots = big_ring_slots(in);
+  a.ring_g = rings;
+  rc = launch_pass(mode, true, a, n, nseg, stream);
+  if (rc) return rc;
   return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
 }
 
@@ -133,7 +162,7 @@ int check_grid(const cp_grid* g) {
 
 // ring slots needed by the points of one p-class: max over (m, M_L) of
 // min(m, max_s floor(m_lim[s] / m_f[s])) -- greedy and feasible static plans never exceed it
-int sweep_ring_lg(const cp_grid* g, int p) {
+int sweep_ring_slots(const cp_grid* g, int p) {
   long long r = 1;
   for (int im = 0; im < g->n_mb_n; ++im)
     for (int ix = 0; ix < g->n_mem; ++ix) {
@@ -145,7 +174,7 @@ int sweep_ring_lg(const cp_grid* g, int p) {
       }
       r = std::max(r, std::min<long long>(need, g->n_mb_vals[im]));
     }
-  return lg2_ceil(r);
+  return (int)r;
 }
 
 long long point_cost(const cp_grid* g, int i_pp, int i_mb) {
@@ -216,11 +245,10 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
   (void)ws; (void)ws_bytes;
   if (lo == hi) return CP_OK;
   const long long per_pp = np / g->n_pp_n;        // p is the slowest axis: one contiguous block per p
-  const int sms = cpk::device_sm_count();
   for (int ip = 0; ip < g->n_pp_n; ++ip) {
     const long long a0 = std::max<long long>(lo, ip * per_pp), a1 = std::min<long long>(hi, (ip + 1) * per_pp);
     if (a0 >= a1) continue;
-    Args a;
+    cpk::Args a;
     std::memset(&a, 0, sizeof(a));
     a.grid = *g;
     a.pt_lo = a0;
@@ -228,16 +256,9 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
     a.keys = reinterpret_cast<unsigned long long*>(keys);
     a.cand_ms = cand_ms;
     a.seg_lg = lg2_ceil(g->n_pp_vals[ip]);
-    a.ring_lg = sweep_ring_lg(g, g->n_pp_vals[ip]);
-    const int wpb = (int)std::min<size_t>(4, kMaxSmemPerBlock / ring_bytes_per_warp(a.ring_lg));
-    if (wpb < 1) return CP_EUNSUPPORTED;
-    const size_t smem = ring_bytes_per_warp(a.ring_lg) * wpb;
-    const int threads = 32 * wpb;
-    const int nseg = 32 >> a.seg_lg;
-    const int bps = cpk::engine_blocks_per_sm(cpk::MODE_SWEEP, false, threads, smem);
-    const long long need = (a1 - a0 + (long long)nseg * wpb - 1) / ((long long)nseg * wpb);
-    const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
-    if (cpk::launch_engine(cpk::MODE_SWEEP, false, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+    a.ring_slots = sweep_ring_slots(g, g->n_pp_vals[ip]);
+    const int rc = launch_pass(cpk::MODE_SWEEP, false, a, a1 - a0, 32 >> a.seg_lg, stream);
+    if (rc) return rc;
   }
   return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
 }

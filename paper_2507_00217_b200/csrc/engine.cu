@@ -3,23 +3,30 @@
 // One warp evaluates 32/W items at a time: lane = pipeline stage, W = pow2 >= p is
 // the lane-segment width (small-p items are packed several per warp; shuffles use
 // the `width` argument so segments never talk to each other).  Evaluation is
-// round-synchronous dataflow:
-//   * each lane holds its stage's clock, memory, per-type counters and the FIFO
-//     clocks of its two outgoing links in registers;
+// round-synchronous dataflow; each round every lane executes at most one block:
+//   * the lane holds its stage's clock, memory, per-type counters and the FIFO clocks
+//     of its two outgoing links in registers;
 //   * a finished F (resp. D/B) block pushes its message through the link clock
 //     (Alg. 1 :404-407: E_bw = BW_model(end), T_avail = E_bw + T_lat) and writes the
-//     arrival time into the consumer's shared-memory arrival ring (slot-major
-//     [R][32] layout: lane l always hits bank l -> conflict-free);
-//   * producer counts are exchanged with one __shfl_up / __shfl_down per round.
-// MODE_SIM    : plan-driven (cp_simulate): a lane executes its next plan entry as
-//               soon as the entry's input is known (the §3.5 max-plus recurrence).
-// MODE_GREEDY : Alg. 1 + §4.2.2 (cp_greedy): every lane computes its schedulable
-//               time t*_s; two min-plus warp scans give a causal horizon H_s and every
-//               lane with t*_s < H_s decides in the same round (DESIGN.md "round-
-//               parallel greedy"), which reproduces sequential Alg. 1 exactly.
-// MODE_SWEEP  : (cp_sweep_shard) grid point -> instance synthesis in registers ->
-//               GPipe / 1F1B plans generated arithmetically + greedy n_sub = 1, 2, 4 ->
-//               packed (makespan << 8 | cand) argmin per point.
+//     arrival time into the consumer's shared-memory arrival ring (slot-major [R][32]
+//     layout: lane l always touches bank l or l+-1 -> conflict-free);
+//   * producer counts are exchanged with one __shfl_up + one __shfl_down per round;
+//   * block execution is branch-free (selects), so a warp walks one path per round
+//     whatever mix of F / D / B / W its lanes execute;
+//   * plan rows are staged in shared memory: one TMA bulk copy (cp.async.bulk,
+//     double-buffered: the next item's plan lands while the current one runs) when a
+//     warp holds one item, a cooperative copy when it holds several;
+//   * one ballot per round detects "no progress"; completion, deadlock, bad plans and
+//     ring overflow are resolved only on that rare path.
+// MODE_SIM    : plan-driven (cp_simulate): a lane executes its next plan entry as soon
+//               as the entry's input is known (the §3.5 max-plus recurrence).
+// MODE_GREEDY : Alg. 1 + §4.2.2 (cp_greedy): every lane computes its schedulable time
+//               t*_s; two min-plus warp scans give a causal horizon and every lane with
+//               t*_s < horizon decides in the same round (DESIGN.md "Round-parallel
+//               greedy"), which reproduces sequential Alg. 1 exactly.
+// MODE_SWEEP  : (cp_sweep_shard) grid point -> instance synthesis in registers -> GPipe /
+//               1F1B plans generated arithmetically + greedy n_sub = 1, 2, 4 -> packed
+//               (makespan << 8 | cand) argmin per point.
 // No tensor cores: nothing here is a dense contraction.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -36,27 +43,66 @@ constexpr unsigned long long KEY_OVER = 0x7ffffffffffffffeull;   // point not ev
 __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
 
+#ifdef CP_DEBUG
+// Debug build only: every shared / global access of the engine goes through a bounds check
+// that records the first violation (tag, index, limit, item, lane) and skips the access.
+__device__ int cp_dbg[8];
+__device__ __noinline__ bool dbg_ok(long long idx, long long lim, int tag, long long item) {
+  if (idx >= 0 && idx < lim) return true;
+  if (atomicCAS(&cp_dbg[0], 0, tag) == 0) {
+    cp_dbg[1] = (int)idx; cp_dbg[2] = (int)lim; cp_dbg[3] = (int)item; cp_dbg[4] = threadIdx.x;
+    cp_dbg[5] = blockIdx.x; cp_dbg[6] = (int)(idx >> 32);
+  }
+  return false;
+}
+#define CHK(idx, lim, tag) dbg_ok((long long)(idx), (long long)(lim), (tag), item)
+#else
+#define CHK(idx, lim, tag) true
+#endif
+
+// ---------------------------------------------------------------------------------- TMA bulk / mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// one elected lane: expect `bytes` and launch the bulk copy global -> shared (TMA, UBLKCP)
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
 // Arithmetic static plans (Table tab:ppschedules :470; readings Q22/Q23).
 // GPipe: F x m, B x m.  1F1B: w = min(p-s-1, m) F, (F,B) x (m-w), B x w.
-__device__ __forceinline__ uint32_t static_code(int cand, int s, int p, int m, int pos) {
-  if (cand == 0) return pos < m ? CP_OP_F : CP_OP_B;
-  int w = imin(p - s - 1, m);
-  if (pos < w) return CP_OP_F;
-  int q = pos - w;
-  if (q < 2 * (m - w)) return (q & 1) ? CP_OP_B : CP_OP_F;
-  return CP_OP_B;
+__device__ __forceinline__ int static_code(int cand, int s, int p, int m, int pos) {
+  if (cand == 0) return pos < m ? (int)CP_OP_F : (int)CP_OP_B;
+  const int w = imin(p - s - 1, m);
+  const int q = pos - w;
+  if (q < 0) return (int)CP_OP_F;
+  if (q < 2 * (m - w)) return (q & 1) ? (int)CP_OP_B : (int)CP_OP_F;
+  return (int)CP_OP_B;
 }
 
 struct LaneCfg {       // per-lane (stage) instance fields
   int p, m, nsub, tagate;
-  int tf, td, tw, wq, wr, mf, md, mw, mlim, tdp;
+  int tf, td, tw, tB, wq, wr, mf, md, mw, mB, mlim, tdp;
   int latF, bwF, latB, bwB;
   int P, Q;            // greedy lookahead: exclusive prefix of (tf+bwF+latF), inclusive prefix of (td+bwB+latB)
 };
 
+// smem layout per warp: [ringF R*32][ringD R*32][plan 2*PW*32][2 mbarriers]
 template <int kMode, bool kRingGlobal>
 __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Args A) {
-  extern __shared__ int32_t smem[];
+  extern __shared__ __align__(128) int32_t smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int lgW = A.seg_lg;
@@ -65,24 +111,59 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   const int seg = lane >> lgW;
   const int nseg = 32 >> lgW;
   const unsigned segmask = (W == 32) ? FULL : (((1u << W) - 1u) << (seg * W));
-  const int RM = (1 << A.ring_lg) - 1;
+  const int R = A.ring_slots;
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  int32_t* ringF = kRingGlobal ? A.ring_g + gwarp * (2LL << (A.ring_lg + 5)) : smem + wib * (2 << (A.ring_lg + 5));
-  int32_t* ringD = ringF + ((RM + 1) << 5);
+  int32_t* wsm = smem + (size_t)wib * A.smem_words_per_warp;
+  int32_t* ringF = kRingGlobal ? A.ring_g + gwarp * (2LL * R * 32) : wsm;
+  int32_t* ringD = ringF + R * 32;
+  const int PW = A.plan_words;                       // plan words staged in smem (0: read from global)
+  uint32_t* plan = reinterpret_cast<uint32_t*>(wsm + (kRingGlobal ? 0 : 2 * R * 32));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(plan + 2 * PW * 32);
+  const bool use_tma = (kMode == MODE_SIM) && A.tma && PW > 0;   // one item per warp, rows contiguous [words][32]
+  const uint32_t plan_bytes = (uint32_t)A.words * 32u * 4u;
 
   long long task = gwarp * nseg + seg;
   const long long task_stride = nwarps * nseg;
+#ifdef CP_DEBUG
+  const long long s_lim = (long long)(blockDim.x >> 5) * A.smem_words_per_warp;
+  const long long g_lim = nwarps * 2LL * R * 32;
+  long long item = -1;
+  auto SOK = [&](const void* p, int tag) -> bool {
+    const int32_t* q = (const int32_t*)p;
+    if (kRingGlobal && q >= A.ring_g && q < A.ring_g + g_lim) return true;
+    return dbg_ok(q - smem, s_lim, tag, item);
+  };
+  const long long n_it = kMode == MODE_SWEEP ? A.pt_hi : A.n_items;
+#else
+  long long item = -1;
+#define SOK(p, tag) true
+#endif
+
+  auto item_of = [&](long long t) -> long long {
+    if (kMode == MODE_SWEEP) return (A.pt_lo + t < A.pt_hi) ? A.pt_lo + t : -1;
+    if (A.from_list) return (t < *(volatile int32_t*)A.ovf_count) ? (long long)A.ovf_list[t] : -1;
+    return t < A.n_items ? t : -1;
+  };
+
+  uint32_t phase = 0;          // mbarrier parity of each plan buffer (bit b)
+  int cur_buf = 0;
+  if (use_tma) {
+    if (lane == 0) { mbar_init(&bars[0]); mbar_init(&bars[1]); }
+    __syncwarp();
+    const long long it0 = item_of(task);
+    if (lane == 0 && it0 >= 0) tma_load_1d(plan, A.ops + it0 * A.words * 32, plan_bytes, &bars[0]);
+  }
 
   LaneCfg c = {};
-  long long item = -1;
-  bool need_load = true;
+  bool need_load = true, any_load = true;
   int load_status = 0;
   int zero1 = 0, valid_inst = 0;
   // dynamic state of this lane's stage
   int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0, linkF = 0, linkB = 0;
+  int slF = 0, slD = 0;                   // ring slots = nF mod R, nD mod R
   int first = 0, busy = 0, pos = 0, plen = 0, comb = 0, last_fd = 0;
-  uint32_t word = 0, nextword = 0;
+  uint32_t emitw = 0;
   bool ovf = false;
   // sweep: current candidate (>= 0), or -(c+1) = "advance to the first candidate >= c"
   int cand = 0;
@@ -91,235 +172,255 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
 
   for (;;) {
     // ------------------------------------------------------------------ fetch + load (per segment)
-    bool just_loaded = false;
-    if (need_load) {
-      need_load = false;
-      item = -1;
+    if (any_load) {
+      bool just_loaded = false;
+      if (need_load) {
+        need_load = false;
+        item = item_of(task);
+        task += task_stride;
+        if (item >= 0) {
+          just_loaded = true;
+          int lat_b_s = 0, bw_b_s = 0;   // lane s validates boundary s in both directions
+          c = LaneCfg{};
+          if (kMode == MODE_SWEEP) {
+            const cp_grid& G = A.grid;
+            long long k = item;
+            const int i_dp = (int)(k % G.n_dp); k /= G.n_dp;
+            const int i_mem = (int)(k % G.n_mem); k /= G.n_mem;
+            const int i_bw = (int)(k % G.n_bw); k /= G.n_bw;
+            const int i_lat = (int)(k % G.n_lat); k /= G.n_lat;
+            const int i_mb = (int)(k % G.n_mb_n); k /= G.n_mb_n;
+            const int i_pp = (int)k;
+            c.p = G.n_pp_vals[i_pp];
+            c.m = G.n_mb_vals[i_mb];
+            c.nsub = 1;
+            zero1 = G.base.flags & 1;
+            const int ndc = imin(G.n_dc, c.p);
+            if (s < c.p) {
+              c.tf = G.base.t_f[s]; c.td = G.base.t_d[s]; c.tw = G.base.t_w[s];
+              c.mf = G.base.m_f[s]; c.md = G.base.m_d[s]; c.mw = G.base.m_w[s];
+              c.mlim = (int)(((long long)G.mlim_x1000[i_mem] * c.p * c.mf + 500) / 1000);
+              c.tdp = G.tdp[i_dp];
+              c.tagate = G.base.t_ag[s];
+              const bool xf = (s < c.p - 1) && (s * ndc / c.p != (s + 1) * ndc / c.p);
+              const bool xb = (s > 0) && ((s - 1) * ndc / c.p != s * ndc / c.p);
+              c.latF = xf ? G.lat[i_lat] : 0; c.bwF = xf ? G.bw[i_bw] : 0;
+              c.latB = xb ? G.lat[i_lat] : 0; c.bwB = xb ? G.bw[i_bw] : 0;
+              lat_b_s = c.latF; bw_b_s = c.bwF;
+            }
+          } else {
+            const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
+            const cp_inst_v1* I = A.inst + ii;
+            c.p = I->n_pp; c.m = I->n_mb; c.nsub = I->n_sub;
+            zero1 = I->flags & 1;
+            if (s < c.p && s < CP_MAX_STAGES) {
+              c.tf = I->t_f[s]; c.td = I->t_d[s]; c.tw = I->t_w[s];
+              c.mf = I->m_f[s]; c.md = I->m_d[s]; c.mw = I->m_w[s]; c.mlim = I->m_lim[s];
+              c.tdp = I->t_dp[s];
+              c.tagate = I->t_ag[s];
+              c.latF = (s < c.p - 1) ? I->lat_f[s] : 0; c.bwF = (s < c.p - 1) ? I->bw_f[s] : 0;
+              c.latB = (s > 0) ? I->lat_b[s - 1] : 0; c.bwB = (s > 0) ? I->bw_b[s - 1] : 0;
+              lat_b_s = (s < c.p - 1) ? I->lat_b[s] : 0; bw_b_s = (s < c.p - 1) ? I->bw_b[s] : 0;
+            }
+          }
+          // instance invariants (readings Q10, Q12)
+          bool bad = c.p < 1 || c.p > CP_MAX_STAGES || c.m < 1 || c.nsub < 1;
+          if (!bad && s < c.p) {
+            bad = !(c.tf > 0 && c.td > 0 && c.tw > 0 && c.tw >= c.nsub && c.mf > 0 && c.md <= 0 && c.mw <= 0 &&
+                    (long long)c.mf + c.md + c.mw == 0 && c.mlim >= c.mf && c.tdp >= 0 && c.tagate >= 0 &&
+                    c.latF >= 0 && c.bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
+          }
+          if (!zero1) c.tagate = 0;
+          valid_inst = !bad;
+          load_status = bad ? CPI_BAD_INSTANCE : 0;
+          c.wq = c.tw / imax(c.nsub, 1);
+          c.wr = c.tw % imax(c.nsub, 1);
+          c.tB = c.td + c.tw;
+          c.mB = c.md + c.mw;
+          plen = 0;
+          if (kMode == MODE_SIM && s < c.p && s < A.stage_stride) {
+            plen = A.len[item * A.stage_stride + s];
+            if (plen > 16 * A.words && !bad) load_status = CPI_BAD_PLAN;     // row longer than its capacity
+          }
+          if (kMode == MODE_GREEDY && !bad && (long long)(2 + c.nsub) * c.m > 16LL * A.words)
+            load_status = CPI_BAD_PLAN;                                      // output row capacity too small
+          if (!load_status && (c.p > W || c.m > CP_MAX_MB || c.nsub > CP_MAX_SUB)) load_status = CPI_OVERFLOW;
+          clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = slF = slD = 0;
+          first = busy = pos = comb = last_fd = 0;
+          emitw = 0;
+          ovf = false;
+          best = KEY_NONE;
+          cand = -1;
+          if (kMode == MODE_SWEEP && A.cand_ms && s == 0)
+            for (int cc = 0; cc < 5; ++cc) A.cand_ms[item * 5 + cc] = -1;
+        }
+      }
+      if (__all_sync(FULL, item < 0)) break;
+
+      // ---------------------------------------------------------------- warp-wide post-load
+      if (__any_sync(FULL, just_loaded)) {
+        const bool act = just_loaded && s < c.p && valid_inst;
+        const int cf = act ? c.tf + c.bwF + c.latF : 0;      // hop s -> s+1 (F)
+        const int cd = act ? c.td + c.bwB + c.latB : 0;      // hop s -> s-1 (D)
+        long long u = 0;                                      // horizon bound U (reading Q21)
+        if (act)
+          u = (long long)c.m * ((long long)c.tf + c.td + c.tw) + c.tagate + c.tdp +
+              (long long)c.m * ((long long)c.latF + c.bwF + c.latB + c.bwB);
+        int pf = cf, qd = cd;
+        for (int d = 1; d < W; d <<= 1) {
+          const int a = __shfl_up_sync(FULL, pf, d, W);
+          const int b = __shfl_up_sync(FULL, qd, d, W);
+          if (s >= d) { pf += a; qd += b; }
+        }
+        for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(FULL, u, d, W);
+        const unsigned b_inst = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_INSTANCE);
+        const unsigned b_plan = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_PLAN);
+        const unsigned b_over = __ballot_sync(FULL, just_loaded && load_status == CPI_OVERFLOW);
+        if (just_loaded) {
+          c.P = pf - cf;
+          c.Q = qd;
+          int st = (b_inst & segmask) ? CPI_BAD_INSTANCE
+                   : (b_plan & segmask) ? CPI_BAD_PLAN
+                   : (b_over & segmask) ? CPI_OVERFLOW : 0;
+          if (!st && u >= (long long)INF) st = CPI_OVERFLOW;     // int32 horizon guard
+          load_status = st;
+          if (kMode != MODE_SWEEP && st != 0) {
+            // per-item failure: report now, no evaluation
+            if (s == 0) {
+              A.makespan[item] = -1;
+              if (A.peak_mem) A.peak_mem[item] = -1;
+              A.status[item] = st;
+            }
+            if (A.stage_stats && s < A.stage_stride)
+              *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = make_int4(0, 0, 0, 0);
+            if (kMode == MODE_GREEDY && s < A.stage_stride) A.len[item * A.stage_stride + s] = 0;
+            need_load = true;
+          }
+        }
+        // stage the plan rows in shared memory
+        if (kMode == MODE_SIM && PW > 0) {
+          if (use_tma) {
+            // this item's rows were prefetched into plan[cur_buf]: wait, then prefetch the next item
+            if (just_loaded) {
+              mbar_wait(&bars[cur_buf], (phase >> cur_buf) & 1u);
+              phase ^= 1u << cur_buf;
+              const long long nxt = item_of(task);
+              if (lane == 0 && nxt >= 0)
+                tma_load_1d(plan + (cur_buf ^ 1) * PW * 32, A.ops + nxt * A.words * 32, plan_bytes,
+                            &bars[cur_buf ^ 1]);
+              if (need_load) cur_buf ^= 1;        // failed item: its buffer is consumed already
+            }
+          } else if (just_loaded && !need_load && s < c.p) {
+            for (int k = 0; k < A.words && k * 16 < plen; ++k)
+              if (SOK(plan + k * 32 + lane, 14) && CHK(item * A.words + k, n_it * A.words, 15))
+                plan[k * 32 + lane] = A.ops[(item * A.words + k) * A.stage_stride + s];
+          }
+          __syncwarp();
+        }
+      }
+
+      // ---------------------------------------------------------------- sweep: next candidate
       if (kMode == MODE_SWEEP) {
-        const long long pt = A.pt_lo + task;
-        if (pt < A.pt_hi) item = pt;
-      } else if (A.from_list) {
-        const int cnt = *(volatile int32_t*)A.ovf_count;
-        if (task < cnt) item = A.ovf_list[task];
-      } else if (task < A.n_items) {
-        item = task;
-      }
-      task += task_stride;
-      if (item >= 0) {
-        just_loaded = true;
-        int lat_b_s = 0, bw_b_s = 0;   // lane s validates boundary s in both directions
-        c = LaneCfg{};
-        if (kMode == MODE_SWEEP) {
-          const cp_grid& G = A.grid;
-          long long k = item;
-          const int i_dp = (int)(k % G.n_dp); k /= G.n_dp;
-          const int i_mem = (int)(k % G.n_mem); k /= G.n_mem;
-          const int i_bw = (int)(k % G.n_bw); k /= G.n_bw;
-          const int i_lat = (int)(k % G.n_lat); k /= G.n_lat;
-          const int i_mb = (int)(k % G.n_mb_n); k /= G.n_mb_n;
-          const int i_pp = (int)k;
-          c.p = G.n_pp_vals[i_pp];
-          c.m = G.n_mb_vals[i_mb];
-          c.nsub = 1;
-          zero1 = G.base.flags & 1;
-          const int ndc = imin(G.n_dc, c.p);
-          if (s < c.p) {
-            c.tf = G.base.t_f[s]; c.td = G.base.t_d[s]; c.tw = G.base.t_w[s];
-            c.mf = G.base.m_f[s]; c.md = G.base.m_d[s]; c.mw = G.base.m_w[s];
-            c.mlim = (int)(((long long)G.mlim_x1000[i_mem] * c.p * c.mf + 500) / 1000);
-            c.tdp = G.tdp[i_dp];
-            c.tagate = G.base.t_ag[s];
-            const bool xf = (s < c.p - 1) && (s * ndc / c.p != (s + 1) * ndc / c.p);
-            const bool xb = (s > 0) && ((s - 1) * ndc / c.p != s * ndc / c.p);
-            c.latF = xf ? G.lat[i_lat] : 0; c.bwF = xf ? G.bw[i_bw] : 0;
-            c.latB = xb ? G.lat[i_lat] : 0; c.bwB = xb ? G.bw[i_bw] : 0;
-            lat_b_s = c.latF; bw_b_s = c.bwF;
+        const bool want = item >= 0 && cand < 0 && !need_load;
+        if (__any_sync(FULL, want)) {
+          const int from = -cand - 1;
+          int next = -1;
+          for (int cc = 0; cc < 5; ++cc) {
+            bool ok = true;       // statically memory-feasible / valid candidate on this stage
+            if (s < c.p) {
+              if (cc == 0) ok = (long long)c.m * c.mf <= c.mlim;                          // GPipe peak m*m_f
+              else if (cc == 1) ok = (long long)imin(c.p - s, c.m) * c.mf <= c.mlim;     // 1F1B peak (Z5)
+              else ok = c.tw >= (1 << (cc - 2));                                           // Q12 t_w >= n_sub
+            }
+            const unsigned nb = __ballot_sync(FULL, !ok);
+            if (want && next < 0 && cc >= from && ((A.grid.cand_mask >> cc) & 1u) && !(nb & segmask)) next = cc;
           }
-        } else {
-          const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
-          const cp_inst_v1* I = A.inst + ii;
-          c.p = I->n_pp; c.m = I->n_mb; c.nsub = I->n_sub;
-          zero1 = I->flags & 1;
-          if (s < c.p && s < CP_MAX_STAGES) {
-            c.tf = I->t_f[s]; c.td = I->t_d[s]; c.tw = I->t_w[s];
-            c.mf = I->m_f[s]; c.md = I->m_d[s]; c.mw = I->m_w[s]; c.mlim = I->m_lim[s];
-            c.tdp = I->t_dp[s];
-            c.tagate = I->t_ag[s];
-            c.latF = (s < c.p - 1) ? I->lat_f[s] : 0; c.bwF = (s < c.p - 1) ? I->bw_f[s] : 0;
-            c.latB = (s > 0) ? I->lat_b[s - 1] : 0; c.bwB = (s > 0) ? I->bw_b[s - 1] : 0;
-            lat_b_s = (s < c.p - 1) ? I->lat_b[s] : 0; bw_b_s = (s < c.p - 1) ? I->bw_b[s] : 0;
-          }
-        }
-        // instance invariants (readings Q10, Q12)
-        bool bad = c.p < 1 || c.p > CP_MAX_STAGES || c.m < 1 || c.nsub < 1;
-        if (!bad && s < c.p) {
-          bad = !(c.tf > 0 && c.td > 0 && c.tw > 0 && c.tw >= c.nsub && c.mf > 0 && c.md <= 0 && c.mw <= 0 &&
-                  (long long)c.mf + c.md + c.mw == 0 && c.mlim >= c.mf && c.tdp >= 0 && c.tagate >= 0 &&
-                  c.latF >= 0 && c.bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
-        }
-        if (!zero1) c.tagate = 0;
-        valid_inst = !bad;
-        load_status = bad ? CPI_BAD_INSTANCE : 0;
-        c.wq = c.tw / imax(c.nsub, 1);
-        c.wr = c.tw % imax(c.nsub, 1);
-        plen = 0; word = nextword = 0;
-        if (kMode == MODE_SIM && s < c.p && s < A.stage_stride) {
-          plen = A.len[item * A.stage_stride + s];
-          if (plen > 16 * A.words) {
-            if (!bad) load_status = CPI_BAD_PLAN;           // row longer than its capacity
-          } else {
-            if (plen > 0) word = A.ops[(item * A.words) * A.stage_stride + s];
-            if (plen > 16) nextword = A.ops[(item * A.words + 1) * A.stage_stride + s];
-          }
-        }
-        if (kMode == MODE_GREEDY && !bad && (long long)(2 + c.nsub) * c.m > 16LL * A.words)
-          load_status = CPI_BAD_PLAN;                          // output row capacity too small
-        if (!load_status && (c.p > W || c.m > CP_MAX_MB || c.nsub > CP_MAX_SUB)) load_status = CPI_OVERFLOW;
-        clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = 0;
-        first = busy = pos = comb = last_fd = 0;
-        word = (kMode == MODE_GREEDY) ? 0u : word;
-        ovf = false;
-        best = KEY_NONE;
-        cand = -1;
-        if (kMode == MODE_SWEEP && A.cand_ms && s == 0)
-          for (int cc = 0; cc < 5; ++cc) A.cand_ms[item * 5 + cc] = -1;
-      }
-    }
-    if (__all_sync(FULL, item < 0)) break;
-
-    // ------------------------------------------------------------------ warp-wide post-load
-    if (__any_sync(FULL, just_loaded)) {
-      const bool act = just_loaded && s < c.p && valid_inst;
-      const int cf = act ? c.tf + c.bwF + c.latF : 0;      // hop s -> s+1 (F)
-      const int cd = act ? c.td + c.bwB + c.latB : 0;      // hop s -> s-1 (D)
-      long long u = 0;                                      // horizon bound U (reading Q21)
-      if (act)
-        u = (long long)c.m * ((long long)c.tf + c.td + c.tw) + c.tagate + c.tdp +
-            (long long)c.m * ((long long)c.latF + c.bwF + c.latB + c.bwB);
-      int pf = cf, qd = cd;
-      for (int d = 1; d < W; d <<= 1) {
-        const int a = __shfl_up_sync(FULL, pf, d, W);
-        const int b = __shfl_up_sync(FULL, qd, d, W);
-        if (s >= d) { pf += a; qd += b; }
-      }
-      for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(FULL, u, d, W);
-      const unsigned b_inst = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_INSTANCE);
-      const unsigned b_plan = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_PLAN);
-      const unsigned b_over = __ballot_sync(FULL, just_loaded && load_status == CPI_OVERFLOW);
-      if (just_loaded) {
-        c.P = pf - cf;
-        c.Q = qd;
-        int st = (b_inst & segmask) ? CPI_BAD_INSTANCE
-                 : (b_plan & segmask) ? CPI_BAD_PLAN
-                 : (b_over & segmask) ? CPI_OVERFLOW : 0;
-        if (!st && u >= (long long)INF) st = CPI_OVERFLOW;     // int32 horizon guard
-        load_status = st;
-        if (kMode != MODE_SWEEP && st != 0) {
-          // per-item failure: report now, no evaluation
-          if (s == 0) {
-            A.makespan[item] = -1;
-            if (A.peak_mem) A.peak_mem[item] = -1;
-            A.status[item] = st;
-          }
-          if (A.stage_stats && s < A.stage_stride)
-            *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = make_int4(0, 0, 0, 0);
-          if (kMode == MODE_GREEDY && s < A.stage_stride) A.len[item * A.stage_stride + s] = 0;
-          need_load = true;
-        }
-      }
-    }
-
-    // ------------------------------------------------------------------ sweep: next candidate
-    if (kMode == MODE_SWEEP) {
-      const bool want = item >= 0 && cand < 0 && !need_load;
-      if (__any_sync(FULL, want)) {
-        const int from = -cand - 1;
-        int next = -1;
-        for (int cc = 0; cc < 5; ++cc) {
-          bool ok = true;       // statically memory-feasible / valid candidate on this stage
-          if (s < c.p) {
-            if (cc == 0) ok = (long long)c.m * c.mf <= c.mlim;                          // GPipe peak m*m_f
-            else if (cc == 1) ok = (long long)imin(c.p - s, c.m) * c.mf <= c.mlim;     // 1F1B peak (Z5)
-            else ok = c.tw >= (1 << (cc - 2));                                           // Q12 t_w >= n_sub
-          }
-          const unsigned nb = __ballot_sync(FULL, !ok);
-          if (want && next < 0 && cc >= from && ((A.grid.cand_mask >> cc) & 1u) && !(nb & segmask)) next = cc;
-        }
-        if (want) {
-          if (load_status != 0) {
-            if (s == 0) A.keys[item] = (load_status == CPI_OVERFLOW) ? KEY_OVER : KEY_NONE;
-            need_load = true;
-          } else if (next < 0) {
-            if (s == 0) A.keys[item] = best;
-            need_load = true;
-          } else {
-            cand = next;
-            cand_greedy = next >= 2;
-            c.nsub = cand_greedy ? (1 << (next - 2)) : 1;
-            c.wq = c.tw / c.nsub;
-            c.wr = c.tw % c.nsub;
-            clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = 0;
-            first = busy = pos = comb = last_fd = 0;
-            ovf = false;
-            plen = (s < c.p && !cand_greedy) ? 2 * c.m : 0;
+          if (want) {
+            if (load_status != 0) {
+              if (s == 0) A.keys[item] = (load_status == CPI_OVERFLOW) ? KEY_OVER : KEY_NONE;
+              need_load = true;
+            } else if (next < 0) {
+              if (s == 0) A.keys[item] = best;
+              need_load = true;
+            } else {
+              cand = next;
+              cand_greedy = next >= 2;
+              c.nsub = cand_greedy ? (1 << (next - 2)) : 1;
+              c.wq = c.tw / c.nsub;
+              c.wr = c.tw % c.nsub;
+              clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = slF = slD = 0;
+              first = busy = pos = comb = last_fd = 0;
+              ovf = false;
+              plen = (s < c.p && !cand_greedy) ? 2 * c.m : 0;
+            }
           }
         }
       }
+      any_load = __any_sync(FULL, need_load);
+      if (any_load) continue;     // warp-uniform: (re)load before running rounds
     }
 
     // ------------------------------------------------------------------ one round
-    const bool in_round = item >= 0 && !need_load;
+    const bool in_round = item >= 0;
     const bool is_greedy = (kMode == MODE_GREEDY) || (kMode == MODE_SWEEP && cand_greedy);
-    const bool act = in_round && s < c.p;
-    bool fin;
-    if (is_greedy) fin = !act || (nF == c.m && nD == c.m && nW == c.m);
-    else fin = !act || pos >= plen;
-    const bool live = act && !fin;
+    const bool act = in_round && s < c.p && !ovf;
+    const bool live = act && (is_greedy ? (nW < c.m || nD < c.m || nF < c.m) : pos < plen);
 
     const int leftF = __shfl_up_sync(FULL, nF, 1, W);
     const int rightD = __shfl_down_sync(FULL, nD, 1, W);
-    const int arrF = ringF[((nF & RM) << 5) + lane];
-    const int arrD = ringD[((nD & RM) << 5) + lane];
+    const bool lastS = s == c.p - 1;
     const bool knowF = nF < c.m && (s == 0 || leftF > nF);
-    const int availF = imax(s == 0 ? 0 : arrF, c.tagate);
-    const bool knowD = nD < c.m && (s == c.p - 1 ? nF > nD : rightD > nD);
-    const int availD = (s == c.p - 1) ? 0 : arrD;
+    const bool knowD = nD < c.m && (lastS ? nF > nD : rightD > nD);
 
-    int op = -1, start = 0;
-    bool badp = false;
+    bool go = false, isF = false, isW = false, isB = false, badp = false;
+    int start = 0;
     if (kMode != MODE_GREEDY) {
-      if (live && !is_greedy) {
-        uint32_t code;
-        if (kMode == MODE_SIM) code = (word >> ((pos & 15) << 1)) & 3u;
-        else code = static_code(cand, s, c.p, c.m, pos);
-        if (kMode == MODE_SIM) {
-          // reading Q29: counts, W prefix <= n_sub * D, stage all-combined or all-split
-          const int wents = nW * c.nsub + wsub;
-          badp = (code == CP_OP_F && nF >= c.m) || ((code == CP_OP_D || code == CP_OP_B) && nD >= c.m) ||
-                 (code == CP_OP_W && wents >= c.nsub * nD) || (code == CP_OP_B && comb == 2) ||
-                 ((code == CP_OP_D || code == CP_OP_W) && comb == 1);
-        }
-        const bool ready = (code == CP_OP_F) ? knowF : (code == CP_OP_W ? true : knowD);
-        if (!badp && ready) {
-          op = (int)code;
-          start = imax(clk, code == CP_OP_F ? availF : (code == CP_OP_W ? 0 : availD));
-        }
+      // ---- plan-driven selection
+      int code;
+      if (kMode == MODE_SIM) {
+        const int pq = live ? pos : 0;       // finished rows may sit at pos == 16*words: never index past them
+        const uint32_t wv = (PW > 0) ? (SOK(plan + cur_buf * PW * 32 + ((pq >> 4) << 5) + lane, 1)
+                                            ? plan[cur_buf * PW * 32 + ((pq >> 4) << 5) + lane] : 0u)
+                                     : (live && CHK(item * A.words + (pq >> 4), n_it * A.words, 2)
+                                            ? A.ops[(item * A.words + (pq >> 4)) * A.stage_stride + s] : 0u);
+        code = (int)((wv >> ((pq & 15) << 1)) & 3u);
+      } else {
+        code = static_code(cand, s, c.p, c.m, pos);
+      }
+      const bool cF = code == (int)CP_OP_F, cW = code == (int)CP_OP_W, cB = code == (int)CP_OP_B;
+      const int* ap = cF ? ringF + slF * 32 + lane : ringD + slD * 32 + lane;
+      const int arr = SOK(ap, 3) ? ap[0] : 0;
+      const int avail = cF ? imax(s == 0 ? 0 : arr, c.tagate) : ((cW || lastS) ? 0 : arr);
+      const bool ready = cF ? knowF : (cW || knowD);
+      if (kMode == MODE_SIM) {
+        // reading Q29: counts, W prefix <= n_sub * D, stage all-combined or all-split
+        badp = live && (cF ? nF >= c.m
+                           : (cW ? (nW * c.nsub + wsub >= c.nsub * nD || comb == 1)
+                                 : (nD >= c.m || (cB ? comb == 2 : comb == 1))));
+      }
+      if (!is_greedy) {
+        go = live && ready && !badp;
+        isF = cF; isW = cW; isB = cB;
+        start = imax(clk, avail);
       }
     }
     if (kMode != MODE_SIM) {
-      int tstar = INF;
-      bool hasF = false, hasD = false;
-      if (live && is_greedy) {
-        hasF = knowF && mem + c.mf <= c.mlim;         // Q15: memory-infeasible F is not eligible
-        hasD = knowD;
-        const bool hasW = nW < nD;
-        int mn = INF;
-        if (hasF) mn = availF;
-        if (hasD) mn = imin(mn, availD);
-        if (hasW) mn = imin(mn, clk);                 // W avail = its D end <= clk
-        if (hasF || hasD || hasW) tstar = imax(clk, mn);   // §4.2.2 :419 schedulable time
-      }
-      if (kMode == MODE_GREEDY || __any_sync(FULL, is_greedy && act)) {
+      // ---- greedy selection (Alg. 1 lines 6 and 10, §4.2.2)
+      const int arrF = SOK(ringF + slF * 32 + lane, 4) ? ringF[slF * 32 + lane] : 0;
+      const int arrD = SOK(ringD + slD * 32 + lane, 5) ? ringD[slD * 32 + lane] : 0;
+      const int availF = imax(s == 0 ? 0 : arrF, c.tagate);
+      const int availD = lastS ? 0 : arrD;
+      const bool gl = live && is_greedy;
+      const bool hasF = gl && knowF && mem + c.mf <= c.mlim;      // Q15: memory-infeasible F is not eligible
+      const bool hasD = gl && knowD;
+      const bool hasW = gl && nW < nD;                             // W avail = its D end <= clk
+      int mn = hasF ? availF : INF;
+      mn = imin(mn, hasD ? availD : INF);
+      mn = imin(mn, hasW ? clk : INF);
+      const int tstar = (hasF || hasD || hasW) ? imax(clk, mn) : INF;   // §4.2.2 :419
+      bool run_scan = true;
+      if (kMode == MODE_SWEEP) run_scan = __any_sync(FULL, gl);
+      if (run_scan) {
         // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s
         int x = tstar - c.P, y = tstar + c.Q;
         for (int d = 1; d < W; d <<= 1) {
@@ -332,88 +433,77 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         const int ye = __shfl_down_sync(FULL, y, 1, W);
         const int Lh = (s == 0) ? INF : c.P + xe;
         const int Rh = (s == W - 1) ? INF : ye - c.Q;
-        if (live && is_greedy && tstar < INF && tstar < imin(Lh, Rh)) {
-          // §4.2.2 operation selection (reading Q13): opposite of the last full F/D block,
-          // then the other, then a W sub-block
-          const bool cF = hasF && availF <= tstar, cD = hasD && availD <= tstar;
-          if (last_fd == 1) op = cD ? (int)CP_OP_D : (cF ? (int)CP_OP_F : (int)CP_OP_W);
-          else op = cF ? (int)CP_OP_F : (cD ? (int)CP_OP_D : (int)CP_OP_W);
+        const bool g_go = tstar < INF && tstar < imin(Lh, Rh);   // L, R may exceed INF: guard idle lanes
+        // operation selection (reading Q13): opposite of the last full F/D block, then the
+        // other, then a W sub-block
+        const bool cF = hasF && availF <= tstar, cD = hasD && availD <= tstar;
+        const bool pickD = (last_fd == 1) ? cD : (cD && !cF);
+        const bool pickF = !pickD && cF;
+        if (is_greedy) {
+          go = g_go;
+          isF = pickF; isW = !pickF && !pickD; isB = false;
           start = tstar;
         }
       }
     }
-    // ------------------------------------------------------------------ execute the chosen block
-    if (op >= 0) {
-      int dur;
-      if (op == (int)CP_OP_F) dur = c.tf;
-      else if (op == (int)CP_OP_D) dur = c.td;
-      else if (op == (int)CP_OP_B) dur = c.td + c.tw;
-      else dur = c.wq + (wsub < c.wr ? 1 : 0);       // Q12 integer sub-block durations
+
+    // ------------------------------------------------------------------ execute (branch-free)
+    if (go) {
+      const bool isDB = !isF && !isW;
+      const bool wfin = isW && (wsub + 1 == c.nsub);
+      const int dur = isF ? c.tf : (isW ? c.wq + (wsub < c.wr ? 1 : 0) : (isB ? c.tB : c.td));
       const int end = start + dur;
-      if (pos == 0) first = start;
+      first = (pos == 0) ? start : first;
       busy += dur;
       clk = end;
-      if (kMode != MODE_SWEEP && A.t_start && pos < A.len_stride)
+      mem += isF ? c.mf : (isW ? (wfin ? c.mw : 0) : (isB ? c.mB : c.md));
+      peak = imax(peak, mem);
+      if (kMode == MODE_SIM) comb = isF ? comb : (isB ? 1 : 2);
+      last_fd = isF ? 1 : (isDB ? 2 : last_fd);
+      // message through the FIFO link clock (= first fit under UD, App. X1)
+      const int lk = isF ? linkF : linkB;
+      const int nl = imax(end, lk) + (isF ? c.bwF : c.bwB);
+      const bool send = isF ? (s < c.p - 1) : (isDB && s > 0);
+      int* wp = isF ? ringF + slF * 32 + lane + 1 : ringD + slD * 32 + lane - 1;
+      if (send && SOK(wp, 6)) wp[0] = nl + (isF ? c.latF : c.latB);
+      linkF = isF ? nl : linkF;
+      linkB = isDB ? nl : linkB;
+      nF += isF;
+      nD += isDB;
+      slF = isF ? (slF + 1 == R ? 0 : slF + 1) : slF;
+      slD = isDB ? (slD + 1 == R ? 0 : slD + 1) : slD;
+      wsub = isW ? (wfin ? 0 : wsub + 1) : wsub;
+      nW += wfin;
+      if (!kRingGlobal && nF - nD > R) ovf = true;
+      if (kMode != MODE_SWEEP && A.t_start && pos < A.len_stride && CHK(item * A.stage_stride + s, n_it * A.stage_stride, 7))
         A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
       if (kMode == MODE_GREEDY) {
-        word |= (uint32_t)op << ((pos & 15) << 1);
-        if ((pos & 15) == 15) {
-          A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = word;
-          word = 0;
-        }
+        const int code = isF ? (int)CP_OP_F : (isW ? (int)CP_OP_W : (int)CP_OP_D);
+        emitw |= (uint32_t)code << ((pos & 15) << 1);
+        if (PW > 0) { if (SOK(plan + ((pos >> 4) << 5) + lane, 8)) plan[((pos >> 4) << 5) + lane] = emitw; }
+        else if ((pos & 15) == 15 && CHK(item * A.words + (pos >> 4), n_it * A.words, 9)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
+        emitw = ((pos & 15) == 15) ? 0u : emitw;
       }
-      if (op == (int)CP_OP_F) {
-        mem += c.mf;
-        ++nF;
-        last_fd = 1;
-        if (s < c.p - 1) {
-          const int ws = imax(end, linkF);        // FIFO link clock = first fit under UD (App. X1)
-          linkF = ws + c.bwF;
-          ringF[(((nF - 1) & RM) << 5) + lane + 1] = linkF + c.latF;   // T_avail = E_bw + T_lat
-        }
-        if (!kRingGlobal && nF - nD > RM + 1) ovf = true;
-      } else if (op == (int)CP_OP_W) {
-        if (++wsub == c.nsub) { wsub = 0; ++nW; mem += c.mw; }     // W releases at its last sub-block
-        if (kMode == MODE_SIM) comb = 2;
-      } else {
-        mem += (op == (int)CP_OP_D) ? c.md : c.md + c.mw;
-        ++nD;
-        last_fd = 2;
-        if (kMode == MODE_SIM) comb = (op == (int)CP_OP_B) ? 1 : 2;
-        if (s > 0) {
-          const int ws = imax(end, linkB);
-          linkB = ws + c.bwB;
-          ringD[(((nD - 1) & RM) << 5) + lane - 1] = linkB + c.latB;
-        }
-      }
-      peak = imax(peak, mem);
       ++pos;
-      if (kMode == MODE_SIM && (pos & 15) == 0) {
-        word = nextword;
-        const int kw = (pos >> 4) + 1;
-        nextword = (kw < A.words && kw * 16 < plen) ? A.ops[(item * A.words + kw) * A.stage_stride + s] : 0u;
-      }
     }
     __syncwarp();
 
-    // ------------------------------------------------------------------ completion (per segment)
-    bool fin2;
-    if (is_greedy) fin2 = !act || (nF == c.m && nD == c.m && nW == c.m);
-    else fin2 = !act || pos >= plen;
-    const unsigned b_unfin = __ballot_sync(FULL, in_round && !fin2);
-    const unsigned b_prog = __ballot_sync(FULL, op >= 0);
-    const unsigned b_bad = __ballot_sync(FULL, badp);
-    const unsigned b_ovf = __ballot_sync(FULL, ovf);
-    const bool seg_complete = in_round && !(b_unfin & segmask);
-    const bool seg_stuck = in_round && !seg_complete && !(b_prog & segmask);
-    const bool seg_bad = in_round && (b_bad & segmask);
-    const bool seg_ovf = in_round && (b_ovf & segmask);
-    const bool seg_end = seg_complete || seg_stuck || seg_bad || seg_ovf;
-    if (__any_sync(FULL, seg_end)) {
+    // ------------------------------------------------------------------ completion (rare path)
+    const unsigned b_go = __ballot_sync(FULL, go);
+    const bool seg_idle = in_round && !(b_go & segmask);
+    if (__any_sync(FULL, seg_idle || badp || ovf)) {
+      const unsigned b_unfin = __ballot_sync(FULL, live);
+      const unsigned b_bad = __ballot_sync(FULL, badp);
+      const unsigned b_ovf = __ballot_sync(FULL, ovf);
+      const bool seg_bad = in_round && (b_bad & segmask);
+      const bool seg_ovf = in_round && (b_ovf & segmask) && !seg_bad;
+      const bool seg_end = seg_idle || seg_bad || seg_ovf;
+      const bool seg_complete = seg_end && !seg_bad && !seg_ovf && !(b_unfin & segmask);
+      const bool seg_stuck = seg_end && !seg_complete && !seg_ovf && !seg_bad;
       bool badc = false;
       if (kMode == MODE_SIM && seg_complete && act)          // Q29 counts at the end of the walk
         badc = nF != c.m || nD != c.m || (comb != 1 && nW * c.nsub + wsub != c.nsub * nD);
-      if (kMode == MODE_SIM && seg_stuck && !seg_bad && act) {
+      if (kMode == MODE_SIM && seg_stuck && act) {
         // cannot complete: a statically bad plan still reports BAD_PLAN -> scan the rest
         int cF = nF, cD = nD, cW = nW * c.nsub + wsub, cb = comb;
         for (int k = pos; k < plen && !badc; ++k) {
@@ -427,14 +517,14 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       }
       const unsigned b_badc = __ballot_sync(FULL, badc);
       const unsigned b_mem = __ballot_sync(FULL, act && peak > c.mlim);
-      int ms = act ? imax(clk + c.tdp, c.tagate) : 0;   // App. A runtime incl. DP tail / AG
-      int pk = act ? peak : 0;
+      int ms = (in_round && s < c.p) ? imax(clk + c.tdp, c.tagate) : 0;   // App. A runtime incl. DP tail / AG
+      int pk = (in_round && s < c.p) ? peak : 0;
       for (int d = 1; d < W; d <<= 1) {
         ms = imax(ms, __shfl_xor_sync(FULL, ms, d, W));
         pk = imax(pk, __shfl_xor_sync(FULL, pk, d, W));
       }
       if (seg_end) {
-        int st = 0;
+        int st;
         bool completed = false;
         if (seg_bad || (b_badc & segmask)) st = CPI_BAD_PLAN;
         else if (seg_ovf) st = -1;
@@ -443,12 +533,13 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         if (st == -1) {
           // an F lead exceeded the ring: the item is re-run by the global-ring fix-up pass
           if (kMode == MODE_SWEEP) {
-            if (s == 0) A.keys[item] = KEY_OVER;                     // host sizes R so this never happens
-            need_load = true;
-          } else {
-            if (s == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
-            need_load = true;
+            if (s == 0) A.keys[item] = KEY_OVER;                       // host sizes R so this never happens
+          } else if (s == 0) {
+            const int slot = atomicAdd(A.ovf_count, 1);
+            A.ovf_list[slot] = (int32_t)item;
           }
+          need_load = true;
+          cand = 0;
         } else if (kMode == MODE_SWEEP) {
           const bool feas = completed && st == 0;
           if (A.cand_ms && s == 0) A.cand_ms[item * 5 + cand] = feas ? ms : -1;
@@ -457,7 +548,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           cand = -(cand + 2);                  // advance to the first candidate > cand
           cand_greedy = false;
         } else {
-          if (s == 0) {
+          if (s == 0 && CHK(item, n_it, 13)) {
             A.makespan[item] = completed ? (long long)ms : -1LL;
             if (A.peak_mem) A.peak_mem[item] = completed ? pk : -1;
             A.status[item] = st;
@@ -465,17 +556,26 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
               atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
           }
           if (A.stage_stats && s < A.stage_stride) {
-            const int4 v = (completed && act) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
+            const int4 v = (completed && s < c.p) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
             *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = v;
           }
           if (kMode == MODE_GREEDY && s < A.stage_stride) {
-            if (act && (pos & 15)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = word;
-            A.len[item * A.stage_stride + s] = (uint16_t)(act ? pos : 0);
-            word = 0;
+            const bool own = s < c.p;
+            if (PW > 0) {
+              for (int k = 0; own && k * 16 < pos; ++k)
+                if (SOK(plan + (k << 5) + lane, 10) && CHK(item * A.words + k, n_it * A.words, 16))
+                  A.ops[(item * A.words + k) * A.stage_stride + s] = plan[(k << 5) + lane];
+            } else if (own && (pos & 15)) {
+              A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
+            }
+            if (CHK(item, n_it, 11)) A.len[item * A.stage_stride + s] = (uint16_t)(own ? pos : 0);
+            emitw = 0;
           }
           need_load = true;
         }
+        if (use_tma && need_load) cur_buf ^= 1;
       }
+      any_load = __any_sync(FULL, need_load || (kMode == MODE_SWEEP && item >= 0 && cand < 0));
     }
   }
 }
@@ -518,3 +618,10 @@ int device_sm_count() {
 }
 
 }  // namespace cpk
+
+#ifdef CP_DEBUG
+extern "C" int cp_debug_read(int* out8) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out8, cpk::cp_dbg, 8 * sizeof(int));
+}
+#endif

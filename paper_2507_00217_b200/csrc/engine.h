@@ -20,7 +20,10 @@ struct Args {
   int32_t n_items;
   // lane geometry
   int32_t seg_lg;          // segment width W = 1 << seg_lg (>= p of every item)
-  int32_t ring_lg;         // arrival-ring slots R = 1 << ring_lg
+  int32_t ring_slots;      // arrival-ring slots R (>= every producer->consumer lead)
+  int32_t plan_words;      // plan words staged in shared memory per buffer (0: plans read from global)
+  int32_t smem_words_per_warp;
+  int32_t tma;             // plan rows fetched by TMA bulk copies, double-buffered (one item per warp)
   int32_t* ring_g;         // global rings (ring_global launches): [warps][2][R][32]
   // plans
   uint32_t* ops;
