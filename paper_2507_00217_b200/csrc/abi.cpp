@@ -78,7 +78,7 @@ int launch_pass(cpk::Mode mode, bool ring_global, cpk::Args& a, long long n_task
   const size_t smem = per_warp * wpb;
   if (smem > kMaxSmemPerBlock) return CP_EUNSUPPORTED;
   const int threads = 32 * wpb;
-  const int bps = cpk::engine_blocks_per_sm(mode, false, threads, smem);
+  const int bps = cpk::engine_blocks_per_sm(mode, false, threads, smem, a.t_start != nullptr);
   const long long need = (n_tasks + (long long)nseg * wpb - 1) / ((long long)nseg * wpb);
   const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
   return cpk::launch_engine(mode, false, a, blocks, threads, smem, stream) == cudaSuccess ? CP_OK : CP_ECUDA;

@@ -99,8 +99,10 @@ struct LaneCfg {       // per-lane (stage) instance fields
   int P, Q;            // greedy lookahead: exclusive prefix of (tf+bwF+latF), inclusive prefix of (td+bwB+latB)
 };
 
-// smem layout per warp: [ringF R*32][ringD R*32][plan 2*PW*32][2 mbarriers]
-template <int kMode, bool kRingGlobal>
+// smem layout per warp (32-bit words, integer offsets from the warp base):
+//   [ringF R*32][ringD R*32][plan 2*PW*32][2 mbarriers]   (rings live in global memory in
+//   the fix-up pass, kRingGlobal)
+template <int kMode, bool kRingGlobal, bool kTimeline>
 __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Args A) {
   extern __shared__ __align__(128) int32_t smem[];
   const int lane = threadIdx.x & 31;
@@ -114,30 +116,31 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   const int R = A.ring_slots;
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  int32_t* wsm = smem + (size_t)wib * A.smem_words_per_warp;
-  int32_t* ringF = kRingGlobal ? A.ring_g + gwarp * (2LL * R * 32) : wsm;
-  int32_t* ringD = ringF + R * 32;
-  const int PW = A.plan_words;                       // plan words staged in smem (0: read from global)
-  uint32_t* plan = reinterpret_cast<uint32_t*>(wsm + (kRingGlobal ? 0 : 2 * R * 32));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(plan + 2 * PW * 32);
+  const int wbase = wib * A.smem_words_per_warp;      // this warp's smem window (words)
+  int32_t* const rg = kRingGlobal ? A.ring_g + gwarp * (2LL * R * 32) : nullptr;
+  const int RW = R * 32;                               // D ring starts RW words after the F ring
+  const int PW = A.plan_words;                         // plan words staged in smem (0: read from global)
+  const int pbase = wbase + (kRingGlobal ? 0 : 2 * RW);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + pbase + 2 * PW * 32);
+  uint32_t* const plan = reinterpret_cast<uint32_t*>(smem + pbase);
   const bool use_tma = (kMode == MODE_SIM) && A.tma && PW > 0;   // one item per warp, rows contiguous [words][32]
   const uint32_t plan_bytes = (uint32_t)A.words * 32u * 4u;
+  // ring accessors: offsets are relative to the F ring of this warp
+  auto ring_ld = [&](int off) -> int { return kRingGlobal ? rg[off] : smem[wbase + off]; };
+  auto ring_st = [&](int off, int v) { if (kRingGlobal) rg[off] = v; else smem[wbase + off] = v; };
 
   long long task = gwarp * nseg + seg;
   const long long task_stride = nwarps * nseg;
 #ifdef CP_DEBUG
   const long long s_lim = (long long)(blockDim.x >> 5) * A.smem_words_per_warp;
-  const long long g_lim = nwarps * 2LL * R * 32;
   long long item = -1;
-  auto SOK = [&](const void* p, int tag) -> bool {
-    const int32_t* q = (const int32_t*)p;
-    if (kRingGlobal && q >= A.ring_g && q < A.ring_g + g_lim) return true;
-    return dbg_ok(q - smem, s_lim, tag, item);
-  };
+  auto ROK = [&](int off, int tag) -> bool { return dbg_ok(kRingGlobal ? off : wbase + off, kRingGlobal ? 2LL * RW : s_lim, tag, item); };
+  auto POK = [&](int off, int tag) -> bool { return dbg_ok(pbase + off, s_lim, tag, item); };
   const long long n_it = kMode == MODE_SWEEP ? A.pt_hi : A.n_items;
 #else
   long long item = -1;
-#define SOK(p, tag) true
+#define ROK(off, tag) true
+#define POK(off, tag) true
 #endif
 
   auto item_of = [&](long long t) -> long long {
@@ -165,6 +168,8 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   int first = 0, busy = 0, pos = 0, plen = 0, comb = 0, last_fd = 0;
   uint32_t emitw = 0;
   bool ovf = false;
+  int fmask = 0, dmask = 0;               // -1 where the lane consumes F (s > 0) / D (s < p-1) arrivals
+  bool fmask_next = false;                // the lane sends F blocks (s < p-1)
   // sweep: current candidate (>= 0), or -(c+1) = "advance to the first candidate >= c"
   int cand = 0;
   bool cand_greedy = (kMode == MODE_GREEDY);
@@ -237,6 +242,9 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           c.wr = c.tw % imax(c.nsub, 1);
           c.tB = c.td + c.tw;
           c.mB = c.md + c.mw;
+          fmask = (s > 0) ? -1 : 0;
+          dmask = (s < c.p - 1) ? -1 : 0;
+          fmask_next = s < c.p - 1;
           plen = 0;
           if (kMode == MODE_SIM && s < c.p && s < A.stage_stride) {
             plen = A.len[item * A.stage_stride + s];
@@ -312,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
             }
           } else if (just_loaded && !need_load && s < c.p) {
             for (int k = 0; k < A.words && k * 16 < plen; ++k)
-              if (SOK(plan + k * 32 + lane, 14) && CHK(item * A.words + k, n_it * A.words, 15))
+              if (POK(k * 32 + lane, 14) && CHK(item * A.words + k, n_it * A.words, 15))
                 plan[k * 32 + lane] = A.ops[(item * A.words + k) * A.stage_stride + s];
           }
           __syncwarp();
@@ -364,33 +372,32 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
     const bool in_round = item >= 0;
     const bool is_greedy = (kMode == MODE_GREEDY) || (kMode == MODE_SWEEP && cand_greedy);
     const bool act = in_round && s < c.p && !ovf;
-    const bool live = act && (is_greedy ? (nW < c.m || nD < c.m || nF < c.m) : pos < plen);
+    // greedy: W_{m-1} is a stage's last block, so the stage is done iff nW == m
+    const bool live = act && (is_greedy ? nW < c.m : pos < plen);
 
     const int leftF = __shfl_up_sync(FULL, nF, 1, W);
     const int rightD = __shfl_down_sync(FULL, nD, 1, W);
-    const bool lastS = s == c.p - 1;
-    const bool knowF = nF < c.m && (s == 0 || leftF > nF);
-    const bool knowD = nD < c.m && (lastS ? nF > nD : rightD > nD);
+    const bool knowF = nF < c.m && (fmask == 0 || leftF > nF);
+    const bool knowD = nD < c.m && (dmask == 0 ? nF > nD : rightD > nD);
 
     bool go = false, isF = false, isW = false, isB = false, badp = false;
     int start = 0;
     if (kMode != MODE_GREEDY) {
-      // ---- plan-driven selection
+      // ---- plan-driven selection: next entry of this stage's row
       int code;
       if (kMode == MODE_SIM) {
         const int pq = live ? pos : 0;       // finished rows may sit at pos == 16*words: never index past them
-        const uint32_t wv = (PW > 0) ? (SOK(plan + cur_buf * PW * 32 + ((pq >> 4) << 5) + lane, 1)
-                                            ? plan[cur_buf * PW * 32 + ((pq >> 4) << 5) + lane] : 0u)
-                                     : (live && CHK(item * A.words + (pq >> 4), n_it * A.words, 2)
-                                            ? A.ops[(item * A.words + (pq >> 4)) * A.stage_stride + s] : 0u);
+        uint32_t wv;
+        if (PW > 0) wv = POK(cur_buf * PW * 32 + ((pq >> 4) << 5) + lane, 1) ? plan[cur_buf * PW * 32 + ((pq >> 4) << 5) + lane] : 0u;
+        else wv = (live && CHK(item * A.words + (pq >> 4), n_it * A.words, 2)) ? A.ops[(item * A.words + (pq >> 4)) * A.stage_stride + s] : 0u;
         code = (int)((wv >> ((pq & 15) << 1)) & 3u);
       } else {
         code = static_code(cand, s, c.p, c.m, pos);
       }
       const bool cF = code == (int)CP_OP_F, cW = code == (int)CP_OP_W, cB = code == (int)CP_OP_B;
-      const int* ap = cF ? ringF + slF * 32 + lane : ringD + slD * 32 + lane;
-      const int arr = SOK(ap, 3) ? ap[0] : 0;
-      const int avail = cF ? imax(s == 0 ? 0 : arr, c.tagate) : ((cW || lastS) ? 0 : arr);
+      const int roff = (cF ? (slF << 5) : RW + (slD << 5)) + lane;
+      const int arr = ROK(roff, 3) ? ring_ld(roff) : 0;
+      const int avail = cF ? imax(arr & fmask, c.tagate) : (cW ? 0 : (arr & dmask));
       const bool ready = cF ? knowF : (cW || knowD);
       if (kMode == MODE_SIM) {
         // reading Q29: counts, W prefix <= n_sub * D, stage all-combined or all-split
@@ -406,10 +413,10 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
     }
     if (kMode != MODE_SIM) {
       // ---- greedy selection (Alg. 1 lines 6 and 10, §4.2.2)
-      const int arrF = SOK(ringF + slF * 32 + lane, 4) ? ringF[slF * 32 + lane] : 0;
-      const int arrD = SOK(ringD + slD * 32 + lane, 5) ? ringD[slD * 32 + lane] : 0;
-      const int availF = imax(s == 0 ? 0 : arrF, c.tagate);
-      const int availD = lastS ? 0 : arrD;
+      const int arrF = ROK((slF << 5) + lane, 4) ? ring_ld((slF << 5) + lane) : 0;
+      const int arrD = ROK(RW + (slD << 5) + lane, 5) ? ring_ld(RW + (slD << 5) + lane) : 0;
+      const int availF = imax(arrF & fmask, c.tagate);
+      const int availD = arrD & dmask;
       const bool gl = live && is_greedy;
       const bool hasF = gl && knowF && mem + c.mf <= c.mlim;      // Q15: memory-infeasible F is not eligible
       const bool hasD = gl && knowD;
@@ -426,8 +433,8 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         for (int d = 1; d < W; d <<= 1) {
           const int xu = __shfl_up_sync(FULL, x, d, W);
           const int yd = __shfl_down_sync(FULL, y, d, W);
-          if (s >= d) x = imin(x, xu);
-          if (s + d < W) y = imin(y, yd);
+          x = (s >= d) ? imin(x, xu) : x;
+          y = (s + d < W) ? imin(y, yd) : y;
         }
         const int xe = __shfl_up_sync(FULL, x, 1, W);
         const int ye = __shfl_down_sync(FULL, y, 1, W);
@@ -447,44 +454,46 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       }
     }
 
-    // ------------------------------------------------------------------ execute (branch-free)
-    if (go) {
+    // ------------------------------------------------------------------ execute (pure selects)
+    {
       const bool isDB = !isF && !isW;
       const bool wfin = isW && (wsub + 1 == c.nsub);
       const int dur = isF ? c.tf : (isW ? c.wq + (wsub < c.wr ? 1 : 0) : (isB ? c.tB : c.td));
       const int end = start + dur;
-      first = (pos == 0) ? start : first;
-      busy += dur;
-      clk = end;
-      mem += isF ? c.mf : (isW ? (wfin ? c.mw : 0) : (isB ? c.mB : c.md));
-      peak = imax(peak, mem);
-      if (kMode == MODE_SIM) comb = isF ? comb : (isB ? 1 : 2);
-      last_fd = isF ? 1 : (isDB ? 2 : last_fd);
+      const int dmem = isF ? c.mf : (isW ? (wfin ? c.mw : 0) : (isB ? c.mB : c.md));
       // message through the FIFO link clock (= first fit under UD, App. X1)
-      const int lk = isF ? linkF : linkB;
-      const int nl = imax(end, lk) + (isF ? c.bwF : c.bwB);
-      const bool send = isF ? (s < c.p - 1) : (isDB && s > 0);
-      int* wp = isF ? ringF + slF * 32 + lane + 1 : ringD + slD * 32 + lane - 1;
-      if (send && SOK(wp, 6)) wp[0] = nl + (isF ? c.latF : c.latB);
-      linkF = isF ? nl : linkF;
-      linkB = isDB ? nl : linkB;
-      nF += isF;
-      nD += isDB;
-      slF = isF ? (slF + 1 == R ? 0 : slF + 1) : slF;
-      slD = isDB ? (slD + 1 == R ? 0 : slD + 1) : slD;
-      wsub = isW ? (wfin ? 0 : wsub + 1) : wsub;
-      nW += wfin;
-      if (!kRingGlobal && nF - nD > R) ovf = true;
-      if (kMode != MODE_SWEEP && A.t_start && pos < A.len_stride && CHK(item * A.stage_stride + s, n_it * A.stage_stride, 7))
+      const int nl = imax(end, isF ? linkF : linkB) + (isF ? c.bwF : c.bwB);
+      const int woff = isF ? (slF << 5) + lane + 1 : RW + (slD << 5) + lane - 1;
+      const bool send = go && (isF ? fmask_next : (isDB && fmask != 0));
+      if (send && ROK(woff, 6)) ring_st(woff, nl + (isF ? c.latF : c.latB));
+      if (kTimeline && go && pos < A.len_stride && CHK(item * A.stage_stride + s, n_it * A.stage_stride, 7))
         A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
-      if (kMode == MODE_GREEDY) {
+      if (kMode == MODE_GREEDY && go) {
         const int code = isF ? (int)CP_OP_F : (isW ? (int)CP_OP_W : (int)CP_OP_D);
         emitw |= (uint32_t)code << ((pos & 15) << 1);
-        if (PW > 0) { if (SOK(plan + ((pos >> 4) << 5) + lane, 8)) plan[((pos >> 4) << 5) + lane] = emitw; }
-        else if ((pos & 15) == 15 && CHK(item * A.words + (pos >> 4), n_it * A.words, 9)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
+        if (PW > 0) { if (POK(((pos >> 4) << 5) + lane, 8)) plan[((pos >> 4) << 5) + lane] = emitw; }
+        else if ((pos & 15) == 15 && CHK(item * A.words + (pos >> 4), n_it * A.words, 9))
+          A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
         emitw = ((pos & 15) == 15) ? 0u : emitw;
       }
-      ++pos;
+      const bool gF = go && isF, gD = go && isDB, gW = go && isW;
+      first = (go && pos == 0) ? start : first;
+      clk = go ? end : clk;
+      busy += go ? dur : 0;
+      mem += go ? dmem : 0;
+      peak = imax(peak, mem);
+      linkF = gF ? nl : linkF;
+      linkB = gD ? nl : linkB;
+      nF += gF ? 1 : 0;
+      nD += gD ? 1 : 0;
+      slF = gF ? (slF + 1 == R ? 0 : slF + 1) : slF;
+      slD = gD ? (slD + 1 == R ? 0 : slD + 1) : slD;
+      wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
+      nW += (gW && wfin) ? 1 : 0;
+      if (kMode == MODE_SIM) comb = go && !isF ? (isB ? 1 : 2) : comb;
+      last_fd = gF ? 1 : (gD ? 2 : last_fd);
+      pos += go ? 1 : 0;
+      if (!kRingGlobal) ovf = ovf || (nF - nD > R);
     }
     __syncwarp();
 
@@ -563,7 +572,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
             const bool own = s < c.p;
             if (PW > 0) {
               for (int k = 0; own && k * 16 < pos; ++k)
-                if (SOK(plan + (k << 5) + lane, 10) && CHK(item * A.words + k, n_it * A.words, 16))
+                if (POK((k << 5) + lane, 10) && CHK(item * A.words + k, n_it * A.words, 16))
                   A.ops[(item * A.words + k) * A.stage_stride + s] = plan[(k << 5) + lane];
             } else if (own && (pos & 15)) {
               A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
@@ -580,19 +589,23 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   }
 }
 
-template <int kMode, bool kRG>
-static void* kernel_ptr() { return (void*)k_engine<kMode, kRG>; }
+template <int kMode, bool kRG, bool kTL>
+static void* kernel_ptr() { return (void*)k_engine<kMode, kRG, kTL>; }
 
-static void* pick(Mode mode, bool rg) {
+static void* pick(Mode mode, bool rg, bool tl) {
   switch (mode) {
-    case MODE_SIM: return rg ? kernel_ptr<MODE_SIM, true>() : kernel_ptr<MODE_SIM, false>();
-    case MODE_GREEDY: return rg ? kernel_ptr<MODE_GREEDY, true>() : kernel_ptr<MODE_GREEDY, false>();
-    default: return rg ? kernel_ptr<MODE_SWEEP, true>() : kernel_ptr<MODE_SWEEP, false>();
+    case MODE_SIM:
+      return rg ? (tl ? kernel_ptr<MODE_SIM, true, true>() : kernel_ptr<MODE_SIM, true, false>())
+                : (tl ? kernel_ptr<MODE_SIM, false, true>() : kernel_ptr<MODE_SIM, false, false>());
+    case MODE_GREEDY:
+      return rg ? (tl ? kernel_ptr<MODE_GREEDY, true, true>() : kernel_ptr<MODE_GREEDY, true, false>())
+                : (tl ? kernel_ptr<MODE_GREEDY, false, true>() : kernel_ptr<MODE_GREEDY, false, false>());
+    default: return kernel_ptr<MODE_SWEEP, false, false>();
   }
 }
 
 int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  void* fn = pick(mode, ring_global);
+  void* fn = pick(mode, ring_global, a.t_start != nullptr);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
@@ -602,8 +615,8 @@ int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int th
   return (int)e;
 }
 
-int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem) {
-  void* fn = pick(mode, ring_global);
+int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem, bool timeline) {
+  void* fn = pick(mode, ring_global, timeline);
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;

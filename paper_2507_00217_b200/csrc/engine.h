@@ -51,7 +51,7 @@ struct Args {
 
 // launchers (return cudaError_t as int)
 int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int threads, size_t smem, void* stream);
-int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem);
+int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem, bool timeline);
 int device_sm_count();
 
 constexpr int kThreads = 128;          // 4 warps per block
