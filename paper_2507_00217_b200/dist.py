@@ -18,14 +18,20 @@ def world():
     return 0, 1
 
 
-def sweep(grid, *, cand=False, group=None, stream=None, bounds=None):
-    """cp_sweep(grid) = cost-balanced shard on every rank + all_reduce(MIN) of the keys.
-    Returns (keys [n_points] int64 on every rank, cand_ms of the local shard or None)."""
+def sweep(grid, *, cand=False, group=None, stream=None, bounds=None, shard_fn=None):
+    """cp_sweep(grid) = cost-balanced shard on every rank + all_reduce(MIN) of the int64 keys.
+
+    Returns (keys [n_points] on every rank, cand_ms of the local shard or None).  `shard_fn`
+    (grid, lo, hi) -> (keys, cand_ms) replaces the CUDA shard (tests drive the host logic on CPU)."""
     rank, ws = world()
     cg = api.to_cp_grid(grid)
     if bounds is None:
         bounds = api.sweep_partition(grid, ws, cgrid=cg)
-    keys, cm = api.sweep_shard(grid, bounds[rank], bounds[rank + 1], cand=cand, stream=stream, cgrid=cg)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    if shard_fn is None:
+        keys, cm = api.sweep_shard(grid, lo, hi, cand=cand, stream=stream, cgrid=cg)
+    else:
+        keys, cm = shard_fn(grid, lo, hi)
     if ws > 1:
         dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
     return keys, cm
