@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
 
   uint32_t phase = 0;          // mbarrier parity of each plan buffer (bit b)
   int cur_buf = 0;
+  int plan_off = lane;         // cur_buf * PW * 32 + lane
   if (use_tma) {
     if (lane == 0) { mbar_init(&bars[0]); mbar_init(&bars[1]); }
     __syncwarp();
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   }
 
   LaneCfg c = {};
-  bool need_load = true, any_load = true;
+  bool need_load = true, any_load = true, has_item = false;
   int load_status = 0;
   int zero1 = 0, valid_inst = 0;
   // dynamic state of this lane's stage
@@ -167,7 +168,6 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   int slF = 0, slD = 0;                   // ring slots = nF mod R, nD mod R
   int first = 0, busy = 0, pos = 0, plen = 0, comb = 0, last_fd = 0;
   uint32_t emitw = 0;
-  bool ovf = false;
   int fmask = 0, dmask = 0;               // -1 where the lane consumes F (s > 0) / D (s < p-1) arrivals
   bool fmask_next = false;                // the lane sends F blocks (s < p-1)
   // sweep: current candidate (>= 0), or -(c+1) = "advance to the first candidate >= c"
@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         need_load = false;
         item = item_of(task);
         task += task_stride;
+        has_item = item >= 0;
         if (item >= 0) {
           just_loaded = true;
           int lat_b_s = 0, bw_b_s = 0;   // lane s validates boundary s in both directions
@@ -256,7 +257,6 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = slF = slD = 0;
           first = busy = pos = comb = last_fd = 0;
           emitw = 0;
-          ovf = false;
           best = KEY_NONE;
           cand = -1;
           if (kMode == MODE_SWEEP && A.cand_ms && s == 0)
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
               if (lane == 0 && nxt >= 0)
                 tma_load_1d(plan + (cur_buf ^ 1) * PW * 32, A.ops + nxt * A.words * 32, plan_bytes,
                             &bars[cur_buf ^ 1]);
-              if (need_load) cur_buf ^= 1;        // failed item: its buffer is consumed already
+              if (need_load) { cur_buf ^= 1; plan_off = cur_buf * PW * 32 + lane; }   // failed item
             }
           } else if (just_loaded && !need_load && s < c.p) {
             for (int k = 0; k < A.words && k * 16 < plen; ++k)
@@ -358,7 +358,6 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
               c.wr = c.tw % c.nsub;
               clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = slF = slD = 0;
               first = busy = pos = comb = last_fd = 0;
-              ovf = false;
               plen = (s < c.p && !cand_greedy) ? 2 * c.m : 0;
             }
           }
@@ -369,52 +368,51 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
     }
 
     // ------------------------------------------------------------------ one round
-    const bool in_round = item >= 0;
+    const bool in_round = has_item;                    // segment-uniform
     const bool is_greedy = (kMode == MODE_GREEDY) || (kMode == MODE_SWEEP && cand_greedy);
-    const bool act = in_round && s < c.p && !ovf;
     // greedy: W_{m-1} is a stage's last block, so the stage is done iff nW == m
-    const bool live = act && (is_greedy ? nW < c.m : pos < plen);
+    const bool live = in_round && s < c.p && (is_greedy ? nW < c.m : pos < plen);
 
     const int leftF = __shfl_up_sync(FULL, nF, 1, W);
     const int rightD = __shfl_down_sync(FULL, nD, 1, W);
-    const bool knowF = nF < c.m && (fmask == 0 || leftF > nF);
+    // a lane's next F/D input is known once its producer has emitted it; an F additionally needs
+    // room in the consumer's ring (lead <= R) -- a full ring stalls the lane and the
+    // rare path hands the item to the global-ring fix-up pass
+    const bool roomF = kRingGlobal || (nF - nD < R);
+    const bool knowF = nF < c.m && (fmask == 0 || leftF > nF) && roomF;
     const bool knowD = nD < c.m && (dmask == 0 ? nF > nD : rightD > nD);
 
-    bool go = false, isF = false, isW = false, isB = false, badp = false;
+    bool go = false, isF = false, isW = false, isB = false;
     int start = 0;
     if (kMode != MODE_GREEDY) {
-      // ---- plan-driven selection: next entry of this stage's row
+      // ---- plan-driven selection: next entry of this stage's row.  Entries that violate the
+      // static rules (Q29) are simply never ready; a stalled item is classified on the rare path.
       int code;
       if (kMode == MODE_SIM) {
         const int pq = live ? pos : 0;       // finished rows may sit at pos == 16*words: never index past them
         uint32_t wv;
-        if (PW > 0) wv = POK(cur_buf * PW * 32 + ((pq >> 4) << 5) + lane, 1) ? plan[cur_buf * PW * 32 + ((pq >> 4) << 5) + lane] : 0u;
+        if (PW > 0) wv = POK(plan_off + ((pq >> 4) << 5), 1) ? plan[plan_off + ((pq >> 4) << 5)] : 0u;
         else wv = (live && CHK(item * A.words + (pq >> 4), n_it * A.words, 2)) ? A.ops[(item * A.words + (pq >> 4)) * A.stage_stride + s] : 0u;
         code = (int)((wv >> ((pq & 15) << 1)) & 3u);
       } else {
         code = static_code(cand, s, c.p, c.m, pos);
       }
       const bool cF = code == (int)CP_OP_F, cW = code == (int)CP_OP_W, cB = code == (int)CP_OP_B;
-      const int roff = (cF ? (slF << 5) : RW + (slD << 5)) + lane;
+      const int roff = cF ? lane + (slF << 5) : RW + lane + (slD << 5);
       const int arr = ROK(roff, 3) ? ring_ld(roff) : 0;
       const int avail = cF ? imax(arr & fmask, c.tagate) : (cW ? 0 : (arr & dmask));
-      const bool ready = cF ? knowF : (cW || knowD);
-      if (kMode == MODE_SIM) {
-        // reading Q29: counts, W prefix <= n_sub * D, stage all-combined or all-split
-        badp = live && (cF ? nF >= c.m
-                           : (cW ? (nW * c.nsub + wsub >= c.nsub * nD || comb == 1)
-                                 : (nD >= c.m || (cB ? comb == 2 : comb == 1))));
-      }
+      bool ready = cF ? knowF : (cW ? (nW * c.nsub + wsub < c.nsub * nD) : knowD);
+      if (kMode == MODE_SIM) ready = ready && (cB ? comb != 2 : (cF || comb != 1));
       if (!is_greedy) {
-        go = live && ready && !badp;
+        go = live && ready;
         isF = cF; isW = cW; isB = cB;
         start = imax(clk, avail);
       }
     }
     if (kMode != MODE_SIM) {
       // ---- greedy selection (Alg. 1 lines 6 and 10, §4.2.2)
-      const int arrF = ROK((slF << 5) + lane, 4) ? ring_ld((slF << 5) + lane) : 0;
-      const int arrD = ROK(RW + (slD << 5) + lane, 5) ? ring_ld(RW + (slD << 5) + lane) : 0;
+      const int arrF = ROK(lane + (slF << 5), 4) ? ring_ld(lane + (slF << 5)) : 0;
+      const int arrD = ROK(RW + lane + (slD << 5), 5) ? ring_ld(RW + lane + (slD << 5)) : 0;
       const int availF = imax(arrF & fmask, c.tagate);
       const int availD = arrD & dmask;
       const bool gl = live && is_greedy;
@@ -463,7 +461,8 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       const int dmem = isF ? c.mf : (isW ? (wfin ? c.mw : 0) : (isB ? c.mB : c.md));
       // message through the FIFO link clock (= first fit under UD, App. X1)
       const int nl = imax(end, isF ? linkF : linkB) + (isF ? c.bwF : c.bwB);
-      const int woff = isF ? (slF << 5) + lane + 1 : RW + (slD << 5) + lane - 1;
+      const int sl = isF ? slF : slD;
+      const int woff = (isF ? lane + 1 : RW + lane - 1) + (sl << 5);
       const bool send = go && (isF ? fmask_next : (isDB && fmask != 0));
       if (send && ROK(woff, 6)) ring_st(woff, nl + (isF ? c.latF : c.latB));
       if (kTimeline && go && pos < A.len_stride && CHK(item * A.stage_stride + s, n_it * A.stage_stride, 7))
@@ -477,6 +476,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         emitw = ((pos & 15) == 15) ? 0u : emitw;
       }
       const bool gF = go && isF, gD = go && isDB, gW = go && isW;
+      const int sl1 = (sl + 1 == R) ? 0 : sl + 1;
       first = (go && pos == 0) ? start : first;
       clk = go ? end : clk;
       busy += go ? dur : 0;
@@ -486,34 +486,30 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       linkB = gD ? nl : linkB;
       nF += gF ? 1 : 0;
       nD += gD ? 1 : 0;
-      slF = gF ? (slF + 1 == R ? 0 : slF + 1) : slF;
-      slD = gD ? (slD + 1 == R ? 0 : slD + 1) : slD;
+      slF = gF ? sl1 : slF;
+      slD = gD ? sl1 : slD;
       wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
       nW += (gW && wfin) ? 1 : 0;
-      if (kMode == MODE_SIM) comb = go && !isF ? (isB ? 1 : 2) : comb;
-      last_fd = gF ? 1 : (gD ? 2 : last_fd);
+      if (kMode == MODE_SIM) comb = (go && !isF) ? (isB ? 1 : 2) : comb;
+      if (kMode != MODE_SIM) last_fd = gF ? 1 : (gD ? 2 : last_fd);
       pos += go ? 1 : 0;
-      if (!kRingGlobal) ovf = ovf || (nF - nD > R);
     }
     __syncwarp();
 
     // ------------------------------------------------------------------ completion (rare path)
     const unsigned b_go = __ballot_sync(FULL, go);
-    const bool seg_idle = in_round && !(b_go & segmask);
-    if (__any_sync(FULL, seg_idle || badp || ovf)) {
+    const bool seg_idle = in_round && !(b_go & segmask);      // no block executed in this segment
+    if (__any_sync(FULL, seg_idle)) {
+      const bool act = in_round && s < c.p;
       const unsigned b_unfin = __ballot_sync(FULL, live);
-      const unsigned b_bad = __ballot_sync(FULL, badp);
-      const unsigned b_ovf = __ballot_sync(FULL, ovf);
-      const bool seg_bad = in_round && (b_bad & segmask);
-      const bool seg_ovf = in_round && (b_ovf & segmask) && !seg_bad;
-      const bool seg_end = seg_idle || seg_bad || seg_ovf;
-      const bool seg_complete = seg_end && !seg_bad && !seg_ovf && !(b_unfin & segmask);
-      const bool seg_stuck = seg_end && !seg_complete && !seg_ovf && !seg_bad;
+      const unsigned b_ring = __ballot_sync(FULL, act && !kRingGlobal && nF - nD >= R && nF < c.m);
+      const bool seg_complete = seg_idle && !(b_unfin & segmask);
+      const bool seg_stuck = seg_idle && !seg_complete;
       bool badc = false;
       if (kMode == MODE_SIM && seg_complete && act)          // Q29 counts at the end of the walk
         badc = nF != c.m || nD != c.m || (comb != 1 && nW * c.nsub + wsub != c.nsub * nD);
       if (kMode == MODE_SIM && seg_stuck && act) {
-        // cannot complete: a statically bad plan still reports BAD_PLAN -> scan the rest
+        // cannot continue: a statically bad plan reports BAD_PLAN (precedence) -> scan the rest
         int cF = nF, cD = nD, cW = nW * c.nsub + wsub, cb = comb;
         for (int k = pos; k < plen && !badc; ++k) {
           const uint32_t wv = A.ops[(item * A.words + (k >> 4)) * A.stage_stride + s];
@@ -526,21 +522,21 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       }
       const unsigned b_badc = __ballot_sync(FULL, badc);
       const unsigned b_mem = __ballot_sync(FULL, act && peak > c.mlim);
-      int ms = (in_round && s < c.p) ? imax(clk + c.tdp, c.tagate) : 0;   // App. A runtime incl. DP tail / AG
-      int pk = (in_round && s < c.p) ? peak : 0;
+      int ms = act ? imax(clk + c.tdp, c.tagate) : 0;   // App. A runtime incl. DP tail / AG
+      int pk = act ? peak : 0;
       for (int d = 1; d < W; d <<= 1) {
         ms = imax(ms, __shfl_xor_sync(FULL, ms, d, W));
         pk = imax(pk, __shfl_xor_sync(FULL, pk, d, W));
       }
-      if (seg_end) {
+      if (seg_idle) {
         int st;
         bool completed = false;
-        if (seg_bad || (b_badc & segmask)) st = CPI_BAD_PLAN;
-        else if (seg_ovf) st = -1;
+        if (b_badc & segmask) st = CPI_BAD_PLAN;
+        else if (seg_stuck && (b_ring & segmask)) st = -1;
         else if (seg_stuck) st = CPI_DEADLOCK;
         else { completed = true; st = (b_mem & segmask) ? CPI_MEM_EXCEEDED : 0; }
         if (st == -1) {
-          // an F lead exceeded the ring: the item is re-run by the global-ring fix-up pass
+          // a stage's F lead reached the ring capacity: re-run the item in the global-ring pass
           if (kMode == MODE_SWEEP) {
             if (s == 0) A.keys[item] = KEY_OVER;                       // host sizes R so this never happens
           } else if (s == 0) {
@@ -582,9 +578,9 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           }
           need_load = true;
         }
-        if (use_tma && need_load) cur_buf ^= 1;
+        if (use_tma && need_load) { cur_buf ^= 1; plan_off = cur_buf * PW * 32 + lane; }
       }
-      any_load = __any_sync(FULL, need_load || (kMode == MODE_SWEEP && item >= 0 && cand < 0));
+      any_load = __any_sync(FULL, need_load || (kMode == MODE_SWEEP && has_item && cand < 0));
     }
   }
 }
