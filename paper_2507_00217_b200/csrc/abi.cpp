@@ -115,6 +115,29 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
 
   const int nseg = 32 >> a.seg_lg;
   a.plan_words = sc->words <= kPlanCapWords ? sc->words : 0;
+#ifndef CP_DEBUG
+  if (mode == cpk::MODE_SIM && nseg == 1 && sc->stage_stride == 32 && a.plan_words > 0 && !res->t_start) {
+    // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row
+    a.ring_slots = ring_slots_for(in);
+    a.smem_words_per_warp = (2 * a.ring_slots * 32 + 2 * (a.plan_words + 1) * 32 + 32 + 4 + 3) & ~3;
+    const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
+    if (per_warp * 2 <= kMaxSmemPerBlock) {
+      const int wpb = 2, threads = 64;
+      const size_t smem = per_warp * wpb;
+      const int bps = cpk::sim32_blocks_per_sm(threads, smem);
+      const long long need = (n + wpb - 1) / wpb;
+      const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
+      if (cpk::launch_sim32(a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      a.from_list = 1;
+      a.tma = 0;
+      a.ring_slots = big_ring_slots(in);
+      a.ring_g = rings;
+      const int rc = launch_pass(mode, true, a, n, nseg, stream);
+      if (rc) return rc;
+      return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
+    }
+  }
+#endif
   // fast pass: shared-memory rings sized to the in-flight bound, occupancy-sized persistent grid
   a.ring_slots = ring_slots_for(in);
   a.tma = (mode == cpk::MODE_SIM && nseg == 1 && sc->stage_stride == 32 && a.plan_words > 0) ? 1 : 0;

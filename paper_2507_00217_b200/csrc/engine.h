@@ -51,6 +51,9 @@ struct Args {
 
 // launchers (return cudaError_t as int)
 int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int threads, size_t smem, void* stream);
+// fast path of cp_simulate (sim32.cu): one item per warp, stage_stride 32, smem plans (TMA), no timeline
+int launch_sim32(const Args& a, int blocks, int threads, size_t smem, void* stream);
+int sim32_blocks_per_sm(int threads, size_t smem);
 int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem, bool timeline);
 int device_sm_count();
 

@@ -1,0 +1,224 @@
+// sim32.cu -- fast path of cp_simulate for the dominant shape: one item per warp (17..32
+// stages, stage_stride 32), plan rows staged in shared memory by double-buffered TMA bulk
+// copies, arrival rings in shared memory, no per-entry timeline.
+//
+// Same semantics as k_engine<MODE_SIM> (engine.cu), which remains the reference GPU path for
+// every other shape and for the fix-up pass; tests compare both against the CPU oracle.
+// What makes this kernel fast is what it leaves out: the warp is one segment, so the "no block
+// executed this round" test is a single ballot with a warp-uniform branch; the state is the
+// minimum the §3.5 recurrence needs; the plan buffers carry one spare row so finished lanes
+// read without clamping.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "engine.h"
+#include "ptx.cuh"
+
+namespace cpk {
+
+namespace {
+constexpr int32_t INF32 = 1 << 30;
+constexpr unsigned FULLM = 0xffffffffu;
+__device__ __forceinline__ int mn(int a, int b) { return a < b ? a : b; }
+__device__ __forceinline__ int mx(int a, int b) { return a > b ? a : b; }
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args A) {
+  extern __shared__ __align__(128) int32_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int R = A.ring_slots;
+  const int RW = R * 32;
+  const int PW = A.plan_words;                    // == words (host guarantees)
+  const int PWr = PW + 1;                         // one spare row per buffer
+  const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  // per-warp smem (words): [ringF R*32][ringD R*32][plan 2*(PW+1)*32][dummy 32][2 mbarriers]
+  const int wbase = wib * A.smem_words_per_warp;
+  const int pbase0 = wbase + 2 * RW;
+  const int dum_row = 2 * RW + 2 * PWr * 32;      // relative to wbase
+  uint32_t* const plan = reinterpret_cast<uint32_t*>(smem + pbase0);
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + wbase + dum_row + 32);
+  const uint32_t plan_bytes = (uint32_t)A.words * 32u * 4u;
+
+  long long item = gwarp;
+  if (lane == 0) { mbar_init(&bars[0]); mbar_init(&bars[1]); }
+  __syncwarp();
+  if (lane == 0 && item < A.n_items) tma_load_1d(plan, A.ops + item * A.words * 32, plan_bytes, &bars[0]);
+  uint32_t phase = 0;
+  int buf = 0;
+
+  for (; item < A.n_items; item += nwarps) {
+    // ------------------------------------------------------------------ load (warp-uniform)
+    const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
+    const cp_inst_v1* I = A.inst + ii;
+    const int p = I->n_pp, m = I->n_mb, nsub = I->n_sub;
+    const bool zero1 = I->flags & 1;
+    const int s = lane;
+    int tf = 0, td = 0, tw = 0, mf = 0, md = 0, mw = 0, mlim = 0, tdp = 0, tag = 0;
+    int latF = 0, bwF = 0, latB = 0, bwB = 0, latbs = 0, bwbs = 0, plen = 0;
+    if (s < p) {
+      tf = I->t_f[s]; td = I->t_d[s]; tw = I->t_w[s];
+      mf = I->m_f[s]; md = I->m_d[s]; mw = I->m_w[s]; mlim = I->m_lim[s];
+      tdp = I->t_dp[s]; tag = I->t_ag[s];
+      if (s < p - 1) { latF = I->lat_f[s]; bwF = I->bw_f[s]; latbs = I->lat_b[s]; bwbs = I->bw_b[s]; }
+      if (s > 0) { latB = I->lat_b[s - 1]; bwB = I->bw_b[s - 1]; }
+      plen = A.len[item * 32 + s];
+    }
+    bool bad = p < 1 || p > CP_MAX_STAGES || m < 1 || nsub < 1;
+    if (!bad && s < p)
+      bad = !(tf > 0 && td > 0 && tw > 0 && tw >= nsub && mf > 0 && md <= 0 && mw <= 0 &&
+              (long long)mf + md + mw == 0 && mlim >= mf && tdp >= 0 && tag >= 0 && latF >= 0 && bwF >= 0 &&
+              latbs >= 0 && bwbs >= 0);
+    if (!zero1) tag = 0;
+    long long u = (s < p && !bad) ? (long long)m * ((long long)tf + td + tw) + tag + tdp +
+                                        (long long)m * ((long long)latF + bwF + latB + bwB)
+                                  : 0;
+    for (int d = 16; d > 0; d >>= 1) u += __shfl_xor_sync(FULLM, u, d);
+    int st0 = 0;
+    if (__any_sync(FULLM, bad)) st0 = CPI_BAD_INSTANCE;
+    else if (__any_sync(FULLM, plen > 16 * A.words)) st0 = CPI_BAD_PLAN;
+    else if (m > CP_MAX_MB || nsub > CP_MAX_SUB || u >= (long long)INF32) st0 = CPI_OVERFLOW;
+    // this item's rows were prefetched into plan[buf]: wait, then prefetch the next item's
+    mbar_wait(&bars[buf], (phase >> buf) & 1u);
+    phase ^= 1u << buf;
+    if (lane == 0 && item + nwarps < A.n_items)
+      tma_load_1d(plan + (buf ^ 1) * PWr * 32, A.ops + (item + nwarps) * A.words * 32, plan_bytes, &bars[buf ^ 1]);
+    buf ^= 1;
+    if (st0) {
+      if (lane == 0) {
+        A.makespan[item] = -1;
+        if (A.peak_mem) A.peak_mem[item] = -1;
+        A.status[item] = st0;
+      }
+      if (A.stage_stats) *reinterpret_cast<int4*>(A.stage_stats + (item * 32 + s) * 4) = make_int4(0, 0, 0, 0);
+      __syncwarp();
+      continue;
+    }
+    const int wq = tw / nsub, wr = tw % nsub, tB = td + tw, mB = md + mw;
+    const int fmask = s > 0 ? -1 : 0;             // lane consumes F arrivals
+    const int dmask = s < p - 1 ? -1 : 0;         // lane consumes D arrivals
+    const bool sendF = s < p - 1, sendD = s > 0 && s < p;
+    // integer smem indices (shared window addressing, no generic pointers in the loop)
+    const int iF = wbase + lane;                  // own F column
+    const int iD = wbase + RW + lane;             // own D column
+    const int iDum = wbase + dum_row + lane;      // store sink for lanes that send nothing
+    const int iP = pbase0 + (buf ^ 1) * PWr * 32 + lane;   // this item's plan column (buf already flipped)
+
+    // ------------------------------------------------------------------ rounds
+    int clk = 0, mem = 0, peak = 0, busy = 0, first = 0, pos = 0;
+    int nF = 0, nD = 0, nW = 0, wsub = 0, slF = 0, slD = 0, linkF = 0, linkB = 0, comb = 0;
+    uint32_t wv = (uint32_t)smem[iP];             // plan word of entry `pos`, prefetched one round ahead
+    for (;;) {
+      const int leftF = __shfl_up_sync(FULLM, nF, 1);
+      const int rightD = __shfl_down_sync(FULLM, nD, 1);
+      const int aF = smem[iF + (slF << 5)];       // both ring heads, independent of the entry type
+      const int aD = smem[iD + (slD << 5)];
+      const int code = (int)((wv >> ((pos & 15) << 1)) & 3u);
+      const bool isF = code == (int)CP_OP_F, isW = code == (int)CP_OP_W, isB = code == (int)CP_OP_B;
+      const bool isDB = !isF && !isW;
+      // readiness: input produced; ring room (lead <= R); Q29 rules (a violating entry stalls)
+      const bool knowF = nF < m && (fmask == 0 || leftF > nF) && nF - nD < R;
+      const bool knowD = nD < m && (dmask == 0 ? nF > nD : rightD > nD) && (isB ? comb != 2 : comb != 1);
+      const bool wok = nW * nsub + wsub < nsub * nD && comb != 1;
+      const bool go = pos < plen && (isF ? knowF : (isW ? wok : knowD));
+      const int avail = isF ? mx(aF & fmask, tag) : (isW ? 0 : (aD & dmask));
+      const int start = mx(clk, avail);
+      const bool wfin = isW && wsub + 1 == nsub;
+      const int dur = isF ? tf : (isW ? wq + (wsub < wr ? 1 : 0) : (isB ? tB : td));
+      const int dm = isF ? mf : (isW ? (wfin ? mw : 0) : (isB ? mB : md));
+      const int end = start + dur;
+      const int nl = mx(end, isF ? linkF : linkB) + (isF ? bwF : bwB);   // FIFO link clock (App. X1)
+      const bool send = go && (isF ? sendF : (isDB && sendD));
+      const int iw = send ? (isF ? iF + (slF << 5) + 1 : iD + (slD << 5) - 1) : iDum;
+      smem[iw] = nl + (isF ? latF : latB);
+      const bool gF = go && isF, gD = go && isDB, gW = go && isW;
+      first = (go && pos == 0) ? start : first;
+      clk = go ? end : clk;
+      busy += go ? dur : 0;
+      mem += go ? dm : 0;
+      peak = mx(peak, mem);
+      linkF = gF ? nl : linkF;
+      linkB = gD ? nl : linkB;
+      const int sl = isF ? slF : slD;
+      const int sl1 = sl + 1 == R ? 0 : sl + 1;
+      slF = gF ? sl1 : slF;
+      slD = gD ? sl1 : slD;
+      nF += gF ? 1 : 0;
+      nD += gD ? 1 : 0;
+      wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
+      nW += (gW && wfin) ? 1 : 0;
+      comb = gD ? (isB ? 1 : 2) : comb;
+      pos += go ? 1 : 0;
+      wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];   // next round's word (spare row covers pos == 16*PW)
+      __syncwarp();
+      if (__ballot_sync(FULLM, go) != 0u) continue;   // warp-uniform: some block executed
+
+      // ---------------------------------------------------------------- no progress: classify
+      const bool unfin = pos < plen;
+      const bool complete = !__any_sync(FULLM, unfin);
+      bool badc = false;
+      if (complete) {
+        badc = s < p && (nF != m || nD != m || (comb != 1 && nW * nsub + wsub != nsub * nD));
+      } else if (s < p) {
+        int cF = nF, cD = nD, cW = nW * nsub + wsub, cb = comb;
+        for (int k = pos; k < plen && !badc; ++k) {
+          const uint32_t w2 = A.ops[(item * A.words + (k >> 4)) * 32 + s];
+          const uint32_t c2 = (w2 >> ((k & 15) << 1)) & 3u;
+          if (c2 == CP_OP_F) { badc = cF >= m; ++cF; }
+          else if (c2 == CP_OP_W) { badc = cW >= nsub * cD || cb == 1; ++cW; cb = 2; }
+          else { badc = cD >= m || (c2 == CP_OP_B ? cb == 2 : cb == 1); ++cD; cb = (c2 == CP_OP_B) ? 1 : 2; }
+        }
+        if (!badc) badc = cF != m || cD != m || (cb != 1 && cW != nsub * cD);
+      }
+      int st;
+      if (__any_sync(FULLM, badc)) st = CPI_BAD_PLAN;
+      else if (!complete && __any_sync(FULLM, s < p && nF < m && nF - nD >= R)) st = -1;
+      else if (!complete) st = CPI_DEADLOCK;
+      else st = __any_sync(FULLM, s < p && peak > mlim) ? CPI_MEM_EXCEEDED : 0;
+      if (st == -1) {                            // ring capacity reached: hand to the fix-up pass
+        if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
+        break;
+      }
+      int ms = s < p ? mx(clk + tdp, tag) : 0, pk = s < p ? peak : 0;
+      for (int d = 16; d > 0; d >>= 1) {
+        ms = mx(ms, __shfl_xor_sync(FULLM, ms, d));
+        pk = mx(pk, __shfl_xor_sync(FULLM, pk, d));
+      }
+      const bool done = complete && !(st & CPI_BAD_PLAN);
+      if (lane == 0) {
+        A.makespan[item] = done ? (long long)ms : -1LL;
+        if (A.peak_mem) A.peak_mem[item] = done ? pk : -1;
+        A.status[item] = st;
+        if (A.best_key && st == 0)
+          atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
+      }
+      if (A.stage_stats) {
+        const int4 v = (done && s < p) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(A.stage_stats + (item * 32 + s) * 4) = v;
+      }
+      break;
+    }
+    __syncwarp();
+  }
+}
+
+int launch_sim32(const Args& a, int blocks, int threads, size_t smem, void* stream) {
+  const void* fn = (const void*)k_sim32;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  void* params[] = {(void*)&a};
+  return (int)cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
+}
+
+int sim32_blocks_per_sm(int threads, size_t smem) {
+  const void* fn = (const void*)k_sim32;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;
+  return n > 0 ? n : 1;
+}
+
+}  // namespace cpk
