@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "engine.h"
 #include "ptx.cuh"
 
@@ -105,71 +107,101 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
     const int iDum = wbase + dum_row + lane;      // store sink for lanes that send nothing
     const int iP = pbase0 + (buf ^ 1) * PWr * 32 + lane;   // this item's plan column (buf already flipped)
 
-    // ------------------------------------------------------------------ rounds
-    int clk = 0, mem = 0, peak = 0, busy = 0, first = 0, pos = 0;
-    int nF = 0, nD = 0, nW = 0, wsub = 0, slF = 0, slD = 0, linkF = 0, linkB = 0, comb = 0;
-    uint32_t wv = (uint32_t)smem[iP];             // plan word of entry `pos`, prefetched one round ahead
-    for (;;) {
-      const int leftF = __shfl_up_sync(FULLM, nF, 1);
-      const int rightD = __shfl_down_sync(FULLM, nD, 1);
-      const int aF = smem[iF + (slF << 5)];       // both ring heads, independent of the entry type
-      const int aD = smem[iD + (slD << 5)];
-      const int code = (int)((wv >> ((pos & 15) << 1)) & 3u);
-      const bool isF = code == (int)CP_OP_F, isW = code == (int)CP_OP_W, isB = code == (int)CP_OP_B;
-      const bool isDB = !isF && !isW;
-      // readiness: input produced; ring room (lead <= R); Q29 rules (a violating entry stalls)
-      const bool knowF = nF < m && (fmask == 0 || leftF > nF) && nF - nD < R;
-      const bool knowD = nD < m && (dmask == 0 ? nF > nD : rightD > nD) && (isB ? comb != 2 : comb != 1);
-      const bool wok = nW * nsub + wsub < nsub * nD && comb != 1;
-      const bool go = pos < plen && (isF ? knowF : (isW ? wok : knowD));
-      const int avail = isF ? mx(aF & fmask, tag) : (isW ? 0 : (aD & dmask));
-      const int start = mx(clk, avail);
-      const bool wfin = isW && wsub + 1 == nsub;
-      const int dur = isF ? tf : (isW ? wq + (wsub < wr ? 1 : 0) : (isB ? tB : td));
-      const int dm = isF ? mf : (isW ? (wfin ? mw : 0) : (isB ? mB : md));
-      const int end = start + dur;
-      const int nl = mx(end, isF ? linkF : linkB) + (isF ? bwF : bwB);   // FIFO link clock (App. X1)
-      const bool send = go && (isF ? sendF : (isDB && sendD));
-      const int iw = send ? (isF ? iF + (slF << 5) + 1 : iD + (slD << 5) - 1) : iDum;
-      smem[iw] = nl + (isF ? latF : latB);
-      const bool gF = go && isF, gD = go && isDB, gW = go && isW;
-      first = (go && pos == 0) ? start : first;
-      clk = go ? end : clk;
-      busy += go ? dur : 0;
-      mem += go ? dm : 0;
-      peak = mx(peak, mem);
-      linkF = gF ? nl : linkF;
-      linkB = gD ? nl : linkB;
-      const int sl = isF ? slF : slD;
-      const int sl1 = sl + 1 == R ? 0 : sl + 1;
-      slF = gF ? sl1 : slF;
-      slD = gD ? sl1 : slD;
-      nF += gF ? 1 : 0;
-      nD += gD ? 1 : 0;
-      wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
-      nW += (gW && wfin) ? 1 : 0;
-      comb = gD ? (isB ? 1 : 2) : comb;
-      pos += go ? 1 : 0;
-      wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];   // next round's word (spare row covers pos == 16*PW)
+    // ---- Q29 count / mixing rules, once per row (popcounts over the staged words); the W-prefix
+    // rule stays dynamic (a violating W entry stalls and the rare path classifies the item)
+    bool bad_static = false;
+    if (s < p) {
+      int cF = 0, cB = 0, cD = 0, cW = 0;
+      for (int k = 0; k * 16 < plen; ++k) {
+        const uint32_t w = (uint32_t)smem[iP + (k << 5)];
+        const int n = mn(16, plen - 16 * k);
+        const uint32_t valid = (n == 16 ? 0xffffffffu : ((1u << (2 * n)) - 1u)) & 0x55555555u;
+        const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
+        cF += __popc(~lo & ~hi & valid);
+        cB += __popc(lo & ~hi & valid);
+        cD += __popc(~lo & hi & valid);
+        cW += __popc(lo & hi & valid);
+      }
+      bad_static = cF != m || cB + cD != m || (cB > 0 && cD + cW > 0) || cW != nsub * cD;
+    }
+    if (__any_sync(FULLM, bad_static)) {
+      if (lane == 0) {
+        A.makespan[item] = -1;
+        if (A.peak_mem) A.peak_mem[item] = -1;
+        A.status[item] = CPI_BAD_PLAN;
+      }
+      if (A.stage_stats) *reinterpret_cast<int4*>(A.stage_stats + (item * 32 + s) * 4) = make_int4(0, 0, 0, 0);
       __syncwarp();
-      if (__ballot_sync(FULLM, go) != 0u) continue;   // warp-uniform: some block executed
+      continue;
+    }
 
-      // ---------------------------------------------------------------- no progress: classify
+    // ------------------------------------------------------------------ rounds
+    int clk = 0, mem = 0, peak = 0, first = 0, pos = 0;
+    int nF = 0, nD = 0, went = 0, wcap = 0, wsub = 0, slF = 0, slD = 0, linkF = 0, linkB = 0;
+    uint32_t wv = (uint32_t)smem[iP];             // plan word of entry `pos`, prefetched one round ahead
+    auto rounds = [&](auto n1) {
+      constexpr bool kN1 = decltype(n1)::value;   // n_sub == 1: a W entry is a whole W block
+      for (;;) {
+        const int leftF = __shfl_up_sync(FULLM, nF, 1);
+        const int rightD = __shfl_down_sync(FULLM, nD, 1);
+        const int aF = smem[iF + (slF << 5)];     // both ring heads, independent of the entry type
+        const int aD = smem[iD + (slD << 5)];
+        const int code = (int)((wv >> ((pos & 15) << 1)) & 3u);
+        const bool isF = code == (int)CP_OP_F, isW = code == (int)CP_OP_W, isB = code == (int)CP_OP_B;
+        const bool isDB = !isF && !isW;
+        // readiness: input produced; ring room (lead <= R); W sub-blocks only after their D
+        const bool knowF = (fmask == 0 || leftF > nF) && nF - nD < R;
+        const bool knowD = dmask == 0 ? nF > nD : rightD > nD;
+        const bool go = pos < plen && (isF ? knowF : (isW ? went < wcap : knowD));
+        const int avail = isF ? mx(aF & fmask, tag) : (isW ? 0 : (aD & dmask));
+        const int start = mx(clk, avail);
+        const bool wfin = kN1 ? true : (wsub + 1 == nsub);
+        const int wdur = kN1 ? tw : wq + (wsub < wr ? 1 : 0);
+        const int dur = isF ? tf : (isW ? wdur : (isB ? tB : td));
+        const int dm = isF ? mf : (isW ? (wfin ? mw : 0) : (isB ? mB : md));
+        const int end = start + dur;
+        const int nl = mx(end, isF ? linkF : linkB) + (isF ? bwF : bwB);   // FIFO link clock (App. X1)
+        const bool send = go && (isF ? sendF : (isDB && sendD));
+        const int iw = send ? (isF ? iF + (slF << 5) + 1 : iD + (slD << 5) - 1) : iDum;
+        smem[iw] = nl + (isF ? latF : latB);
+        const bool gF = go && isF, gD = go && isDB, gW = go && isW;
+        first = (go && pos == 0) ? start : first;
+        clk = go ? end : clk;
+        mem += go ? dm : 0;
+        peak = mx(peak, mem);
+        linkF = gF ? nl : linkF;
+        linkB = gD ? nl : linkB;
+        const int sl = isF ? slF : slD;
+        const int sl1 = sl + 1 == R ? 0 : sl + 1;
+        slF = gF ? sl1 : slF;
+        slD = gD ? sl1 : slD;
+        nF += gF ? 1 : 0;
+        nD += gD ? 1 : 0;
+        wcap += gD ? nsub : 0;
+        went += gW ? 1 : 0;
+        if (!kN1) wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
+        pos += go ? 1 : 0;
+        wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];   // next round's word (spare row covers pos == 16*PW)
+        __syncwarp();
+        if (__ballot_sync(FULLM, go) == 0u) break;      // warp-uniform: nothing executed -> classify
+      }
+    };
+    if (nsub == 1) rounds(std::true_type{});
+    else rounds(std::false_type{});
+
+    // ------------------------------------------------------------------ no progress: classify
+    {
       const bool unfin = pos < plen;
       const bool complete = !__any_sync(FULLM, unfin);
       bool badc = false;
-      if (complete) {
-        badc = s < p && (nF != m || nD != m || (comb != 1 && nW * nsub + wsub != nsub * nD));
-      } else if (s < p) {
-        int cF = nF, cD = nD, cW = nW * nsub + wsub, cb = comb;
+      if (!complete && s < p) {
+        // cannot continue: a W entry ahead of its D (prefix rule) reports BAD_PLAN -> scan the rest
+        int cD = nD, cW = went;
         for (int k = pos; k < plen && !badc; ++k) {
-          const uint32_t w2 = A.ops[(item * A.words + (k >> 4)) * 32 + s];
-          const uint32_t c2 = (w2 >> ((k & 15) << 1)) & 3u;
-          if (c2 == CP_OP_F) { badc = cF >= m; ++cF; }
-          else if (c2 == CP_OP_W) { badc = cW >= nsub * cD || cb == 1; ++cW; cb = 2; }
-          else { badc = cD >= m || (c2 == CP_OP_B ? cb == 2 : cb == 1); ++cD; cb = (c2 == CP_OP_B) ? 1 : 2; }
+          const uint32_t c2 = ((uint32_t)smem[iP + ((k >> 4) << 5)] >> ((k & 15) << 1)) & 3u;
+          if (c2 == CP_OP_W) { badc = cW >= nsub * cD; ++cW; }
+          else if (c2 != CP_OP_F) ++cD;
         }
-        if (!badc) badc = cF != m || cD != m || (cb != 1 && cW != nsub * cD);
       }
       int st;
       if (__any_sync(FULLM, badc)) st = CPI_BAD_PLAN;
@@ -178,26 +210,27 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
       else st = __any_sync(FULLM, s < p && peak > mlim) ? CPI_MEM_EXCEEDED : 0;
       if (st == -1) {                            // ring capacity reached: hand to the fix-up pass
         if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
-        break;
+      } else {
+        int ms = s < p ? mx(clk + tdp, tag) : 0, pk = s < p ? peak : 0;
+        for (int d = 16; d > 0; d >>= 1) {
+          ms = mx(ms, __shfl_xor_sync(FULLM, ms, d));
+          pk = mx(pk, __shfl_xor_sync(FULLM, pk, d));
+        }
+        const bool done = complete && !(st & CPI_BAD_PLAN);
+        if (lane == 0) {
+          A.makespan[item] = done ? (long long)ms : -1LL;
+          if (A.peak_mem) A.peak_mem[item] = done ? pk : -1;
+          A.status[item] = st;
+          if (A.best_key && st == 0)
+            atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
+        }
+        if (A.stage_stats) {
+          // a completed valid row executed every block exactly once: busy = m (t_f + t_d + t_w)
+          const int busy = m * (tf + td + tw);
+          const int4 v = (done && s < p) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
+          *reinterpret_cast<int4*>(A.stage_stats + (item * 32 + s) * 4) = v;
+        }
       }
-      int ms = s < p ? mx(clk + tdp, tag) : 0, pk = s < p ? peak : 0;
-      for (int d = 16; d > 0; d >>= 1) {
-        ms = mx(ms, __shfl_xor_sync(FULLM, ms, d));
-        pk = mx(pk, __shfl_xor_sync(FULLM, pk, d));
-      }
-      const bool done = complete && !(st & CPI_BAD_PLAN);
-      if (lane == 0) {
-        A.makespan[item] = done ? (long long)ms : -1LL;
-        if (A.peak_mem) A.peak_mem[item] = done ? pk : -1;
-        A.status[item] = st;
-        if (A.best_key && st == 0)
-          atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
-      }
-      if (A.stage_stats) {
-        const int4 v = (done && s < p) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
-        *reinterpret_cast<int4*>(A.stage_stats + (item * 32 + s) * 4) = v;
-      }
-      break;
     }
     __syncwarp();
   }

@@ -319,3 +319,51 @@ def test_config4_full_size_sampled(O):
         assert (int(ms[i]), int(st[i])) == (w["makespan"], w["status"]), i
     bk = int(r["best_key"][0])
     assert (bk >> 32) == ms.min() and ms[bk & 0xFFFFFFFF] == ms.min()
+
+
+def test_simulate_fast_path_invalid_and_overflow(O):
+    """The one-item-per-warp fast path (k_sim32: p > 16, stride 32, no timeline) on valid,
+    deadlocking, statically bad (counts / mixing), W-before-D, and memory-violating plans (which
+    also overflow the shared-memory rings and go through the global-ring fix-up pass)."""
+    rng = np.random.default_rng(19)
+    big = K.random_instances(400, seed=20, max_p=32, max_m=12)
+    keep = [i for i in range(len(big)) if big.p[i] >= 17][:70]
+    batch = big.take(keep)
+    plans, inst_of = [], []
+    for i in range(len(batch)):
+        d = batch.item(i)
+        base = random_valid_plan(d, rng)
+        for kind in range(7):
+            pl = [list(x) for x in base]
+            s = int(rng.integers(d["p"]))
+            if kind == 1 and len(pl[s]) > 1:
+                k = int(rng.integers(len(pl[s]) - 1)); pl[s][k], pl[s][k + 1] = pl[s][k + 1], pl[s][k]
+            elif kind == 2:
+                pl[s].pop(int(rng.integers(len(pl[s]))))
+            elif kind == 3:
+                pl[s].insert(int(rng.integers(len(pl[s]) + 1)), 0)
+            elif kind == 4:
+                pl[s][int(rng.integers(len(pl[s])))] = 1
+            elif kind == 5 and 3 in pl[s]:                # move the first W to the front (W before its D)
+                j = pl[s].index(3); pl[s].insert(0, pl[s].pop(j))
+            elif kind == 6:
+                for _ in range(4):
+                    s2 = int(rng.integers(d["p"]))
+                    if len(pl[s2]) > 1:
+                        k = int(rng.integers(len(pl[s2]) - 1)); pl[s2][k], pl[s2][k + 1] = pl[s2][k + 1], pl[s2][k]
+            plans.append(pl)
+            inst_of.append(i)
+    cut = InstanceBatch.concat([batch, batch.take(np.arange(len(batch)))])
+    n0 = len(batch)
+    cut.m_lim[n0:] = np.maximum(cut.m_f[n0:], cut.m_lim[n0:] // 3)
+    for i in range(n0):
+        plans.append(random_valid_plan(batch.item(i), rng))
+        inst_of.append(n0 + i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(cut, ops, ln, inst_of, stats=True, timeline=False)
+    codes, lens = unpack_plans(ops, ln)
+    seen = set()
+    for j, i in enumerate(inst_of):
+        w = compare_sim(O, cut.item(i), codes[j], lens[j], r, j, codes.shape[2], timeline=False)
+        seen.add(w["status"])
+    assert {0, 1, 2, 4} <= seen, seen
