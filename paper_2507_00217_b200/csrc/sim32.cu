@@ -136,23 +136,26 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
     }
 
     // ------------------------------------------------------------------ rounds
+    // ring heads are kept as pre-scaled word indices (own column + slot*32), wrapping at R slots
+    const int iFend = iF + RW, iDend = iD + RW;
     int clk = 0, mem = 0, peak = 0, first = 0, pos = 0;
-    int nF = 0, nD = 0, went = 0, wcap = 0, wsub = 0, slF = 0, slD = 0, linkF = 0, linkB = 0;
+    int nF = 0, nD = 0, went = 0, wcap = 0, wsub = 0, hF = iF, hD = iD, linkF = 0, linkB = 0;
     uint32_t wv = (uint32_t)smem[iP];             // plan word of entry `pos`, prefetched one round ahead
     auto rounds = [&](auto n1) {
       constexpr bool kN1 = decltype(n1)::value;   // n_sub == 1: a W entry is a whole W block
       for (;;) {
         const int leftF = __shfl_up_sync(FULLM, nF, 1);
         const int rightD = __shfl_down_sync(FULLM, nD, 1);
-        const int aF = smem[iF + (slF << 5)];     // both ring heads, independent of the entry type
-        const int aD = smem[iD + (slD << 5)];
-        const int code = (int)((wv >> ((pos & 15) << 1)) & 3u);
-        const bool isF = code == (int)CP_OP_F, isW = code == (int)CP_OP_W, isB = code == (int)CP_OP_B;
-        const bool isDB = !isF && !isW;
+        const int aF = smem[hF];                  // both ring heads, independent of the entry type
+        const int aD = smem[hD];
+        const unsigned code = (wv >> ((pos & 15) << 1)) & 3u;
+        const bool isF = code == CP_OP_F, isW = code == CP_OP_W, isB = code == CP_OP_B;
+        const bool isDB = !isF & !isW;
         // readiness: input produced; ring room (lead <= R); W sub-blocks only after their D
-        const bool knowF = (fmask == 0 || leftF > nF) && nF - nD < R;
-        const bool knowD = dmask == 0 ? nF > nD : rightD > nD;
-        const bool go = pos < plen && (isF ? knowF : (isW ? went < wcap : knowD));
+        const bool knowF = ((fmask == 0) | (leftF > nF)) & (nF - nD < R);
+        const bool knowD = (dmask == 0) ? (nF > nD) : (rightD > nD);
+        const bool wok = kN1 ? (went < nD) : (went < wcap);
+        const bool go = (pos < plen) & (isF ? knowF : (isW ? wok : knowD));
         const int avail = isF ? mx(aF & fmask, tag) : (isW ? 0 : (aD & dmask));
         const int start = mx(clk, avail);
         const bool wfin = kN1 ? true : (wsub + 1 == nsub);
@@ -161,26 +164,26 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
         const int dm = isF ? mf : (isW ? (wfin ? mw : 0) : (isB ? mB : md));
         const int end = start + dur;
         const int nl = mx(end, isF ? linkF : linkB) + (isF ? bwF : bwB);   // FIFO link clock (App. X1)
-        const bool send = go && (isF ? sendF : (isDB && sendD));
-        const int iw = send ? (isF ? iF + (slF << 5) + 1 : iD + (slD << 5) - 1) : iDum;
-        smem[iw] = nl + (isF ? latF : latB);
-        const bool gF = go && isF, gD = go && isDB, gW = go && isW;
-        first = (go && pos == 0) ? start : first;
+        const bool send = go & (isF ? sendF : (isDB & sendD));
+        smem[send ? (isF ? hF + 1 : hD - 1) : iDum] = nl + (isF ? latF : latB);
+        const bool gF = go & isF, gD = go & isDB;
+        first = (go & (pos == 0)) ? start : first;
         clk = go ? end : clk;
         mem += go ? dm : 0;
         peak = mx(peak, mem);
         linkF = gF ? nl : linkF;
         linkB = gD ? nl : linkB;
-        const int sl = isF ? slF : slD;
-        const int sl1 = sl + 1 == R ? 0 : sl + 1;
-        slF = gF ? sl1 : slF;
-        slD = gD ? sl1 : slD;
-        nF += gF ? 1 : 0;
-        nD += gD ? 1 : 0;
-        wcap += gD ? nsub : 0;
-        went += gW ? 1 : 0;
-        if (!kN1) wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
-        pos += go ? 1 : 0;
+        const int h1 = (isF ? hF : hD) + 32;
+        hF = gF ? (h1 == iFend ? iF : h1) : hF;
+        hD = gD ? (h1 == iDend ? iD : h1) : hD;
+        nF += gF;
+        nD += gD;
+        went += go & isW;
+        if (!kN1) {
+          wcap += gD ? nsub : 0;
+          wsub = (go & isW) ? (wfin ? 0 : wsub + 1) : wsub;
+        }
+        pos += go;
         wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];   // next round's word (spare row covers pos == 16*PW)
         __syncwarp();
         if (__ballot_sync(FULLM, go) == 0u) break;      // warp-uniform: nothing executed -> classify
