@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
     // ------------------------------------------------------------------ rounds
     // ring heads are kept as pre-scaled word indices (own column + slot*32), wrapping at R slots
     const int iFend = iF + RW, iDend = iD + RW;
-    int clk = 0, mem = 0, peak = 0, first = 0, pos = 0;
+    int clk = 0, mem = 0, peak = 0, pos = 0;
     int nF = 0, nD = 0, went = 0, wcap = 0, wsub = 0, hF = iF, hD = iD, linkF = 0, linkB = 0;
     uint32_t wv = (uint32_t)smem[iP];             // plan word of entry `pos`, prefetched one round ahead
     auto rounds = [&](auto n1) {
@@ -167,7 +167,6 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
         const bool send = go & (isF ? sendF : (isDB & sendD));
         smem[send ? (isF ? hF + 1 : hD - 1) : iDum] = nl + (isF ? latF : latB);
         const bool gF = go & isF, gD = go & isDB;
-        first = (go & (pos == 0)) ? start : first;
         clk = go ? end : clk;
         mem += go ? dm : 0;
         peak = mx(peak, mem);
@@ -228,8 +227,17 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
             atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
         }
         if (A.stage_stats) {
-          // a completed valid row executed every block exactly once: busy = m (t_f + t_d + t_w)
+          // a completed valid row executed every block exactly once: busy = m (t_f + t_d + t_w);
+          // every row starts with F_0, whose message opens its link, so first_start is the max-plus
+          // prefix first[s] = max(t_ag[s], first[s-1] + t_f + bw_f + lat_f of s-1) = P_s + max_{k<=s}(ag_k - P_k)
           const int busy = m * (tf + td + tw);
+          const int cfw = s < p ? tf + bwF + latF : 0;
+          int P = cfw;                              // inclusive prefix sum of hop costs
+          for (int d = 1; d < 32; d <<= 1) { const int t = __shfl_up_sync(FULLM, P, d); if (s >= d) P += t; }
+          P -= cfw;                                 // exclusive: P_s
+          int x = (s < p ? tag : 0) - P;
+          for (int d = 1; d < 32; d <<= 1) { const int t = __shfl_up_sync(FULLM, x, d); if (s >= d) x = mx(x, t); }
+          const int first = P + x;
           const int4 v = (done && s < p) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
           *reinterpret_cast<int4*>(A.stage_stats + (item * 32 + s) * 4) = v;
         }
