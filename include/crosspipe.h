@@ -110,9 +110,9 @@ typedef struct {
   int32_t* stage_stats;       /* [n][stage_stride][4] first_start, last_end, busy, peak (nullable) */
   int32_t* t_start;           /* [n][stage_stride][len_stride] start tick of every entry (nullable) */
   int32_t len_stride;
-  int32_t _pad;
-  uint64_t* best_key;         /* [1] nullable: atomic min of (makespan << 32 | i) over items with
-                                 status 0; the caller initializes it to INT64_MAX */
+  int32_t index_base;         /* added to the item index in best_key (chunked calls report global ids) */
+  uint64_t* best_key;         /* [1] nullable: atomic min of (makespan << 32 | (index_base + i)) over
+                                 items with status 0; the caller initializes it to INT64_MAX */
 } cp_results;
 
 #define CP_GRID_MAX_AXIS 128

@@ -9,7 +9,7 @@ from . import _lib
 _lib.load()
 
 from .api import (  # noqa: E402,F401
-    KEY_NONE, KEY_OVER, Instances, decode_key, greedy, pack_instances, quantize, records_to_device, ring_hint,
+    KEY_NONE, KEY_OVER, HostPipeline, Instances, decode_key, greedy, pack_instances, quantize, records_to_device, ring_hint,
     simulate, sweep_partition, sweep_shard, to_cp_grid, validate_record,
 )
 

@@ -48,7 +48,7 @@ class CpSchedules(C.Structure):
 class CpResults(C.Structure):
     _fields_ = [("makespan", C.c_void_p), ("peak_mem", C.c_void_p), ("status", C.c_void_p),
                 ("stage_stats", C.c_void_p), ("t_start", C.c_void_p), ("len_stride", C.c_int32),
-                ("_pad", C.c_int32), ("best_key", C.c_void_p)]
+                ("index_base", C.c_int32), ("best_key", C.c_void_p)]
 
 
 class CpGrid(C.Structure):

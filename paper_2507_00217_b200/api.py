@@ -128,6 +128,61 @@ def simulate(inst: Instances, ops: torch.Tensor, lens: torch.Tensor, inst_of: to
     return r
 
 
+class HostPipeline:
+    """cp_simulate over HOST (pinned) plan buffers with copy/compute overlap.
+
+    The batch is cut into chunks; chunk k+1's host->device copy (copy stream) overlaps chunk k's
+    kernel (compute stream), and results of chunk k stream back while later chunks run.  Every
+    chunk is one cp_simulate call on device views with index_base = chunk start, so best_key
+    carries global schedule ids.  Device buffers and streams are allocated once and reused."""
+
+    def __init__(self, inst: Instances, n: int, words: int, stride: int, chunks: int = 8, device="cuda"):
+        self.inst, self.n, self.chunks = inst, n, max(1, chunks)
+        self.ops_d = torch.empty((n, words, stride), dtype=torch.int32, device=device)
+        self.len_d = torch.empty((n, stride), dtype=torch.int16, device=device)
+        self.r, _ = _results(n, stride, False, False, 0, device, True)
+        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(device) for _ in range(3))
+        self.bounds = [n * k // self.chunks for k in range(self.chunks + 1)]
+        step = max(b - a for a, b in zip(self.bounds, self.bounds[1:]))
+        self.ws = _workspace(0, inst.desc(), step, device)
+        self.words, self.stride = words, stride
+
+    def run(self, ops_h, len_h, makespan_h, peak_h, status_h):
+        """Enqueue one evaluation of the host batch; results land in the pinned host tensors.
+        Returns the device best_key tensor (valid after torch.cuda.synchronize())."""
+        r = self.r
+        cur = torch.cuda.current_stream()
+        self.h2d.wait_stream(cur)
+        self.comp.wait_stream(cur)
+        with torch.cuda.stream(self.comp):
+            r["best_key"].fill_(KEY_NONE)
+        done_in, done_out = [], []
+        for k in range(self.chunks):
+            a, b = self.bounds[k], self.bounds[k + 1]
+            with torch.cuda.stream(self.h2d):
+                self.ops_d[a:b].copy_(ops_h[a:b], non_blocking=True)
+                self.len_d[a:b].copy_(len_h[a:b], non_blocking=True)
+                e = torch.cuda.Event(); e.record(self.h2d); done_in.append(e)
+            self.comp.wait_event(done_in[k])
+            d = self.inst.desc()
+            sc = L.CpSchedules(b - a, self.stride, self.words, 0, None, self.ops_d[a].data_ptr(),
+                               self.len_d[a].data_ptr())
+            cres = L.CpResults(r["makespan"][a:].data_ptr(), r["peak_mem"][a:].data_ptr(), r["status"][a:].data_ptr(),
+                               None, None, 0, int(a), r["best_key"].data_ptr())
+            rc = L.load().cp_simulate(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(self.ws.data_ptr()),
+                                      self.ws.numel(), C.c_void_p(self.comp.cuda_stream))
+            L.check(rc, "cp_simulate")
+            e = torch.cuda.Event(); e.record(self.comp); done_out.append(e)
+            self.d2h.wait_event(e)
+            with torch.cuda.stream(self.d2h):
+                makespan_h[a:b].copy_(r["makespan"][a:b], non_blocking=True)
+                peak_h[a:b].copy_(r["peak_mem"][a:b], non_blocking=True)
+                status_h[a:b].copy_(r["status"][a:b], non_blocking=True)
+        cur.wait_stream(self.comp)
+        cur.wait_stream(self.d2h)
+        return r["best_key"]
+
+
 def greedy(inst: Instances, *, stats=False, timeline=False, stage_stride=None, words=None, ring=None,
            stream=None, ws=None, out=None):
     """cp_greedy: one Alg.-1 schedule per instance -> dict(ops, len, makespan, peak_mem, status, ...)."""

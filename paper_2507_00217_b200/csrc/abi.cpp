@@ -106,6 +106,7 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
   a.t_start = res->t_start;
   a.len_stride = res->len_stride;
   a.best_key = reinterpret_cast<unsigned long long*>(res->best_key);
+  a.index_base = res->index_base;
   char* base = static_cast<char*>(ws);
   a.ovf_count = reinterpret_cast<int32_t*>(base);
   a.ovf_list = reinterpret_cast<int32_t*>(base + kCtrlBytes);

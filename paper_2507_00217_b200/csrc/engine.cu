@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
             if (A.peak_mem) A.peak_mem[item] = completed ? pk : -1;
             A.status[item] = st;
             if (A.best_key && st == 0)
-              atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
+              atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)(item + A.index_base));
           }
           if (A.stage_stats && s < A.stage_stride) {
             const int4 v = (completed && s < c.p) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);

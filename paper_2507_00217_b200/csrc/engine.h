@@ -38,6 +38,7 @@ struct Args {
   int32_t* t_start;
   int32_t len_stride;
   int32_t from_list;       // items come from the overflow list (fix-up pass)
+  int32_t index_base;      // added to item ids in best_key
   unsigned long long* best_key;
   // overflow list (items whose lead exceeded R in the fast pass)
   int32_t* ovf_count;

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
           if (A.peak_mem) A.peak_mem[item] = done ? pk : -1;
           A.status[item] = st;
           if (A.best_key && st == 0)
-            atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)item);
+            atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)(item + A.index_base));
         }
         if (A.stage_stats) {
           // a completed valid row executed every block exactly once: busy = m (t_f + t_d + t_w);

@@ -367,3 +367,23 @@ def test_simulate_fast_path_invalid_and_overflow(O):
         w = compare_sim(O, cut.item(i), codes[j], lens[j], r, j, codes.shape[2], timeline=False)
         seen.add(w["status"])
     assert {0, 1, 2, 4} <= seen, seen
+
+
+def test_host_pipeline_matches_device_call():
+    """cp.HostPipeline (chunked H2D / kernel / D2H overlap over pinned host buffers) returns the
+    same per-schedule results and the same global best key as one device-resident cp_simulate."""
+    b = K.perturbed_instance()
+    n = 20_000
+    ops, ln = PL.plans_device(b, n, seed=K.PERTURB_SEED)
+    inst = cp.Instances(b)
+    ref = cp.simulate(inst, ops, ln, best=True)
+    ops_h = ops.cpu().pin_memory(); ln_h = ln.cpu().pin_memory()
+    ms_h = torch.empty(n, dtype=torch.int64).pin_memory()
+    pk_h = torch.empty(n, dtype=torch.int32).pin_memory()
+    st_h = torch.empty(n, dtype=torch.int32).pin_memory()
+    pipe = cp.HostPipeline(inst, n, ops.shape[1], ops.shape[2], chunks=7)
+    bk = pipe.run(ops_h, ln_h, ms_h, pk_h, st_h)
+    torch.cuda.synchronize()
+    assert torch.equal(ms_h, ref["makespan"].cpu()) and torch.equal(st_h, ref["status"].cpu())
+    assert torch.equal(pk_h, ref["peak_mem"].cpu())
+    assert int(bk[0]) == int(ref["best_key"][0])
