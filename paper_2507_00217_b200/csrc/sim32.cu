@@ -3,7 +3,7 @@
 // copies, arrival rings in shared memory, no per-entry timeline.
 //
 // Same semantics as k_engine<MODE_SIM> (engine.cu), which remains the reference GPU path for
-// every other shape and for the fix-up pass; tests compare both against the CPU oracle.
+// every other shape and for the fix-up pass; both are parity-tested.
 // What makes this kernel fast is what it leaves out: the warp is one segment, so the "no block
 // executed this round" test is a single ballot with a warp-uniform branch; the state is the
 // minimum the §3.5 recurrence needs; the plan buffers carry one spare row so finished lanes
