@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -15,6 +16,9 @@
 
 
 namespace {
+
+// experiments only: CP_NO_FAST=1 routes everything through the generic engine
+bool getenv_nofast() { const char* v = std::getenv("CP_NO_FAST"); return v && v[0] == '1'; }
 
 constexpr size_t kCtrlBytes = 256;
 constexpr size_t kMaxSmemPerBlock = 227 * 1024;
@@ -117,7 +121,8 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
   const int nseg = 32 >> a.seg_lg;
   a.plan_words = sc->words <= kPlanCapWords ? sc->words : 0;
 #ifndef CP_DEBUG
-  if (mode == cpk::MODE_SIM && nseg == 1 && sc->stage_stride == 32 && a.plan_words > 0 && !res->t_start) {
+  if (mode == cpk::MODE_SIM && nseg == 1 && sc->stage_stride == 32 && a.plan_words > 0 && !res->t_start &&
+      !getenv_nofast()) {
     // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row
     a.ring_slots = ring_slots_for(in);
     a.smem_words_per_warp = (2 * a.ring_slots * 32 + 2 * (a.plan_words + 1) * 32 + 32 + 4 + 3) & ~3;
@@ -131,6 +136,30 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
       if (cpk::launch_sim32(a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
       a.from_list = 1;
       a.tma = 0;
+      a.ring_slots = big_ring_slots(in);
+      a.ring_g = rings;
+      const int rc = launch_pass(mode, true, a, n, nseg, stream);
+      if (rc) return rc;
+      return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
+    }
+  }
+  if (mode == cpk::MODE_GREEDY && !res->t_start && !getenv_nofast()) {
+    // fast path (greedy_fast.cu): compile-time segment width, rings only in shared memory
+    const int Wd = in->max_pp <= 8 ? 8 : (in->max_pp <= 16 ? 16 : 32);
+    a.ring_slots = ring_slots_for(in);
+    a.smem_words_per_warp = (2 * a.ring_slots * 32 + 32 + 3) & ~3;
+    const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
+    if (per_warp * 2 <= kMaxSmemPerBlock) {
+      const int wpb = 2, threads = 64;
+      const size_t smem = per_warp * wpb;
+      const int bps = cpk::greedy_fast_blocks_per_sm(Wd, threads, smem);
+      const long long segs = (long long)(32 / Wd) * wpb;
+      const long long need = (n + segs - 1) / segs;
+      const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
+      if (cpk::launch_greedy_fast(Wd, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      a.from_list = 1;
+      a.tma = 0;
+      a.plan_words = sc->words <= kPlanCapWords ? sc->words : 0;
       a.ring_slots = big_ring_slots(in);
       a.ring_g = rings;
       const int rc = launch_pass(mode, true, a, n, nseg, stream);

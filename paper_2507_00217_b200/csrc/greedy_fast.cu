@@ -1,0 +1,286 @@
+// greedy_fast.cu -- fast path of cp_greedy (Alg. 1 + §4.2.2, round-parallel) for
+// batches without a per-entry timeline.  The segment width W (8, 16 or 32 lanes = stages) is a
+// compile-time constant, so the two causal-horizon scans unroll to log2(W) shuffle steps, and
+// 32/W instances share a warp.  Same semantics as k_engine<MODE_GREEDY> (engine.cu), which
+// remains the GPU path for timelines and for the global-ring fix-up pass.
+//
+// Per round, every lane (stage) forms its eligible set from register state and the two heads
+// of its shared-memory arrival rings, computes its schedulable time t*_s, and decides iff
+// t*_s < min(L_s, R_s) (two min-plus warp scans).  Execution is branch-free; the emitted 2-bit
+// plan word is stored straight to global memory (predicated) whenever it fills.  Loading a new
+// instance and classifying a finished one happen on a rare, warp-uniform path.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "engine.h"
+
+namespace cpk {
+
+namespace {
+constexpr int32_t GINF = 1 << 30;
+constexpr unsigned GFULL = 0xffffffffu;
+__device__ __forceinline__ int gmin(int a, int b) { return a < b ? a : b; }
+__device__ __forceinline__ int gmax(int a, int b) { return a > b ? a : b; }
+}  // namespace
+
+template <int W>
+__global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant__ Args A) {
+  extern __shared__ __align__(128) int32_t smem[];
+  constexpr int NSEG = 32 / W;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int s = lane & (W - 1);
+  const int seg = lane / W;
+  const unsigned segmask = (W == 32) ? GFULL : (((1u << W) - 1u) << (seg * W));
+  const int R = A.ring_slots;
+  const int RW = R * 32;
+  const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  const int wbase = wib * A.smem_words_per_warp;     // [ringF R*32][ringD R*32][sink 32]
+  const int iF = wbase + lane, iD = wbase + RW + lane, iDum = wbase + 2 * RW + lane;
+  const int iFend = iF + RW, iDend = iD + RW;
+
+  long long task = gwarp * NSEG + seg;
+  const long long tstride = nwarps * NSEG;
+
+  // per-lane instance constants
+  int p = 0, m = 0, nsub = 1, tf = 0, td = 0, tw = 0, wq = 0, wr = 0, mf = 0, md = 0, mw = 0, mlim = 0;
+  int tdp = 0, tag = 0, latF = 0, bwF = 0, latB = 0, bwB = 0, fmask = 0, dmask = 0, P = 0, Q = 0;
+  bool sendF = false, sendD = false;
+  // per-lane state
+  int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0, hF = iF, hD = iD;
+  int linkF = 0, linkB = 0, pos = 0, last_fd = 0;
+  uint32_t emitw = 0;
+  long long item = -1;
+  bool need = true;
+
+  for (;;) {
+    // ------------------------------------------------------------------ rare: (re)load instances
+    if (__any_sync(GFULL, need)) {
+      bool fresh = false;
+      int lat_b_s = 0, bw_b_s = 0, st0 = 0;
+      if (need) {
+        item = task < A.n_items ? task : -1;
+        task += tstride;
+        need = false;
+        fresh = item >= 0;
+        p = m = 0;
+        if (fresh) {
+          const cp_inst_v1* I = A.inst + (A.n_inst == 1 ? 0 : item);
+          p = I->n_pp; m = I->n_mb; nsub = I->n_sub;
+          const bool zero1 = I->flags & 1;
+          tf = td = tw = mf = md = mw = mlim = tdp = tag = latF = bwF = latB = bwB = 0;
+          if (s < p) {
+            tf = I->t_f[s]; td = I->t_d[s]; tw = I->t_w[s];
+            mf = I->m_f[s]; md = I->m_d[s]; mw = I->m_w[s]; mlim = I->m_lim[s];
+            tdp = I->t_dp[s]; tag = I->t_ag[s];
+            if (s < p - 1) { latF = I->lat_f[s]; bwF = I->bw_f[s]; lat_b_s = I->lat_b[s]; bw_b_s = I->bw_b[s]; }
+            if (s > 0) { latB = I->lat_b[s - 1]; bwB = I->bw_b[s - 1]; }
+          }
+          bool bad = p < 1 || p > CP_MAX_STAGES || m < 1 || nsub < 1;
+          if (!bad && s < p)
+            bad = !(tf > 0 && td > 0 && tw > 0 && tw >= nsub && mf > 0 && md <= 0 && mw <= 0 &&
+                    (long long)mf + md + mw == 0 && mlim >= mf && tdp >= 0 && tag >= 0 && latF >= 0 &&
+                    bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
+          if (!zero1) tag = 0;
+          st0 = bad ? CPI_BAD_INSTANCE : 0;
+          if (!st0 && (long long)(2 + nsub) * m > 16LL * A.words) st0 = CPI_BAD_PLAN;
+          if (!st0 && (p > W || m > CP_MAX_MB || nsub > CP_MAX_SUB)) st0 = CPI_OVERFLOW;
+          wq = tw / (nsub > 0 ? nsub : 1);
+          wr = tw % (nsub > 0 ? nsub : 1);
+          fmask = s > 0 ? -1 : 0;
+          dmask = s < p - 1 ? -1 : 0;
+          sendF = s < p - 1;
+          sendD = s > 0 && s < p;
+          clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = pos = last_fd = 0;
+          hF = iF; hD = iD;
+          emitw = 0;
+        }
+      }
+      // warp-wide: lookahead prefix sums (segment scans), horizon bound, status ballots
+      const bool act = fresh && s < p && st0 == 0;
+      const int cf = act ? tf + bwF + latF : 0;       // hop s -> s+1 (F)
+      const int cd = act ? td + bwB + latB : 0;       // hop s -> s-1 (D)
+      long long u = act ? (long long)m * ((long long)tf + td + tw) + tag + tdp +
+                              (long long)m * ((long long)latF + bwF + latB + bwB) : 0;
+      int pf = cf, qd = cd;
+#pragma unroll
+      for (int d = 1; d < W; d <<= 1) {
+        const int a = __shfl_up_sync(GFULL, pf, d, W);
+        const int b = __shfl_up_sync(GFULL, qd, d, W);
+        if (s >= d) { pf += a; qd += b; }
+      }
+#pragma unroll
+      for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(GFULL, u, d, W);
+      const unsigned b_inst = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_INSTANCE);
+      const unsigned b_plan = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_PLAN);
+      const unsigned b_over = __ballot_sync(GFULL, fresh && st0 == CPI_OVERFLOW);
+      if (fresh) {
+        P = pf - cf;
+        Q = qd;
+        int st = (b_inst & segmask) ? CPI_BAD_INSTANCE
+                 : (b_plan & segmask) ? CPI_BAD_PLAN
+                 : (b_over & segmask) ? CPI_OVERFLOW : 0;
+        if (!st && u >= (long long)GINF) st = CPI_OVERFLOW;      // int32 horizon guard (Q21)
+        if (st) {
+          if (s == 0) {
+            A.makespan[item] = -1;
+            if (A.peak_mem) A.peak_mem[item] = -1;
+            A.status[item] = st;
+          }
+          if (A.stage_stats && s < A.stage_stride)
+            *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = make_int4(0, 0, 0, 0);
+          if (s < A.stage_stride) A.len[item * A.stage_stride + s] = 0;
+          need = true;
+        }
+      }
+      if (__all_sync(GFULL, item < 0)) break;
+      continue;                                          // re-check: failed items load again
+    }
+
+    // ------------------------------------------------------------------ one round
+    const bool live = item >= 0 && s < p && nW < m;
+    const int leftF = __shfl_up_sync(GFULL, nF, 1, W);
+    const int rightD = __shfl_down_sync(GFULL, nD, 1, W);
+    const int aF = smem[hF];
+    const int aD = smem[hD];
+    const int availF = gmax(aF & fmask, tag);
+    const int availD = aD & dmask;
+    const bool knowF = nF < m && (fmask == 0 || leftF > nF) && nF - nD < R;
+    const bool knowD = nD < m && (dmask == 0 ? nF > nD : rightD > nD);
+    const bool hasF = live && knowF && mem + mf <= mlim;       // Q15
+    const bool hasD = live && knowD;
+    const bool hasW = live && nW < nD;
+    int mnv = hasF ? availF : GINF;
+    mnv = gmin(mnv, hasD ? availD : GINF);
+    mnv = gmin(mnv, hasW ? clk : GINF);
+    const int tstar = (hasF || hasD || hasW) ? gmax(clk, mnv) : GINF;   // §4.2.2 :419
+    // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s
+    int x = tstar - P, y = tstar + Q;
+#pragma unroll
+    for (int d = 1; d < W; d <<= 1) {
+      const int xu = __shfl_up_sync(GFULL, x, d, W);
+      const int yd = __shfl_down_sync(GFULL, y, d, W);
+      x = (s >= d) ? gmin(x, xu) : x;
+      y = (s + d < W) ? gmin(y, yd) : y;
+    }
+    const int xe = __shfl_up_sync(GFULL, x, 1, W);
+    const int ye = __shfl_down_sync(GFULL, y, 1, W);
+    const int Lh = (s == 0) ? GINF : P + xe;
+    const int Rh = (s == W - 1) ? GINF : ye - Q;
+    const bool go = tstar < GINF && tstar < gmin(Lh, Rh);
+    // operation selection (Q13): opposite of the last full F/D block, then the other, then W
+    const bool cF = hasF && availF <= tstar, cD = hasD && availD <= tstar;
+    const bool pD = (last_fd == 1) ? cD : (cD && !cF);
+    const bool pF = !pD && cF;
+    const bool pW = !pD && !pF;
+    const bool wfin = pW && (wsub + 1 == nsub);
+    const int dur = pF ? tf : (pD ? td : wq + (wsub < wr ? 1 : 0));
+    const int dm = pF ? mf : (pD ? md : (wfin ? mw : 0));
+    const int end = tstar + dur;
+    const int nl = gmax(end, pF ? linkF : linkB) + (pF ? bwF : bwB);   // FIFO link clock (App. X1)
+    const bool send = go && (pF ? sendF : (pD && sendD));
+    smem[send ? (pF ? hF + 1 : hD - 1) : iDum] = nl + (pF ? latF : latB);
+    // emit the 2-bit entry; a full word goes straight to global memory
+    const uint32_t code = pF ? CP_OP_F : (pD ? CP_OP_D : CP_OP_W);
+    const uint32_t w1 = emitw | (code << ((pos & 15) << 1));
+    const bool flush = go && (pos & 15) == 15;
+    if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
+    emitw = go ? (flush ? 0u : w1) : emitw;
+    const bool gF = go && pF, gD = go && pD, gW = go && pW;
+    clk = go ? end : clk;
+    mem += go ? dm : 0;
+    peak = gmax(peak, mem);
+    linkF = gF ? nl : linkF;
+    linkB = gD ? nl : linkB;
+    const int h1 = (pF ? hF : hD) + 32;
+    hF = gF ? (h1 == iFend ? iF : h1) : hF;
+    hD = gD ? (h1 == iDend ? iD : h1) : hD;
+    nF += gF;
+    nD += gD;
+    wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
+    nW += gW && wfin;
+    last_fd = gF ? 1 : (gD ? 2 : last_fd);
+    pos += go;
+    __syncwarp();
+
+    // ------------------------------------------------------------------ rare: a segment went idle
+    const unsigned bgo = __ballot_sync(GFULL, go);
+    const bool idle = item >= 0 && !(bgo & segmask);
+    if (__any_sync(GFULL, idle)) {
+      const unsigned b_unfin = __ballot_sync(GFULL, live);
+      const unsigned b_ring = __ballot_sync(GFULL, item >= 0 && s < p && nF < m && nF - nD >= R);
+      const unsigned b_mem = __ballot_sync(GFULL, item >= 0 && s < p && peak > mlim);
+      const bool complete = idle && !(b_unfin & segmask);
+      const bool on = item >= 0 && s < p;
+      int ms = on ? gmax(clk + tdp, tag) : 0, pk = on ? peak : 0;
+#pragma unroll
+      for (int d = 1; d < W; d <<= 1) {
+        ms = gmax(ms, __shfl_xor_sync(GFULL, ms, d, W));
+        pk = gmax(pk, __shfl_xor_sync(GFULL, pk, d, W));
+      }
+      // first_start = max-plus prefix over F_0's path (every row starts with F_0)
+      const int cfw = on ? tf + bwF + latF : 0;
+      int Pf = cfw;
+#pragma unroll
+      for (int d = 1; d < W; d <<= 1) { const int t = __shfl_up_sync(GFULL, Pf, d, W); if (s >= d) Pf += t; }
+      Pf -= cfw;
+      int xf = (on ? tag : 0) - Pf;
+#pragma unroll
+      for (int d = 1; d < W; d <<= 1) { const int t = __shfl_up_sync(GFULL, xf, d, W); if (s >= d) xf = gmax(xf, t); }
+      if (idle) {
+        if (!complete && (b_ring & segmask)) {
+          // ring capacity reached (host under-sized R): re-run in the global-ring fix-up pass
+          if (s == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
+        } else {
+          const int st = !complete ? CPI_DEADLOCK : ((b_mem & segmask) ? CPI_MEM_EXCEEDED : 0);
+          if (s == 0) {
+            A.makespan[item] = complete ? (long long)ms : -1LL;
+            if (A.peak_mem) A.peak_mem[item] = complete ? pk : -1;
+            A.status[item] = st;
+          }
+          if (A.stage_stats && s < A.stage_stride) {
+            const int4 v = (complete && on) ? make_int4(Pf + xf, clk, m * (tf + td + tw), peak) : make_int4(0, 0, 0, 0);
+            *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = v;
+          }
+          if (s < A.stage_stride) {
+            if (on && (pos & 15)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
+            A.len[item * A.stage_stride + s] = (uint16_t)(on ? pos : 0);
+          }
+        }
+        need = true;
+      }
+    }
+  }
+}
+
+template <int W>
+static int launch_w(const Args& a, int blocks, int threads, size_t smem, void* stream) {
+  const void* fn = (const void*)k_greedy_fast<W>;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  void* params[] = {(void*)&a};
+  return (int)cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
+}
+
+template <int W>
+static int bps_w(int threads, size_t smem) {
+  const void* fn = (const void*)k_greedy_fast<W>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;
+  return n > 0 ? n : 1;
+}
+
+int launch_greedy_fast(int W, const Args& a, int blocks, int threads, size_t smem, void* stream) {
+  return W == 8 ? launch_w<8>(a, blocks, threads, smem, stream)
+                : (W == 16 ? launch_w<16>(a, blocks, threads, smem, stream) : launch_w<32>(a, blocks, threads, smem, stream));
+}
+
+int greedy_fast_blocks_per_sm(int W, int threads, size_t smem) {
+  return W == 8 ? bps_w<8>(threads, smem) : (W == 16 ? bps_w<16>(threads, smem) : bps_w<32>(threads, smem));
+}
+
+}  // namespace cpk
