@@ -296,6 +296,31 @@ def run_ours(args):
                   "workload": "config3: 1e5 instances/GPU, p=16, 2 DCs, m=32, n_sub 1/2/4, memory x DP x ZeRO-1 grid",
                   "ms_per_launch": gms / gsteps, "status_ok": bool((g["status"] == 0).all().item())}
 
+    # ---------------- secondary: sweeps (config 2 on one GPU's shard, config 5 sharded over all
+    # ranks with one all_reduce(MIN) of the packed keys inside the timed region)
+    sweeps = None
+    if not args.no_sweep:
+        sweeps = {}
+        for name, grid, ncand in (("config2", K.gpt16_grid(), 3), ("config5", K.full_sweep_grid(), 5)):
+            cg = cp.to_cp_grid(grid)
+            bounds = cp.sweep_partition(grid, ws, cgrid=cg)
+            for _ in range(2):
+                keys, _ = cpd.sweep(grid, bounds=bounds)
+            sw_steps = 3
+            barrier(ws)
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(stream)
+            for _ in range(sw_steps):
+                keys, _ = cpd.sweep(grid, bounds=bounds)
+            b1.record(stream)
+            torch.cuda.synchronize()
+            sms = max_over_ranks(b0.elapsed_time(b1) / sw_steps, ws)
+            feas = int((keys < cp.KEY_OVER).sum().item())
+            sweeps[name] = {"points": grid.n_points, "candidates_per_point": ncand, "ms_per_sweep": sms,
+                            "points_per_s": grid.n_points / (sms / 1e3),
+                            "candidate_evals_per_s": grid.n_points * ncand / (sms / 1e3),
+                            "feasible_points": feas, "workload": grid.name}
+
     if rank == 0:
         achieved = BYTES_PER_EVAL * n / (kern_ms / 1e3) / 1e9
         alu_peak = 148 * 4 * 16 * (sm_max * 1e6) / 1e12        # Tops/s, ALU pipe
@@ -321,6 +346,7 @@ def run_ours(args):
             "gpu_launches": 2 * args.steps,
             "clocks": clk,
             "greedy": greedy,
+            "sweep": sweeps,
             "best_schedule": {"makespan_ticks": best >> 32, "index": best & 0xFFFFFFFF, "all_status_ok": status_ok},
         }
         if ws == 1 and not args.no_cpu:
@@ -344,6 +370,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="schedules per GPU (default 1e6)")
     ap.add_argument("--n-greedy", type=int, default=0)
     ap.add_argument("--no-greedy", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--chunks", type=int, default=8, help="e2e host pipeline chunks")
     args = ap.parse_args()

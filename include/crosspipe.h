@@ -160,8 +160,11 @@ int32_t cp_simulate(const cp_instances* inst, const cp_schedules* sched, const c
 int32_t cp_greedy(const cp_instances* inst, const cp_schedules* out, const cp_results* res,
                   void* ws, size_t ws_bytes, void* stream);
 
-/* Evaluate grid points [point_lo, point_hi): writes keys[k] for k in range only (the caller
- * fills the rest with INT64_MAX; cp_sweep in python = fill + shard + all_reduce(MIN)).
+/* Evaluate grid points [point_lo, point_hi): initializes and writes keys[k] for k in range only
+ * (the caller fills the rest with INT64_MAX; cp_sweep in python = fill + shard + all_reduce(MIN)).
+ * Work is (point, candidate) tasks taken from a device counter (most expensive first) and combined
+ * with a 64-bit atomicMin per point; p-classes run concurrently on streams forked from `stream`
+ * and joined back to it.  ws: cp_workspace_bytes(2, grid, 0) bytes.
  * cand_makespan (nullable) [n_points][5] int32: makespan of each candidate, -1 if not run
  * or memory-infeasible.  grid is a HOST pointer, passed to the kernel by value. */
 int32_t cp_sweep_shard(const cp_grid* grid, int64_t point_lo, int64_t point_hi,

@@ -245,8 +245,9 @@ def sweep_shard(grid, lo=0, hi=None, *, keys=None, cand=False, stream=None, devi
     if keys is None:
         keys = torch.full((npts,), KEY_NONE, dtype=torch.int64, device=device)
     cm = torch.full((npts, 5), -1, dtype=torch.int32, device=device) if cand is True else (cand if cand is not False and cand is not None else None)
+    ws = torch.empty(int(L.load().cp_workspace_bytes(2, C.byref(g), 0)), dtype=torch.uint8, device=keys.device)
     rc = L.load().cp_sweep_shard(C.byref(g), int(lo), int(hi), C.c_void_p(keys.data_ptr()),
-                                 _ptr(cm), None, 0, _stream(stream))
+                                 _ptr(cm), C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
     L.check(rc, "cp_sweep_shard")
     return keys, cm
 

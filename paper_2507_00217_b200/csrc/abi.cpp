@@ -295,24 +295,62 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
   if (rc) return rc;
   const long long np = grid_points(g);
   if (!keys || lo < 0 || hi < lo || hi > np) return CP_EINVAL;
-  (void)ws; (void)ws_bytes;
+  if (!ws || ws_bytes < kCtrlBytes) return CP_EWORKSPACE;
   if (lo == hi) return CP_OK;
-  const long long per_pp = np / g->n_pp_n;        // p is the slowest axis: one contiguous block per p
-  for (int ip = 0; ip < g->n_pp_n; ++ip) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* ukeys = reinterpret_cast<unsigned long long*>(keys);
+  unsigned long long* counters = static_cast<unsigned long long*>(ws);   // one task counter per p-class
+  if (cpk::launch_sweep_init(ukeys, cand_ms, lo, hi, stream) != cudaSuccess) return CP_ECUDA;
+  if (cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 8, st) != cudaSuccess) return CP_ECUDA;
+  // p is the slowest axis: one contiguous block of points per p-class; each class gets its own
+  // segment width W and ring size, and the classes run concurrently on forked streams
+  const long long per_pp = np / g->n_pp_n;
+  int cls[8], ncls = 0;
+  for (int ip = 0; ip < g->n_pp_n; ++ip)
+    if (std::max<long long>(lo, ip * per_pp) < std::min<long long>(hi, (ip + 1) * per_pp)) cls[ncls++] = ip;
+  cudaEvent_t fork = nullptr;
+  cudaStream_t sub[8] = {};
+  cudaEvent_t join[8] = {};
+  const bool forked = ncls > 1;
+  if (forked) {
+    if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return CP_ECUDA;
+    cudaEventRecord(fork, st);
+  }
+  for (int c = 0; c < ncls; ++c) {
+    const int ip = cls[c];
     const long long a0 = std::max<long long>(lo, ip * per_pp), a1 = std::min<long long>(hi, (ip + 1) * per_pp);
-    if (a0 >= a1) continue;
+    cudaStream_t cs = st;
+    if (forked) {
+      cudaStreamCreateWithFlags(&sub[c], cudaStreamNonBlocking);
+      cudaStreamWaitEvent(sub[c], fork, 0);
+      cs = sub[c];
+    }
     cpk::Args a;
     std::memset(&a, 0, sizeof(a));
     a.grid = *g;
     a.pt_lo = a0;
     a.pt_hi = a1;
-    a.keys = reinterpret_cast<unsigned long long*>(keys);
+    a.keys = ukeys;
     a.cand_ms = cand_ms;
+    a.sweep_counter = counters + c;
     a.seg_lg = lg2_ceil(g->n_pp_vals[ip]);
     a.ring_slots = sweep_ring_slots(g, g->n_pp_vals[ip]);
-    const int rc = launch_pass(cpk::MODE_SWEEP, false, a, a1 - a0, 32 >> a.seg_lg, stream);
-    if (rc) return rc;
+    rc = launch_pass(cpk::MODE_SWEEP, false, a, (a1 - a0) * __builtin_popcount(g->cand_mask & 31u), 32 >> a.seg_lg, cs);
+    if (forked) {
+      cudaEventCreateWithFlags(&join[c], cudaEventDisableTiming);
+      cudaEventRecord(join[c], cs);
+      cudaStreamWaitEvent(st, join[c], 0);
+    }
+    if (rc) break;
   }
+  if (forked) {
+    cudaEventDestroy(fork);
+    for (int c = 0; c < ncls; ++c) {
+      if (join[c]) cudaEventDestroy(join[c]);
+      if (sub[c]) cudaStreamDestroy(sub[c]);     // released once its queued work completes
+    }
+  }
+  if (rc) return rc;
   return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
 }
 

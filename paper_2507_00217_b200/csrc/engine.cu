@@ -31,6 +31,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "engine.h"
 #include "ptx.cuh"
 
@@ -125,7 +127,6 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
 #endif
 
   auto item_of = [&](long long t) -> long long {
-    if (kMode == MODE_SWEEP) return (A.pt_lo + t < A.pt_hi) ? A.pt_lo + t : -1;
     if (A.from_list) return (t < *(volatile int32_t*)A.ovf_count) ? (long long)A.ovf_list[t] : -1;
     return t < A.n_items ? t : -1;
   };
@@ -151,10 +152,9 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   uint32_t emitw = 0;
   int fmask = 0, dmask = 0;               // -1 where the lane consumes F (s > 0) / D (s < p-1) arrivals
   bool fmask_next = false;                // the lane sends F blocks (s < p-1)
-  // sweep: current candidate (>= 0), or -(c+1) = "advance to the first candidate >= c"
+  // sweep: candidate of the current (point, candidate) task
   int cand = 0;
   bool cand_greedy = (kMode == MODE_GREEDY);
-  unsigned long long best = KEY_NONE;
 
   for (;;) {
     // ------------------------------------------------------------------ fetch + load (per segment)
@@ -162,8 +162,30 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       bool just_loaded = false;
       if (need_load) {
         need_load = false;
-        item = item_of(task);
-        task += task_stride;
+        if (kMode == MODE_SWEEP) {
+          // dynamic (point, candidate) tasks, most expensive first (largest m / n_sub at the end)
+          long long t = 0;
+          if (s == 0) t = atomicAdd(A.sweep_counter, 1ull);
+          t = __shfl_sync(segmask, t, seg * W);
+          // task space: active candidates (slowest axis) x points; reversed so the most expensive
+          // tasks (greedy n_sub = 4, largest m) start first, and neighbouring segments of a warp
+          // get the same candidate type (same round code path)
+          const unsigned msk = A.grid.cand_mask & 31u;
+          const long long npts = A.pt_hi - A.pt_lo;
+          const long long ntask = npts * __popc(msk);
+          item = -1;
+          if (t < ntask) {
+            const long long tid = ntask - 1 - t;
+            int ci = (int)(tid / npts);
+            unsigned mm = msk;
+            while (ci-- > 0) mm &= mm - 1;       // ci-th set bit of the mask
+            cand = __ffs(mm) - 1;
+            item = A.pt_lo + tid % npts;
+          }
+        } else {
+          item = item_of(task);
+          task += task_stride;
+        }
         has_item = item >= 0;
         if (item >= 0) {
           just_loaded = true;
@@ -180,7 +202,8 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
             const int i_pp = (int)k;
             c.p = G.n_pp_vals[i_pp];
             c.m = G.n_mb_vals[i_mb];
-            c.nsub = 1;
+            cand_greedy = cand >= 2;
+            c.nsub = cand_greedy ? (1 << (cand - 2)) : 1;
             zero1 = G.base.flags & 1;
             const int ndc = imin(G.n_dc, c.p);
             if (s < c.p) {
@@ -227,7 +250,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           fmask = (s > 0) ? -1 : 0;
           dmask = (s < c.p - 1) ? -1 : 0;
           fmask_next = s < c.p - 1;
-          plen = 0;
+          plen = (kMode == MODE_SWEEP && s < c.p && !cand_greedy) ? 2 * c.m : 0;
           if (kMode == MODE_SIM && s < c.p && s < A.stage_stride) {
             plen = A.len[item * A.stage_stride + s];
             if (plen > 16 * A.words && !bad) load_status = CPI_BAD_PLAN;     // row longer than its capacity
@@ -238,10 +261,6 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = slF = slD = 0;
           first = busy = pos = comb = last_fd = 0;
           emitw = 0;
-          best = KEY_NONE;
-          cand = -1;
-          if (kMode == MODE_SWEEP && A.cand_ms && s == 0)
-            for (int cc = 0; cc < 5; ++cc) A.cand_ms[item * 5 + cc] = -1;
         }
       }
       if (__all_sync(FULL, item < 0)) break;
@@ -262,6 +281,14 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           if (s >= d) { pf += a; qd += b; }
         }
         for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(FULL, u, d, W);
+        // sweep: candidate statically infeasible (GPipe peak m*m_f, 1F1B peak min(p-s,m)*m_f (Z5),
+        // greedy t_w < n_sub (Q12)) or masked out -> skipped (its cand_ms stays -1, no key)
+        bool skip_lane = false;
+        if (kMode == MODE_SWEEP && just_loaded && s < c.p)
+          skip_lane = cand == 0 ? (long long)c.m * c.mf > c.mlim
+                                : (cand == 1 ? (long long)imin(c.p - s, c.m) * c.mf > c.mlim : c.tw < c.nsub);
+        const unsigned b_skip = __ballot_sync(FULL, skip_lane || (kMode == MODE_SWEEP && just_loaded &&
+                                                                 !((A.grid.cand_mask >> cand) & 1u)));
         const unsigned b_inst = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_INSTANCE);
         const unsigned b_plan = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_PLAN);
         const unsigned b_over = __ballot_sync(FULL, just_loaded && load_status == CPI_OVERFLOW);
@@ -273,6 +300,10 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
                    : (b_over & segmask) ? CPI_OVERFLOW : 0;
           if (!st && u >= (long long)INF) st = CPI_OVERFLOW;     // int32 horizon guard
           load_status = st;
+          if (kMode == MODE_SWEEP) {
+            if (st == CPI_OVERFLOW && s == 0) atomicMin(A.keys + item, KEY_OVER);
+            if (st != 0 || (b_skip & segmask)) need_load = true;
+          }
           if (kMode != MODE_SWEEP && st != 0) {
             // per-item failure: report now, no evaluation
             if (s == 0) {
@@ -308,42 +339,6 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         }
       }
 
-      // ---------------------------------------------------------------- sweep: next candidate
-      if (kMode == MODE_SWEEP) {
-        const bool want = item >= 0 && cand < 0 && !need_load;
-        if (__any_sync(FULL, want)) {
-          const int from = -cand - 1;
-          int next = -1;
-          for (int cc = 0; cc < 5; ++cc) {
-            bool ok = true;       // statically memory-feasible / valid candidate on this stage
-            if (s < c.p) {
-              if (cc == 0) ok = (long long)c.m * c.mf <= c.mlim;                          // GPipe peak m*m_f
-              else if (cc == 1) ok = (long long)imin(c.p - s, c.m) * c.mf <= c.mlim;     // 1F1B peak (Z5)
-              else ok = c.tw >= (1 << (cc - 2));                                           // Q12 t_w >= n_sub
-            }
-            const unsigned nb = __ballot_sync(FULL, !ok);
-            if (want && next < 0 && cc >= from && ((A.grid.cand_mask >> cc) & 1u) && !(nb & segmask)) next = cc;
-          }
-          if (want) {
-            if (load_status != 0) {
-              if (s == 0) A.keys[item] = (load_status == CPI_OVERFLOW) ? KEY_OVER : KEY_NONE;
-              need_load = true;
-            } else if (next < 0) {
-              if (s == 0) A.keys[item] = best;
-              need_load = true;
-            } else {
-              cand = next;
-              cand_greedy = next >= 2;
-              c.nsub = cand_greedy ? (1 << (next - 2)) : 1;
-              c.wq = c.tw / c.nsub;
-              c.wr = c.tw % c.nsub;
-              clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = slF = slD = 0;
-              first = busy = pos = comb = last_fd = 0;
-              plen = (s < c.p && !cand_greedy) ? 2 * c.m : 0;
-            }
-          }
-        }
-      }
       any_load = __any_sync(FULL, need_load);
       if (any_load) continue;     // warp-uniform: (re)load before running rounds
     }
@@ -519,20 +514,19 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         if (st == -1) {
           // a stage's F lead reached the ring capacity: re-run the item in the global-ring pass
           if (kMode == MODE_SWEEP) {
-            if (s == 0) A.keys[item] = KEY_OVER;                       // host sizes R so this never happens
+            if (s == 0) atomicMin(A.keys + item, KEY_OVER);            // host sizes R so this never happens
           } else if (s == 0) {
             const int slot = atomicAdd(A.ovf_count, 1);
             A.ovf_list[slot] = (int32_t)item;
           }
           need_load = true;
-          cand = 0;
         } else if (kMode == MODE_SWEEP) {
-          const bool feas = completed && st == 0;
-          if (A.cand_ms && s == 0) A.cand_ms[item * 5 + cand] = feas ? ms : -1;
-          const unsigned long long key = feas ? (((unsigned long long)ms << 8) | (unsigned)cand) : KEY_NONE;
-          best = key < best ? key : best;
-          cand = -(cand + 2);                  // advance to the first candidate > cand
-          cand_greedy = false;
+          // one (point, candidate) task: its makespan and the point's packed argmin key
+          if (completed && st == 0 && s == 0) {
+            if (A.cand_ms) A.cand_ms[item * 5 + cand] = ms;
+            atomicMin(A.keys + item, ((unsigned long long)ms << 8) | (unsigned)cand);
+          }
+          need_load = true;
         } else {
           if (s == 0 && CHK(item, n_it, 13)) {
             A.makespan[item] = completed ? (long long)ms : -1LL;
@@ -561,9 +555,25 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         }
         if (use_tma && need_load) { cur_buf ^= 1; plan_off = cur_buf * PW * 32 + lane; }
       }
-      any_load = __any_sync(FULL, need_load || (kMode == MODE_SWEEP && has_item && cand < 0));
+      any_load = __any_sync(FULL, need_load);
     }
   }
+}
+
+// sweep shard initialisation: keys of the range = INT64_MAX, candidate makespans = -1
+__global__ void k_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi) {
+  for (long long k = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; k < hi; k += (long long)gridDim.x * blockDim.x) {
+    keys[k] = KEY_NONE;
+    if (cand_ms)
+      for (int c = 0; c < 5; ++c) cand_ms[k * 5 + c] = -1;
+  }
+}
+
+int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, void* stream) {
+  const long long n = hi - lo;
+  const int blocks = (int)std::min<long long>(1024, (n + 255) / 256);
+  k_sweep_init<<<blocks > 0 ? blocks : 1, 256, 0, (cudaStream_t)stream>>>(keys, cand_ms, lo, hi);
+  return (int)cudaGetLastError();
 }
 
 template <int kMode, bool kRG, bool kTL>

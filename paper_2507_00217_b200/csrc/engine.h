@@ -46,6 +46,7 @@ struct Args {
   // sweep
   int64_t pt_lo, pt_hi;
   unsigned long long* keys;
+  unsigned long long* sweep_counter;   // dynamic task counter of a sweep launch (workspace)
   int32_t* cand_ms;
   cp_grid grid;
 };
@@ -60,6 +61,7 @@ int launch_greedy_fast(int W, const Args& a, int blocks, int threads, size_t sme
 int greedy_fast_blocks_per_sm(int W, int threads, size_t smem);
 int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem, bool timeline);
 int device_sm_count();
+int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, void* stream);
 
 constexpr int kThreads = 128;          // 4 warps per block
 constexpr int kFixWarps = 148 * 4;     // warps of a global-ring (fix-up) launch
