@@ -387,3 +387,13 @@ def test_host_pipeline_matches_device_call():
     assert torch.equal(ms_h, ref["makespan"].cpu()) and torch.equal(st_h, ref["status"].cpu())
     assert torch.equal(pk_h, ref["peak_mem"].cpu())
     assert int(bk[0]) == int(ref["best_key"][0])
+
+
+@pytest.mark.parametrize("max_p,seed", [(32, 21), (16, 22), (8, 23), (3, 24)])
+def test_greedy_fast_path_random_instances(O, max_p, seed):
+    """cp_greedy without a timeline runs k_greedy_fast<W> (W = 8 / 16 / 32): byte-equal schedules,
+    makespans, peaks and per-stage stats vs sequential Alg. 1 on random instances."""
+    batch = K.random_instances(300, seed=seed, max_p=max_p, max_m=20, intra_delay=True)
+    inst = cp.Instances(batch)
+    g = to_host(cp.greedy(inst, stats=True))
+    check_greedy(O, batch, g, range(len(batch)))
