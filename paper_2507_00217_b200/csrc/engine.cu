@@ -355,7 +355,8 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
     // room in the consumer's ring (lead <= R) -- a full ring stalls the lane and the
     // rare path hands the item to the global-ring fix-up pass
     const bool roomF = kRingGlobal || (nF - nD < R);
-    const bool knowF = nF < c.m && (fmask == 0 || leftF > nF) && roomF;
+    const bool knowFg = nF < c.m && (fmask == 0 || leftF > nF);      // greedy: capacity not part of the decision
+    const bool knowF = knowFg && roomF;
     const bool knowD = nD < c.m && (dmask == 0 ? nF > nD : rightD > nD);
 
     bool go = false, isF = false, isW = false, isB = false;
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       const int availF = imax(arrF & fmask, c.tagate);
       const int availD = arrD & dmask;
       const bool gl = live && is_greedy;
-      const bool hasF = gl && knowF && mem + c.mf <= c.mlim;      // Q15: memory-infeasible F is not eligible
+      const bool hasF = gl && knowFg && mem + c.mf <= c.mlim;     // Q15: memory-infeasible F is not eligible
       const bool hasD = gl && knowD;
       const bool hasW = gl && nW < nD;                             // W avail = its D end <= clk
       int mn = hasF ? availF : INF;
@@ -421,7 +422,9 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         const bool pickD = (last_fd == 1) ? cD : (cD && !cF);
         const bool pickF = !pickD && cF;
         if (is_greedy) {
-          go = g_go;
+          // an F whose consumer ring is full is not executed (lane stalls -> fix-up pass); the
+          // decision itself never depends on the ring capacity
+          go = g_go && !(pickF && !roomF);
           isF = pickF; isW = !pickF && !pickD; isB = false;
           start = tstar;
         }

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
     const int aD = smem[hD];
     const int availF = gmax(aF & fmask, tag);
     const int availD = aD & dmask;
-    const bool knowF = nF < m && (fmask == 0 || leftF > nF) && nF - nD < R;
+    const bool knowF = nF < m && (fmask == 0 || leftF > nF);
     const bool knowD = nD < m && (dmask == 0 ? nF > nD : rightD > nD);
     const bool hasF = live && knowF && mem + mf <= mlim;       // Q15
     const bool hasD = live && knowD;
@@ -168,11 +168,13 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
     const int ye = __shfl_down_sync(GFULL, y, 1, W);
     const int Lh = (s == 0) ? GINF : P + xe;
     const int Rh = (s == W - 1) ? GINF : ye - Q;
-    const bool go = tstar < GINF && tstar < gmin(Lh, Rh);
     // operation selection (Q13): opposite of the last full F/D block, then the other, then W
     const bool cF = hasF && availF <= tstar, cD = hasD && availD <= tstar;
     const bool pD = (last_fd == 1) ? cD : (cD && !cF);
     const bool pF = !pD && cF;
+    // an F whose consumer ring is full (lead would exceed R: undersized ring hint) is not executed:
+    // the lane stalls and the item is re-run by the global-ring fix-up pass (decisions unchanged)
+    const bool go = tstar < GINF && tstar < gmin(Lh, Rh) && !(pF && nF - nD >= R);
     const bool pW = !pD && !pF;
     const bool wfin = pW && (wsub + 1 == nsub);
     const int dur = pF ? tf : (pD ? td : wq + (wsub < wr ? 1 : 0));

@@ -397,3 +397,51 @@ def test_greedy_fast_path_random_instances(O, max_p, seed):
     inst = cp.Instances(batch)
     g = to_host(cp.greedy(inst, stats=True))
     check_greedy(O, batch, g, range(len(batch)))
+
+
+def test_fast_paths_ring_overflow_fixup(O):
+    """Undersized ring hints force every fast-path item (k_sim32 / k_greedy_fast) through the
+    stall -> overflow list -> global-ring fix-up pass; results must be unchanged."""
+    b = K.perturbed_instance()
+    ops, ln = PL.plans_device(b, 500, seed=K.PERTURB_SEED)
+    inst = cp.Instances(b)
+    ref = cp.simulate(inst, ops, ln, stats=True, best=True)
+    for ring in (1, 3, 16):
+        r = cp.simulate(inst, ops, ln, stats=True, best=True, ring=ring)
+        for k in ("makespan", "status", "peak_mem", "stage_stats", "best_key"):
+            assert torch.equal(r[k], ref[k]), (ring, k)
+    batch = K.random_instances(200, seed=25, max_p=16, max_m=16)
+    gi = cp.Instances(batch)
+    gref = cp.greedy(gi, stats=True)
+    for ring in (1, 2):
+        g = cp.greedy(gi, stats=True, ring=ring)
+        for k in ("makespan", "status", "peak_mem", "stage_stats", "ops", "len"):
+            assert torch.equal(g[k], gref[k]), (ring, k)
+    ms = ref["makespan"].cpu().numpy()
+    c, l_ = unpack_plans(ops[:20].cpu().numpy().view(np.uint32), ln[:20].cpu().numpy().view(np.uint16))
+    for i in range(20):
+        assert ms[i] == O.simulate(b.item(0), c[i], l_[i])["makespan"]
+
+
+def test_sweep_edge_grids(O):
+    """Sweep grids with more DCs than stages (p = 2, 3 with 4 DCs), a ZeRO-1 base with allgather
+    times, DP tails, and a candidate subset (1F1B + greedy n_sub = 2 only)."""
+    from workloads.core import Grid
+    base = K.uniform_instance(4, 8, 4, 30, 40, 20, zero1=1, t_ag=25)
+    base.t_ag[0, :] = 25
+    grid = Grid(base=base, n_dc=4, pp_vals=[2, 3, 4], mb_vals=[1, 5], lat=np.array([0, 45]), bw=np.array([0, 20, 70]),
+                mlim_x1000=np.array([1000, 1700]), tdp=np.array([0, 90]), cand_mask=0b01010)
+    keys, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
+
+
+def test_generic_greedy_ring_overflow_fixup():
+    """The generic engine's greedy (timeline requested) with an undersized ring must also hand
+    over to the fix-up pass without changing a single decision."""
+    batch = K.random_instances(150, seed=26, max_p=32, max_m=14)
+    gi = cp.Instances(batch)
+    ref = cp.greedy(gi, stats=True, timeline=True)
+    g = cp.greedy(gi, stats=True, timeline=True, ring=1)
+    for k in ("makespan", "status", "peak_mem", "stage_stats", "ops", "len", "t_start"):
+        assert torch.equal(g[k], ref[k]), k
