@@ -144,16 +144,19 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
     auto rounds = [&](auto n1) {
       constexpr bool kN1 = decltype(n1)::value;   // n_sub == 1: a W entry is a whole W block
       for (;;) {
-        const int leftF = __shfl_up_sync(FULLM, nF, 1);
-        const int rightD = __shfl_down_sync(FULLM, nD, 1);
+        // both neighbours' (nF, nD), 16 bits each, in one shuffle per direction
+        const int cu = __shfl_up_sync(FULLM, nF | (nD << 16), 1);
+        const int cd = __shfl_down_sync(FULLM, nF | (nD << 16), 1);
+        const int leftF = cu & 0xffff, leftD = cu >> 16, rightF = cd & 0xffff, rightD = cd >> 16;
         const int aF = smem[hF];                  // both ring heads, independent of the entry type
         const int aD = smem[hD];
         const unsigned code = (wv >> ((pos & 15) << 1)) & 3u;
         const bool isF = code == CP_OP_F, isW = code == CP_OP_W, isB = code == CP_OP_B;
         const bool isDB = !isF & !isW;
-        // readiness: input produced; ring room (lead <= R); W sub-blocks only after their D
-        const bool knowF = ((fmask == 0) | (leftF > nF)) & (nF - nD < R);
-        const bool knowD = (dmask == 0) ? (nF > nD) : (rightD > nD);
+        // readiness: input produced; room in the consumer's ring (occupancy < R: backpressure);
+        // W sub-blocks only after their D
+        const bool knowF = ((fmask == 0) | (leftF > nF)) & (!sendF | (nF - rightF < R));
+        const bool knowD = ((dmask == 0) ? (nF > nD) : (rightD > nD)) & (!sendD | (nD - leftD < R));
         const bool wok = kN1 ? (went < nD) : (went < wcap);
         const bool go = (pos < plen) & (isF ? knowF : (isW ? wok : knowD));
         const int avail = isF ? mx(aF & fmask, tag) : (isW ? 0 : (aD & dmask));
@@ -193,6 +196,11 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
 
     // ------------------------------------------------------------------ no progress: classify
     {
+      // a stall with a full consumer ring may be an artefact of the small ring (cyclic backpressure):
+      // such items are re-run exactly by the global-ring fix-up pass
+      const int cu = __shfl_up_sync(FULLM, nF | (nD << 16), 1);
+      const int cd = __shfl_down_sync(FULLM, nF | (nD << 16), 1);
+      const bool ring_full = (sendF && nF - (cd & 0xffff) >= R) || (sendD && nD - (cu >> 16) >= R);
       const bool unfin = pos < plen;
       const bool complete = !__any_sync(FULLM, unfin);
       bool badc = false;
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
       }
       int st;
       if (__any_sync(FULLM, badc)) st = CPI_BAD_PLAN;
-      else if (!complete && __any_sync(FULLM, s < p && nF < m && nF - nD >= R)) st = -1;
+      else if (!complete && __any_sync(FULLM, ring_full)) st = -1;
       else if (!complete) st = CPI_DEADLOCK;
       else st = __any_sync(FULLM, s < p && peak > mlim) ? CPI_MEM_EXCEEDED : 0;
       if (st == -1) {                            // ring capacity reached: hand to the fix-up pass
