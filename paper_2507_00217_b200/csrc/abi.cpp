@@ -46,7 +46,8 @@ int big_ring_slots(const cp_instances* in) { return std::max(1, std::min(in->max
 int fast_ring_slots(const cp_instances* in) {
   int cap = 16;
   if (const char* v = std::getenv("CP_RING_CAP")) cap = std::max(1, std::atoi(v));   // experiments
-  return std::min(ring_slots_for(in), cap);
+  // a power of two: the n_sub == 1 rounds address ring slots as count & (R - 1)
+  return 1 << lg2_ceil(std::min(ring_slots_for(in), cap));
 }
 
 constexpr int kPlanCapWords = 64;        // plans up to 1024 entries per stage row are staged in smem
@@ -133,7 +134,7 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
       !getenv_nofast()) {
     // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row
     a.ring_slots = fast_ring_slots(in);
-    a.smem_words_per_warp = (2 * a.ring_slots * 32 + 2 * (a.plan_words + 1) * 32 + 32 + 4 + 3) & ~3;
+    a.smem_words_per_warp = (cpk::kSim32TableWords + 2 * a.ring_slots * 32 + 2 * (a.plan_words + 1) * 32 + 64 + 4 + 3) & ~3;
     const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
     if (per_warp * 2 <= kMaxSmemPerBlock) {
       const int wpb = 2, threads = 64;

@@ -23,6 +23,13 @@ constexpr int32_t INF32 = 1 << 30;
 constexpr unsigned FULLM = 0xffffffffu;
 __device__ __forceinline__ int mn(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int mx(int a, int b) { return a > b ? a : b; }
+// x + g * d as an integer multiply-add: keeps conditional state updates on the FMA pipe
+// (the kernel is ALU-pipe bound; a SEL would land on the ALU pipe)
+__device__ __forceinline__ int madd(int g, int d, int x) {
+  int r;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(g), "r"(d), "r"(x));
+  return r;
+}
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args A) {
@@ -35,15 +42,24 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
   const int PWr = PW + 1;                         // one spare row per buffer
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  // per-warp smem (words): [ringF R*32][ringD R*32][plan 2*(PW+1)*32][dummy 32][2 mbarriers]
+  // per-warp smem (words): [paramA 4*32 int4][paramB 4*32 int4][ringF R*32][ringD R*32]
+  //                        [plan 2*(PW+1)*32][sink 32][zero 32][2 mbarriers]
   const int wbase = wib * A.smem_words_per_warp;
-  const int pbase0 = wbase + 2 * RW;
-  const int dum_row = 2 * RW + 2 * PWr * 32;      // relative to wbase
+  const int rbase = wbase + kSim32TableWords;
+  const int pbase0 = rbase + 2 * RW;
+  const int dum_row = kSim32TableWords + 2 * RW + 2 * PWr * 32;   // relative to wbase
+  const int zero_row = dum_row + 32;
   uint32_t* const plan = reinterpret_cast<uint32_t*>(smem + pbase0);
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + wbase + dum_row + 32);
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + wbase + zero_row + 32);
+  int4* const tabA = reinterpret_cast<int4*>(smem + wbase) + lane;          // [code][lane]
+  int4* const tabB = reinterpret_cast<int4*>(smem + wbase + 512) + lane;
   const uint32_t plan_bytes = (uint32_t)A.words * 32u * 4u;
 
   long long item = gwarp;
+  // the rings never written by a producer (stage 0's F ring) and the zero row read by W entries
+  // must hold 0: clear both ring blocks and the zero row once
+  for (int k = lane; k < 2 * RW; k += 32) smem[rbase + k] = 0;
+  smem[wbase + zero_row + lane] = 0;
   if (lane == 0) { mbar_init(&bars[0]); mbar_init(&bars[1]); }
   __syncwarp();
   if (lane == 0 && item < A.n_items) tma_load_1d(plan, A.ops + item * A.words * 32, plan_bytes, &bars[0]);
@@ -102,8 +118,8 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
     const int dmask = s < p - 1 ? -1 : 0;         // lane consumes D arrivals
     const bool sendF = s < p - 1, sendD = s > 0 && s < p;
     // integer smem indices (shared window addressing, no generic pointers in the loop)
-    const int iF = wbase + lane;                  // own F column
-    const int iD = wbase + RW + lane;             // own D column
+    const int iF = rbase + lane;                  // own F column
+    const int iD = rbase + RW + lane;             // own D column
     const int iDum = wbase + dum_row + lane;      // store sink for lanes that send nothing
     const int iP = pbase0 + (buf ^ 1) * PWr * 32 + lane;   // this item's plan column (buf already flipped)
 
@@ -169,30 +185,90 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
         const int nl = mx(end, isF ? linkF : linkB) + (isF ? bwF : bwB);   // FIFO link clock (App. X1)
         const bool send = go & (isF ? sendF : (isDB & sendD));
         smem[send ? (isF ? hF + 1 : hD - 1) : iDum] = nl + (isF ? latF : latB);
-        const bool gF = go & isF, gD = go & isDB;
-        clk = go ? end : clk;
-        mem += go ? dm : 0;
+        const int gi = go ? 1 : 0, gFi = (go & isF) ? 1 : 0, gDi = (go & isDB) ? 1 : 0;
+        clk = madd(gi, end - clk, clk);
+        mem = madd(gi, dm, mem);
         peak = mx(peak, mem);
-        linkF = gF ? nl : linkF;
-        linkB = gD ? nl : linkB;
+        linkF = madd(gFi, nl - linkF, linkF);
+        linkB = madd(gDi, nl - linkB, linkB);
         const int h1 = (isF ? hF : hD) + 32;
-        hF = gF ? (h1 == iFend ? iF : h1) : hF;
-        hD = gD ? (h1 == iDend ? iD : h1) : hD;
-        nF += gF;
-        nD += gD;
-        went += go & isW;
+        hF = madd(gFi, (h1 == iFend ? iF : h1) - hF, hF);
+        hD = madd(gDi, (h1 == iDend ? iD : h1) - hD, hD);
+        nF = madd(gFi, 1, nF);
+        nD = madd(gDi, 1, nD);
+        went = madd((go & isW) ? 1 : 0, 1, went);
+        const bool gF = go & isF, gD = go & isDB;
         if (!kN1) {
           wcap += gD ? nsub : 0;
           wsub = (go & isW) ? (wfin ? 0 : wsub + 1) : wsub;
         }
-        pos += go;
+        pos = madd(go ? 1 : 0, 1, pos);
         wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];   // next round's word (spare row covers pos == 16*PW)
         __syncwarp();
         if (__ballot_sync(FULLM, go) == 0u) break;      // warp-uniform: nothing executed -> classify
       }
     };
-    if (nsub == 1) rounds(std::true_type{});
-    else rounds(std::false_type{});
+    if (nsub == 1) {
+      // ---- n_sub == 1: table-driven rounds. The per-entry-type parameters come from one
+      // conflict-free 128-bit smem load per table instead of select chains; ring slots are
+      // addressed by the block counters (slot = count mod R, R a power of two), so there are no
+      // head registers; the ZeRO-1 gate max(arrival, t_ag) folds into the initial clock because
+      // F_0 is the first block every completing row executes.
+      const int Rm = R - 1;
+      const bool last = s == p - 1;
+      const int lmF = s == 0 ? 0xffff : 0;          // stage 0 has no F producer: always available
+      const int rmF = last ? 0xffff : 0;            // the last stage has no F consumer: always room
+      if (last && s < 31)                           // its D ring may hold a larger item's arrivals
+        for (int k = 0; k < R; ++k) smem[iD + (k << 5)] = 0;
+      {                                             // every lane: idle lanes get safe entries
+        tabA[0 * 32] = make_int4(tf, mf, bwF, latF);
+        tabA[1 * 32] = make_int4(tB, mB, bwB, latB);
+        tabA[2 * 32] = make_int4(td, md, bwB, latB);
+        tabA[3 * 32] = make_int4(tw, mw, 0, 0);
+        tabB[0 * 32] = make_int4(iF, Rm, sendF ? 1 : 0, 0);
+        tabB[1 * 32] = make_int4(iD, Rm, sendD ? -1 : 0, 0);
+        tabB[2 * 32] = make_int4(iD, Rm, sendD ? -1 : 0, 0);
+        tabB[3 * 32] = make_int4(wbase + zero_row + lane, 0, 0, 0);
+      }
+      __syncwarp();
+      clk = tag;
+      for (;;) {
+        const int me = madd(nD, 65536, nF);
+        const int cu = __shfl_up_sync(FULLM, me, 1);
+        const int cd = __shfl_down_sync(FULLM, me, 1);
+        const int leftF = (cu & 0xffff) | lmF;
+        const int leftD = cu >> 16;                 // stage 0 reads itself: nD - nD < R
+        const int rightF = (cd & 0xffff) | rmF;
+        const int rightD = last ? nF : (cd >> 16);  // the last stage's D follows its own F
+        const unsigned code = (wv >> ((pos & 15) << 1)) & 3u;
+        const int4 ta = tabA[code << 5];            // {duration, memory delta, link bw, latency}
+        const int4 tb = tabB[code << 5];            // {ring column, slot mask, send offset, -}
+        const bool isF = code == CP_OP_F, isW = code == CP_OP_W;
+        const bool rF = (leftF > nF) & (nF - rightF < R);
+        const bool rD = (rightD > nD) & (nD - leftD < R);
+        const bool go = (pos < plen) & (isF ? rF : (isW ? (went < nD) : rD));
+        const int raddr = tb.x + (((isF ? nF : nD) & tb.y) << 5);
+        const int start = mx(clk, smem[raddr]);
+        const int end = start + ta.x;
+        const int nl = mx(end, isF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
+        if (go && tb.z != 0) smem[raddr + tb.z] = nl + ta.w;
+        const int gi = go ? 1 : 0, gFi = (go & isF) ? 1 : 0, gWi = (go & isW) ? 1 : 0;
+        const int gDi = gi - gFi - gWi;
+        clk = madd(gi, end - clk, clk);
+        mem = madd(gi, ta.y, mem);
+        peak = mx(peak, mem);
+        pos = madd(gi, 1, pos);
+        linkF = madd(gFi, nl - linkF, linkF);
+        linkB = madd(gDi, nl - linkB, linkB);
+        nF = madd(gFi, 1, nF);
+        nD = madd(gDi, 1, nD);
+        went = madd(gWi, 1, went);
+        wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];
+        if (__ballot_sync(FULLM, go) == 0u) break;
+      }
+    } else {
+      rounds(std::false_type{});
+    }
 
     // ------------------------------------------------------------------ no progress: classify
     {
