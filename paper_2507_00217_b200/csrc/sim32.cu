@@ -216,8 +216,10 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
       // F_0 is the first block every completing row executes.
       const int Rm = R - 1;
       const bool last = s == p - 1;
-      const int lmF = s == 0 ? 0xffff : 0;          // stage 0 has no F producer: always available
-      const int rmF = last ? 0xffff : 0;            // the last stage has no F consumer: always room
+      int lmF = s == 0 ? 0xffff : 0;                // stage 0 has no F producer: always available
+      int rmF = last ? 0xffff : 0;                  // the last stage has no F consumer: always room
+      asm("mov.b32 %0, %0;" : "+r"(lmF));           // opaque: keeps (x & 0xffff) | m one LOP3
+      asm("mov.b32 %0, %0;" : "+r"(rmF));
       if (last && s < 31)                           // its D ring may hold a larger item's arrivals
         for (int k = 0; k < R; ++k) smem[iD + (k << 5)] = 0;
       {                                             // every lane: idle lanes get safe entries
@@ -246,7 +248,8 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
         const bool isF = code == CP_OP_F, isW = code == CP_OP_W;
         const bool rF = (leftF > nF) & (nF - rightF < R);
         const bool rD = (rightD > nD) & (nD - leftD < R);
-        const bool go = (pos < plen) & (isF ? rF : (isW ? (went < nD) : rD));
+        const bool isDB = !isF & !isW;
+        const bool go = (pos < plen) & ((isF & rF) | (isW & (went < nD)) | (isDB & rD));
         const int raddr = tb.x + (((isF ? nF : nD) & tb.y) << 5);
         const int start = mx(clk, smem[raddr]);
         const int end = start + ta.x;
@@ -264,7 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
         nD = madd(gDi, 1, nD);
         went = madd(gWi, 1, went);
         wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];
-        if (__ballot_sync(FULLM, go) == 0u) break;
+        if (!__any_sync(FULLM, go)) break;
       }
     } else {
       rounds(std::false_type{});
