@@ -267,6 +267,7 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
         nD = madd(gDi, 1, nD);
         went = madd(gWi, 1, went);
         wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];
+        __syncwarp();                               // ring stores visible to the neighbours' next reads
         if (!__any_sync(FULLM, go)) break;
       }
     } else {
