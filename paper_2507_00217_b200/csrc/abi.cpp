@@ -155,8 +155,9 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
   if (mode == cpk::MODE_GREEDY && !res->t_start && !getenv_nofast()) {
     // fast path (greedy_fast.cu): compile-time segment width, rings only in shared memory
     const int Wd = in->max_pp <= 8 ? 8 : (in->max_pp <= 16 ? 16 : 32);
-    a.ring_slots = ring_slots_for(in);          // lead bound (greedy gates on nF - nD, cheaper than occupancy)
-    a.smem_words_per_warp = (2 * a.ring_slots * 32 + 32 + 3) & ~3;
+    // lead bound (greedy gates on nF - nD, cheaper than occupancy); a power of two (count-addressed slots)
+    a.ring_slots = 1 << lg2_ceil(ring_slots_for(in));
+    a.smem_words_per_warp = (cpk::kGreedyTableWords + 2 * a.ring_slots * 32 + 3) & ~3;
     const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
     if (per_warp * 2 <= kMaxSmemPerBlock) {
       const int wpb = 2, threads = 64;

@@ -65,6 +65,7 @@ int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, 
 
 constexpr int kThreads = 128;          // 4 warps per block
 constexpr int kFixWarps = 148 * 4;     // warps of a global-ring (fix-up) launch
+constexpr int kGreedyTableWords = 768;   // k_greedy_fast per-warp parameter table: [6 entries][32 lanes] int4
 constexpr int kSim32TableWords = 1024;  // k_sim32 per-warp parameter tables: 2 x [4 codes][32 lanes] int4
 
 }  // namespace cpk

@@ -21,6 +21,13 @@ constexpr int32_t GINF = 1 << 30;
 constexpr unsigned GFULL = 0xffffffffu;
 __device__ __forceinline__ int gmin(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int gmax(int a, int b) { return a > b ? a : b; }
+// x + g * d as an integer multiply-add: conditional state updates issue on the FMA pipe (the
+// round is ALU-pipe bound; a SEL would land on the ALU pipe)
+__device__ __forceinline__ int gmadd(int g, int d, int x) {
+  int r;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(g), "r"(d), "r"(x));
+  return r;
+}
 }  // namespace
 
 template <int W>
@@ -36,19 +43,24 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
   const int RW = R * 32;
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  const int wbase = wib * A.smem_words_per_warp;     // [ringF R*32][ringD R*32][sink 32]
-  const int iF = wbase + lane, iD = wbase + RW + lane, iDum = wbase + 2 * RW + lane;
-  const int iFend = iF + RW, iDend = iD + RW;
+  const int Rm = R - 1;                              // R is a power of two: slot = count & Rm
+  // per-warp smem (words): [params 6*32 int4][ringF R*32][ringD R*32]
+  const int wbase = wib * A.smem_words_per_warp;
+  const int iF = wbase + kGreedyTableWords + lane, iD = iF + RW;
+  int4* const tab = reinterpret_cast<int4*>(smem + wbase) + lane;    // [entry][lane]
+  // stage 0's F ring is never written by a producer: it must read 0 (cleared once)
+  for (int k = lane; k < 2 * RW; k += 32) smem[wbase + kGreedyTableWords + k] = 0;
+  __syncwarp();
 
   long long task = gwarp * NSEG + seg;
   const long long tstride = nwarps * NSEG;
 
   // per-lane instance constants
   int p = 0, m = 0, nsub = 1, tf = 0, td = 0, tw = 0, wq = 0, wr = 0, mf = 0, md = 0, mw = 0, mlim = 0;
-  int tdp = 0, tag = 0, latF = 0, bwF = 0, latB = 0, bwB = 0, fmask = 0, dmask = 0, P = 0, Q = 0;
-  bool sendF = false, sendD = false;
+  int tdp = 0, tag = 0, latF = 0, bwF = 0, latB = 0, bwB = 0, P = 0, Q = 0, lmF = 0;
+  bool sendF = false, sendD = false, lastS = false;
   // per-lane state
-  int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0, hF = iF, hD = iD;
+  int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0;
   int linkF = 0, linkB = 0, pos = 0, last_fd = 0;
   uint32_t emitw = 0;
   long long item = -1;
@@ -88,13 +100,24 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
           if (!st0 && (p > W || m > CP_MAX_MB || nsub > CP_MAX_SUB)) st0 = CPI_OVERFLOW;
           wq = tw / (nsub > 0 ? nsub : 1);
           wr = tw % (nsub > 0 ? nsub : 1);
-          fmask = s > 0 ? -1 : 0;
-          dmask = s < p - 1 ? -1 : 0;
+          lmF = s == 0 ? 0x7fff : 0;            // stage 0 has no F producer: always available
+          asm("mov.b32 %0, %0;" : "+r"(lmF));   // opaque: (x | m) stays one LOP3
+          lastS = s == p - 1;
           sendF = s < p - 1;
           sendD = s > 0 && s < p;
           clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = pos = last_fd = 0;
-          hF = iF; hD = iD;
           emitw = 0;
+          // the last stage's D ring may hold a larger instance's arrivals: it must read 0
+          if (lastS && s < W - 1)
+            for (int k = 0; k < R; ++k) smem[iD + (k << 5)] = 0;
+          // parameter table: 0 = F, 1 = D, 2 + e + 2f = W sub-block with duration wq + e, memory
+          // delta f ? m_w : 0 (f: last sub-block of its W block)
+          tab[0 * 32] = make_int4(tf, mf, bwF, latF);
+          tab[1 * 32] = make_int4(td, md, bwB, latB);
+          tab[2 * 32] = make_int4(wq, 0, 0, 0);
+          tab[3 * 32] = make_int4(wq + 1, 0, 0, 0);
+          tab[4 * 32] = make_int4(wq, mw, 0, 0);
+          tab[5 * 32] = make_int4(wq + 1, mw, 0, 0);
         }
       }
       // warp-wide: lookahead prefix sums (segment scans), horizon bound, status ballots
@@ -140,70 +163,64 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
 
     // ------------------------------------------------------------------ one round
     const bool live = item >= 0 && s < p && nW < m;
-    const int leftF = __shfl_up_sync(GFULL, nF, 1, W);
-    const int rightD = __shfl_down_sync(GFULL, nD, 1, W);
-    const int aF = smem[hF];
-    const int aD = smem[hD];
-    const int availF = gmax(aF & fmask, tag);
-    const int availD = aD & dmask;
-    const bool knowF = nF < m && (fmask == 0 || leftF > nF);
-    const bool knowD = nD < m && (dmask == 0 ? nF > nD : rightD > nD);
-    const bool hasF = live && knowF && mem + mf <= mlim;       // Q15
-    const bool hasD = live && knowD;
-    const bool hasW = live && nW < nD;
-    int mnv = hasF ? availF : GINF;
-    mnv = gmin(mnv, hasD ? availD : GINF);
-    mnv = gmin(mnv, hasW ? clk : GINF);
-    const int tstar = (hasF || hasD || hasW) ? gmax(clk, mnv) : GINF;   // §4.2.2 :419
-    // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s
+    const int leftF = __shfl_up_sync(GFULL, nF, 1, W) | lmF;
+    const int rD0 = __shfl_down_sync(GFULL, nD, 1, W);
+    const int rightD = lastS ? nF : rD0;                // the last stage's D follows its own F
+    const int adF = iF + ((nF & Rm) << 5), adD = iD + ((nD & Rm) << 5);   // ring heads
+    const int availF = gmax(smem[adF], tag);
+    const int availD = smem[adD];
+    const bool hasF = live & (nF < m) & (leftF > nF) & (mem + mf <= mlim);   // Q15
+    const bool hasD = live & (nD < m) & (rightD > nD);
+    const bool hasW = live & (nW < nD);
+    const int mnv = gmin(gmin(hasF ? availF : GINF, hasD ? availD : GINF), hasW ? clk : GINF);
+    const int tstar = gmax(clk, mnv);                   // §4.2.2 :419 (GINF when nothing is eligible)
+    // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s.
+    // Width-W shuffles return the lane's own value past the segment edge, so the scans need no
+    // lane predicates (min with itself).
     int x = tstar - P, y = tstar + Q;
 #pragma unroll
     for (int d = 1; d < W; d <<= 1) {
-      const int xu = __shfl_up_sync(GFULL, x, d, W);
-      const int yd = __shfl_down_sync(GFULL, y, d, W);
-      x = (s >= d) ? gmin(x, xu) : x;
-      y = (s + d < W) ? gmin(y, yd) : y;
+      x = gmin(x, __shfl_up_sync(GFULL, x, d, W));
+      y = gmin(y, __shfl_down_sync(GFULL, y, d, W));
     }
     const int xe = __shfl_up_sync(GFULL, x, 1, W);
     const int ye = __shfl_down_sync(GFULL, y, 1, W);
     const int Lh = (s == 0) ? GINF : P + xe;
     const int Rh = (s == W - 1) ? GINF : ye - Q;
     // operation selection (Q13): opposite of the last full F/D block, then the other, then W
-    const bool cF = hasF && availF <= tstar, cD = hasD && availD <= tstar;
-    const bool pD = (last_fd == 1) ? cD : (cD && !cF);
-    const bool pF = !pD && cF;
+    const bool cF = hasF & (availF <= tstar), cD = hasD & (availD <= tstar);
+    const bool pD = cD & ((last_fd == 1) | !cF);
+    const bool pF = !pD & cF;
     // an F whose consumer ring is full (lead would exceed R: undersized ring hint) is not executed:
     // the lane stalls and the item is re-run by the global-ring fix-up pass (decisions unchanged)
-    const bool go = tstar < GINF && tstar < gmin(Lh, Rh) && !(pF && nF - nD >= R);
-    const bool pW = !pD && !pF;
-    const bool wfin = pW && (wsub + 1 == nsub);
-    const int dur = pF ? tf : (pD ? td : wq + (wsub < wr ? 1 : 0));
-    const int dm = pF ? mf : (pD ? md : (wfin ? mw : 0));
-    const int end = tstar + dur;
-    const int nl = gmax(end, pF ? linkF : linkB) + (pF ? bwF : bwB);   // FIFO link clock (App. X1)
-    const bool send = go && (pF ? sendF : (pD && sendD));
-    smem[send ? (pF ? hF + 1 : hD - 1) : iDum] = nl + (pF ? latF : latB);
+    // (t* < GINF matters: an idle neighbour's horizon term can exceed GINF)
+    const bool go = (tstar < GINF) & (tstar < gmin(Lh, Rh)) & !(pF & (nF - nD >= R));
+    const bool pW = !pD & !pF;
+    const bool wfin = wsub + 1 == nsub;
+    const int ti = pF ? 0 : (pD ? 1 : 2 + (wsub < wr ? 1 : 0) + (wfin ? 2 : 0));
+    const int4 ta = tab[ti << 5];                        // {duration, memory delta, link bw, latency}
+    const int end = tstar + ta.x;
+    const int nl = gmax(end, pF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
+    if (go & (pF ? sendF : (pD & sendD))) smem[pF ? adF + 1 : adD - 1] = nl + ta.w;
     // emit the 2-bit entry; a full word goes straight to global memory
     const uint32_t code = pF ? CP_OP_F : (pD ? CP_OP_D : CP_OP_W);
     const uint32_t w1 = emitw | (code << ((pos & 15) << 1));
-    const bool flush = go && (pos & 15) == 15;
+    const bool flush = go & ((pos & 15) == 15);
     if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
     emitw = go ? (flush ? 0u : w1) : emitw;
-    const bool gF = go && pF, gD = go && pD, gW = go && pW;
-    clk = go ? end : clk;
-    mem += go ? dm : 0;
+    const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
+    const bool gW = go & pW;
+    clk = gmadd(gi, end - clk, clk);
+    mem = gmadd(gi, ta.y, mem);
     peak = gmax(peak, mem);
-    linkF = gF ? nl : linkF;
-    linkB = gD ? nl : linkB;
-    const int h1 = (pF ? hF : hD) + 32;
-    hF = gF ? (h1 == iFend ? iF : h1) : hF;
-    hD = gD ? (h1 == iDend ? iD : h1) : hD;
-    nF += gF;
-    nD += gD;
+    linkF = gmadd(gFi, nl - linkF, linkF);
+    linkB = gmadd(gDi, nl - linkB, linkB);
+    nF = gmadd(gFi, 1, nF);
+    nD = gmadd(gDi, 1, nD);
     wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
-    nW += gW && wfin;
-    last_fd = gF ? 1 : (gD ? 2 : last_fd);
-    pos += go;
+    nW = gmadd((gW & wfin) ? 1 : 0, 1, nW);
+    last_fd = gFi ? 1 : (gDi ? 2 : last_fd);
+    pos = gmadd(gi, 1, pos);
     __syncwarp();
 
     // ------------------------------------------------------------------ rare: a segment went idle

@@ -197,9 +197,8 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
         nF = madd(gFi, 1, nF);
         nD = madd(gDi, 1, nD);
         went = madd((go & isW) ? 1 : 0, 1, went);
-        const bool gF = go & isF, gD = go & isDB;
         if (!kN1) {
-          wcap += gD ? nsub : 0;
+          wcap += gDi ? nsub : 0;
           wsub = (go & isW) ? (wfin ? 0 : wsub + 1) : wsub;
         }
         pos = madd(go ? 1 : 0, 1, pos);
