@@ -64,11 +64,11 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
   int linkF = 0, linkB = 0, pos = 0, last_fd = 0;
   uint32_t emitw = 0;
   long long item = -1;
-  bool need = true;
+  bool need = true, done = false;
 
   for (;;) {
     // ------------------------------------------------------------------ rare: (re)load instances
-    if (__any_sync(GFULL, need)) {
+    while (__any_sync(GFULL, need)) {
       bool fresh = false;
       int lat_b_s = 0, bw_b_s = 0, st0 = 0;
       if (need) {
@@ -157,117 +157,123 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
           need = true;
         }
       }
-      if (__all_sync(GFULL, item < 0)) break;
-      continue;                                          // re-check: failed items load again
-    }
+      if (__all_sync(GFULL, item < 0)) { done = true; break; }
+    }                                                    // (failed items load again)
+    if (done) break;
+    const bool hasItem = item >= 0;                      // fixed until the next reload
+    const bool onS = hasItem && s < p;
+    for (;;) {
+      __syncwarp();                                        // last round's ring stores -> these reads
 
-    // ------------------------------------------------------------------ one round
-    const bool live = item >= 0 && s < p && nW < m;
-    const int leftF = __shfl_up_sync(GFULL, nF, 1, W) | lmF;
-    const int rD0 = __shfl_down_sync(GFULL, nD, 1, W);
-    const int rightD = lastS ? nF : rD0;                // the last stage's D follows its own F
-    const int adF = iF + ((nF & Rm) << 5), adD = iD + ((nD & Rm) << 5);   // ring heads
-    const int availF = gmax(smem[adF], tag);
-    const int availD = smem[adD];
-    const bool hasF = live & (nF < m) & (leftF > nF) & (mem + mf <= mlim);   // Q15
-    const bool hasD = live & (nD < m) & (rightD > nD);
-    const bool hasW = live & (nW < nD);
-    const int mnv = gmin(gmin(hasF ? availF : GINF, hasD ? availD : GINF), hasW ? clk : GINF);
-    const int tstar = gmax(clk, mnv);                   // §4.2.2 :419 (GINF when nothing is eligible)
-    // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s.
-    // Width-W shuffles return the lane's own value past the segment edge, so the scans need no
-    // lane predicates (min with itself).
-    int x = tstar - P, y = tstar + Q;
-#pragma unroll
-    for (int d = 1; d < W; d <<= 1) {
-      x = gmin(x, __shfl_up_sync(GFULL, x, d, W));
-      y = gmin(y, __shfl_down_sync(GFULL, y, d, W));
-    }
-    const int xe = __shfl_up_sync(GFULL, x, 1, W);
-    const int ye = __shfl_down_sync(GFULL, y, 1, W);
-    const int Lh = (s == 0) ? GINF : P + xe;
-    const int Rh = (s == W - 1) ? GINF : ye - Q;
-    // operation selection (Q13): opposite of the last full F/D block, then the other, then W
-    const bool cF = hasF & (availF <= tstar), cD = hasD & (availD <= tstar);
-    const bool pD = cD & ((last_fd == 1) | !cF);
-    const bool pF = !pD & cF;
-    // an F whose consumer ring is full (lead would exceed R: undersized ring hint) is not executed:
-    // the lane stalls and the item is re-run by the global-ring fix-up pass (decisions unchanged)
-    // (t* < GINF matters: an idle neighbour's horizon term can exceed GINF)
-    const bool go = (tstar < GINF) & (tstar < gmin(Lh, Rh)) & !(pF & (nF - nD >= R));
-    const bool pW = !pD & !pF;
-    const bool wfin = wsub + 1 == nsub;
-    const int ti = pF ? 0 : (pD ? 1 : 2 + (wsub < wr ? 1 : 0) + (wfin ? 2 : 0));
-    const int4 ta = tab[ti << 5];                        // {duration, memory delta, link bw, latency}
-    const int end = tstar + ta.x;
-    const int nl = gmax(end, pF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
-    if (go & (pF ? sendF : (pD & sendD))) smem[pF ? adF + 1 : adD - 1] = nl + ta.w;
-    // emit the 2-bit entry; a full word goes straight to global memory
-    const uint32_t code = pF ? CP_OP_F : (pD ? CP_OP_D : CP_OP_W);
-    const uint32_t w1 = emitw | (code << ((pos & 15) << 1));
-    const bool flush = go & ((pos & 15) == 15);
-    if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
-    emitw = go ? (flush ? 0u : w1) : emitw;
-    const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
-    const bool gW = go & pW;
-    clk = gmadd(gi, end - clk, clk);
-    mem = gmadd(gi, ta.y, mem);
-    peak = gmax(peak, mem);
-    linkF = gmadd(gFi, nl - linkF, linkF);
-    linkB = gmadd(gDi, nl - linkB, linkB);
-    nF = gmadd(gFi, 1, nF);
-    nD = gmadd(gDi, 1, nD);
-    wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
-    nW = gmadd((gW & wfin) ? 1 : 0, 1, nW);
-    last_fd = gFi ? 1 : (gDi ? 2 : last_fd);
-    pos = gmadd(gi, 1, pos);
-    __syncwarp();
-
-    // ------------------------------------------------------------------ rare: a segment went idle
-    const unsigned bgo = __ballot_sync(GFULL, go);
-    const bool idle = item >= 0 && !(bgo & segmask);
-    if (__any_sync(GFULL, idle)) {
-      const unsigned b_unfin = __ballot_sync(GFULL, live);
-      const unsigned b_ring = __ballot_sync(GFULL, item >= 0 && s < p && nF < m && nF - nD >= R);
-      const unsigned b_mem = __ballot_sync(GFULL, item >= 0 && s < p && peak > mlim);
-      const bool complete = idle && !(b_unfin & segmask);
-      const bool on = item >= 0 && s < p;
-      int ms = on ? gmax(clk + tdp, tag) : 0, pk = on ? peak : 0;
-#pragma unroll
+      // ------------------------------------------------------------------ one round
+      const bool live = onS & (nW < m);
+      const int leftF = __shfl_up_sync(GFULL, nF, 1, W) | lmF;
+      const int rD0 = __shfl_down_sync(GFULL, nD, 1, W);
+      const int rightD = lastS ? nF : rD0;                // the last stage's D follows its own F
+      const int adF = iF + ((nF & Rm) << 5), adD = iD + ((nD & Rm) << 5);   // ring heads
+      const int availF = gmax(smem[adF], tag);
+      const int availD = smem[adD];
+      const bool hasF = live & (nF < m) & (leftF > nF) & (mem + mf <= mlim);   // Q15
+      const bool hasD = live & (nD < m) & (rightD > nD);
+      const bool hasW = live & (nW < nD);
+      const int mnv = gmin(gmin(hasF ? availF : GINF, hasD ? availD : GINF), hasW ? clk : GINF);
+      const int tstar = gmax(clk, mnv);                   // §4.2.2 :419 (GINF when nothing is eligible)
+      // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s.
+      // Width-W shuffles return the lane's own value past the segment edge, so the scans need no
+      // lane predicates (min with itself).
+      int x = tstar - P, y = tstar + Q;
+  #pragma unroll
       for (int d = 1; d < W; d <<= 1) {
-        ms = gmax(ms, __shfl_xor_sync(GFULL, ms, d, W));
-        pk = gmax(pk, __shfl_xor_sync(GFULL, pk, d, W));
+        x = gmin(x, __shfl_up_sync(GFULL, x, d, W));
+        y = gmin(y, __shfl_down_sync(GFULL, y, d, W));
       }
-      // first_start = max-plus prefix over F_0's path (every row starts with F_0)
-      const int cfw = on ? tf + bwF + latF : 0;
-      int Pf = cfw;
-#pragma unroll
-      for (int d = 1; d < W; d <<= 1) { const int t = __shfl_up_sync(GFULL, Pf, d, W); if (s >= d) Pf += t; }
-      Pf -= cfw;
-      int xf = (on ? tag : 0) - Pf;
-#pragma unroll
-      for (int d = 1; d < W; d <<= 1) { const int t = __shfl_up_sync(GFULL, xf, d, W); if (s >= d) xf = gmax(xf, t); }
-      if (idle) {
-        if (!complete && (b_ring & segmask)) {
-          // ring capacity reached (host under-sized R): re-run in the global-ring fix-up pass
-          if (s == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
-        } else {
-          const int st = !complete ? CPI_DEADLOCK : ((b_mem & segmask) ? CPI_MEM_EXCEEDED : 0);
-          if (s == 0) {
-            A.makespan[item] = complete ? (long long)ms : -1LL;
-            if (A.peak_mem) A.peak_mem[item] = complete ? pk : -1;
-            A.status[item] = st;
-          }
-          if (A.stage_stats && s < A.stage_stride) {
-            const int4 v = (complete && on) ? make_int4(Pf + xf, clk, m * (tf + td + tw), peak) : make_int4(0, 0, 0, 0);
-            *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = v;
-          }
-          if (s < A.stage_stride) {
-            if (on && (pos & 15)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
-            A.len[item * A.stage_stride + s] = (uint16_t)(on ? pos : 0);
-          }
+      const int xe = __shfl_up_sync(GFULL, x, 1, W);
+      const int ye = __shfl_down_sync(GFULL, y, 1, W);
+      const int Lh = (s == 0) ? GINF : P + xe;
+      const int Rh = (s == W - 1) ? GINF : ye - Q;
+      // operation selection (Q13): opposite of the last full F/D block, then the other, then W
+      const bool cF = hasF & (availF <= tstar), cD = hasD & (availD <= tstar);
+      const bool pD = cD & ((last_fd == 1) | !cF);
+      const bool pF = !pD & cF;
+      // an F whose consumer ring is full (lead would exceed R: undersized ring hint) is not executed:
+      // the lane stalls and the item is re-run by the global-ring fix-up pass (decisions unchanged)
+      // (t* < GINF matters: an idle neighbour's horizon term can exceed GINF)
+      const bool go = (tstar < GINF) & (tstar < gmin(Lh, Rh)) & !(pF & (nF - nD >= R));
+      const bool pW = !pD & !pF;
+      const bool wfin = wsub + 1 == nsub;
+      const int tiW = 2 + (wsub < wr ? 1 : 0) + (wfin ? 2 : 0);
+      const int ti = pF ? 0 : (pD ? 1 : tiW);
+      const int4 ta = tab[ti << 5];                        // {duration, memory delta, link bw, latency}
+      const int end = tstar + ta.x;
+      const int nl = gmax(end, pF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
+      if (go & (pF ? sendF : (pD & sendD))) smem[pF ? adF + 1 : adD - 1] = nl + ta.w;
+      // emit the 2-bit entry; a full word goes straight to global memory
+      const uint32_t code = pF ? CP_OP_F : (pD ? CP_OP_D : CP_OP_W);
+      const uint32_t w1 = emitw | (code << ((pos & 15) << 1));
+      const bool flush = go & ((pos & 15) == 15);
+      if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
+      emitw = go ? (flush ? 0u : w1) : emitw;
+      const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
+      const bool gW = go & pW;
+      clk = gmadd(gi, end - clk, clk);
+      mem = gmadd(gi, ta.y, mem);
+      peak = gmax(peak, mem);
+      linkF = gmadd(gFi, nl - linkF, linkF);
+      linkB = gmadd(gDi, nl - linkB, linkB);
+      nF = gmadd(gFi, 1, nF);
+      nD = gmadd(gDi, 1, nD);
+      wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
+      nW = gmadd((gW & wfin) ? 1 : 0, 1, nW);
+      last_fd = gFi ? 1 : (gDi ? 2 : last_fd);
+      pos = gmadd(gi, 1, pos);
+
+      // ------------------------------------------------------------------ rare: a segment went idle
+      const unsigned bgo = __ballot_sync(GFULL, go);
+      const bool idle = hasItem && !(bgo & segmask);
+      if (__any_sync(GFULL, idle)) {
+        const unsigned b_unfin = __ballot_sync(GFULL, live);
+        const unsigned b_ring = __ballot_sync(GFULL, item >= 0 && s < p && nF < m && nF - nD >= R);
+        const unsigned b_mem = __ballot_sync(GFULL, item >= 0 && s < p && peak > mlim);
+        const bool complete = idle && !(b_unfin & segmask);
+        const bool on = item >= 0 && s < p;
+        int ms = on ? gmax(clk + tdp, tag) : 0, pk = on ? peak : 0;
+  #pragma unroll
+        for (int d = 1; d < W; d <<= 1) {
+          ms = gmax(ms, __shfl_xor_sync(GFULL, ms, d, W));
+          pk = gmax(pk, __shfl_xor_sync(GFULL, pk, d, W));
         }
-        need = true;
+        // first_start = max-plus prefix over F_0's path (every row starts with F_0)
+        const int cfw = on ? tf + bwF + latF : 0;
+        int Pf = cfw;
+  #pragma unroll
+        for (int d = 1; d < W; d <<= 1) { const int t = __shfl_up_sync(GFULL, Pf, d, W); if (s >= d) Pf += t; }
+        Pf -= cfw;
+        int xf = (on ? tag : 0) - Pf;
+  #pragma unroll
+        for (int d = 1; d < W; d <<= 1) { const int t = __shfl_up_sync(GFULL, xf, d, W); if (s >= d) xf = gmax(xf, t); }
+        if (idle) {
+          if (!complete && (b_ring & segmask)) {
+            // ring capacity reached (host under-sized R): re-run in the global-ring fix-up pass
+            if (s == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
+          } else {
+            const int st = !complete ? CPI_DEADLOCK : ((b_mem & segmask) ? CPI_MEM_EXCEEDED : 0);
+            if (s == 0) {
+              A.makespan[item] = complete ? (long long)ms : -1LL;
+              if (A.peak_mem) A.peak_mem[item] = complete ? pk : -1;
+              A.status[item] = st;
+            }
+            if (A.stage_stats && s < A.stage_stride) {
+              const int4 v = (complete && on) ? make_int4(Pf + xf, clk, m * (tf + td + tw), peak) : make_int4(0, 0, 0, 0);
+              *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = v;
+            }
+            if (s < A.stage_stride) {
+              if (on && (pos & 15)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
+              A.len[item * A.stage_stride + s] = (uint16_t)(on ? pos : 0);
+            }
+          }
+          need = true;
+        }
+        break;                                           // reload the finished segments
       }
     }
   }
