@@ -18,5 +18,5 @@ for a, s, c, sm in ins:
         reg[-1][2] += c; reg[-1][3] += 1; reg[-1][5] += sm
     else:
         reg.append([a, c, c, 1, s, sm])
-for a, c0, c, k, s, sm in sorted(reg, key=lambda r: -r[2])[:14]:
+for a, c0, c, k, s, sm in sorted(reg, key=lambda r: -r[2])[:int(sys.argv[3]) if len(sys.argv) > 3 else 14]:
     print(f"{a[-5:]} n={k:4d} per-item {c / n_items:9.1f} ({100 * c / tot:5.1f}%) samples {sm:6d}  first: {s[:60]}")
