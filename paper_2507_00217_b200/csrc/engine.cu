@@ -34,14 +34,13 @@
 #include <algorithm>
 
 #include "engine.h"
+#include "grid_synth.cuh"
 #include "ptx.cuh"
 
 namespace cpk {
 
 constexpr int32_t INF = 1 << 30;        // > every valid tick value (guard U < 2^30)
 constexpr unsigned FULL = 0xffffffffu;
-constexpr unsigned long long KEY_NONE = 0x7fffffffffffffffull;   // no feasible candidate (INT64_MAX)
-constexpr unsigned long long KEY_OVER = 0x7ffffffffffffffeull;   // point not evaluated (CPI_OVERFLOW)
 
 __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
@@ -163,25 +162,11 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
       if (need_load) {
         need_load = false;
         if (kMode == MODE_SWEEP) {
-          // dynamic (point, candidate) tasks, most expensive first (largest m / n_sub at the end)
+          // dynamic (point, candidate) tasks, most expensive first (grid_synth.cuh)
           long long t = 0;
           if (s == 0) t = atomicAdd(A.sweep_counter, 1ull);
           t = __shfl_sync(segmask, t, seg * W);
-          // task space: active candidates (slowest axis) x points; reversed so the most expensive
-          // tasks (greedy n_sub = 4, largest m) start first, and neighbouring segments of a warp
-          // get the same candidate type (same round code path)
-          const unsigned msk = A.grid.cand_mask & 31u;
-          const long long npts = A.pt_hi - A.pt_lo;
-          const long long ntask = npts * __popc(msk);
-          item = -1;
-          if (t < ntask) {
-            const long long tid = ntask - 1 - t;
-            int ci = (int)(tid / npts);
-            unsigned mm = msk;
-            while (ci-- > 0) mm &= mm - 1;       // ci-th set bit of the mask
-            cand = __ffs(mm) - 1;
-            item = A.pt_lo + tid % npts;
-          }
+          item = sweep_task(A.grid.cand_mask & 31u, A.pt_lo, A.pt_hi, t, cand);
         } else {
           item = item_of(task);
           task += task_stride;
@@ -192,32 +177,17 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           int lat_b_s = 0, bw_b_s = 0;   // lane s validates boundary s in both directions
           c = LaneCfg{};
           if (kMode == MODE_SWEEP) {
-            const cp_grid& G = A.grid;
-            long long k = item;
-            const int i_dp = (int)(k % G.n_dp); k /= G.n_dp;
-            const int i_mem = (int)(k % G.n_mem); k /= G.n_mem;
-            const int i_bw = (int)(k % G.n_bw); k /= G.n_bw;
-            const int i_lat = (int)(k % G.n_lat); k /= G.n_lat;
-            const int i_mb = (int)(k % G.n_mb_n); k /= G.n_mb_n;
-            const int i_pp = (int)k;
-            c.p = G.n_pp_vals[i_pp];
-            c.m = G.n_mb_vals[i_mb];
+            const GridLane g = grid_lane(A.grid, item, s);
+            c.p = g.p;
+            c.m = g.m;
             cand_greedy = cand >= 2;
             c.nsub = cand_greedy ? (1 << (cand - 2)) : 1;
-            zero1 = G.base.flags & 1;
-            const int ndc = imin(G.n_dc, c.p);
-            if (s < c.p) {
-              c.tf = G.base.t_f[s]; c.td = G.base.t_d[s]; c.tw = G.base.t_w[s];
-              c.mf = G.base.m_f[s]; c.md = G.base.m_d[s]; c.mw = G.base.m_w[s];
-              c.mlim = (int)(((long long)G.mlim_x1000[i_mem] * c.p * c.mf + 500) / 1000);
-              c.tdp = G.tdp[i_dp];
-              c.tagate = G.base.t_ag[s];
-              const bool xf = (s < c.p - 1) && (s * ndc / c.p != (s + 1) * ndc / c.p);
-              const bool xb = (s > 0) && ((s - 1) * ndc / c.p != s * ndc / c.p);
-              c.latF = xf ? G.lat[i_lat] : 0; c.bwF = xf ? G.bw[i_bw] : 0;
-              c.latB = xb ? G.lat[i_lat] : 0; c.bwB = xb ? G.bw[i_bw] : 0;
-              lat_b_s = c.latF; bw_b_s = c.bwF;
-            }
+            zero1 = g.zero1;
+            c.tf = g.tf; c.td = g.td; c.tw = g.tw;
+            c.mf = g.mf; c.md = g.md; c.mw = g.mw; c.mlim = g.mlim;
+            c.tdp = g.tdp; c.tagate = g.tag;
+            c.latF = g.latF; c.bwF = g.bwF; c.latB = g.latB; c.bwB = g.bwB;
+            lat_b_s = c.latF; bw_b_s = c.bwF;
           } else {
             const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
             const cp_inst_v1* I = A.inst + ii;

@@ -57,8 +57,9 @@ int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int th
 int launch_sim32(const Args& a, int blocks, int threads, size_t smem, void* stream);
 int sim32_blocks_per_sm(int threads, size_t smem);
 // fast path of cp_greedy (greedy_fast.cu): compile-time segment width W in {8, 16, 32}, no timeline
-int launch_greedy_fast(int W, const Args& a, int blocks, int threads, size_t smem, void* stream);
-int greedy_fast_blocks_per_sm(int W, int threads, size_t smem);
+// grid = false: cp_greedy; grid = true: the greedy candidates of cp_sweep_shard
+int launch_greedy_fast(int W, bool grid, const Args& a, int blocks, int threads, size_t smem, void* stream);
+int greedy_fast_blocks_per_sm(int W, bool grid, int threads, size_t smem);
 int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem, bool timeline);
 int device_sm_count();
 int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, void* stream);

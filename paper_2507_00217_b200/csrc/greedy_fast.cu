@@ -13,6 +13,7 @@
 #include <stdint.h>
 
 #include "engine.h"
+#include "grid_synth.cuh"
 
 namespace cpk {
 
@@ -30,7 +31,11 @@ __device__ __forceinline__ int gmadd(int g, int d, int x) {
 }
 }  // namespace
 
-template <int W>
+// kGrid = false: cp_greedy -- instances from memory, plans + metrics out.
+// kGrid = true : cp_sweep_shard's greedy candidates -- (point, candidate) tasks from a device
+//                counter, instances synthesized from the grid (grid_synth.cuh), no plan output;
+//                the candidate's makespan and the point's packed argmin key out.
+template <int W, bool kGrid>
 __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant__ Args A) {
   extern __shared__ __align__(128) int32_t smem[];
   constexpr int NSEG = 32 / W;
@@ -64,6 +69,7 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
   int linkF = 0, linkB = 0, pos = 0, last_fd = 0;
   uint32_t emitw = 0;
   long long item = -1;
+  int cand = 0;                                        // sweep: candidate id (2/3/4 = greedy n_sub 1/2/4)
   bool need = true, done = false;
 
   for (;;) {
@@ -72,22 +78,40 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
       bool fresh = false;
       int lat_b_s = 0, bw_b_s = 0, st0 = 0;
       if (need) {
-        item = task < A.n_items ? task : -1;
-        task += tstride;
+        if (kGrid) {
+          long long t = 0;
+          if (s == 0) t = atomicAdd(A.sweep_counter, 1ull);
+          t = __shfl_sync(segmask, t, seg * W);
+          item = sweep_task(A.grid.cand_mask & 31u, A.pt_lo, A.pt_hi, t, cand);
+        } else {
+          item = task < A.n_items ? task : -1;
+          task += tstride;
+        }
         need = false;
         fresh = item >= 0;
         p = m = 0;
         if (fresh) {
-          const cp_inst_v1* I = A.inst + (A.n_inst == 1 ? 0 : item);
-          p = I->n_pp; m = I->n_mb; nsub = I->n_sub;
-          const bool zero1 = I->flags & 1;
+          bool zero1;
           tf = td = tw = mf = md = mw = mlim = tdp = tag = latF = bwF = latB = bwB = 0;
-          if (s < p) {
-            tf = I->t_f[s]; td = I->t_d[s]; tw = I->t_w[s];
-            mf = I->m_f[s]; md = I->m_d[s]; mw = I->m_w[s]; mlim = I->m_lim[s];
-            tdp = I->t_dp[s]; tag = I->t_ag[s];
-            if (s < p - 1) { latF = I->lat_f[s]; bwF = I->bw_f[s]; lat_b_s = I->lat_b[s]; bw_b_s = I->bw_b[s]; }
-            if (s > 0) { latB = I->lat_b[s - 1]; bwB = I->bw_b[s - 1]; }
+          if (kGrid) {
+            const GridLane g = grid_lane(A.grid, item, s);
+            p = g.p; m = g.m; nsub = 1 << (cand - 2);
+            zero1 = g.zero1;
+            tf = g.tf; td = g.td; tw = g.tw; mf = g.mf; md = g.md; mw = g.mw; mlim = g.mlim;
+            tdp = g.tdp; tag = g.tag;
+            latF = g.latF; bwF = g.bwF; latB = g.latB; bwB = g.bwB;
+            lat_b_s = latF; bw_b_s = bwF;
+          } else {
+            const cp_inst_v1* I = A.inst + (A.n_inst == 1 ? 0 : item);
+            p = I->n_pp; m = I->n_mb; nsub = I->n_sub;
+            zero1 = I->flags & 1;
+            if (s < p) {
+              tf = I->t_f[s]; td = I->t_d[s]; tw = I->t_w[s];
+              mf = I->m_f[s]; md = I->m_d[s]; mw = I->m_w[s]; mlim = I->m_lim[s];
+              tdp = I->t_dp[s]; tag = I->t_ag[s];
+              if (s < p - 1) { latF = I->lat_f[s]; bwF = I->bw_f[s]; lat_b_s = I->lat_b[s]; bw_b_s = I->bw_b[s]; }
+              if (s > 0) { latB = I->lat_b[s - 1]; bwB = I->bw_b[s - 1]; }
+            }
           }
           bool bad = p < 1 || p > CP_MAX_STAGES || m < 1 || nsub < 1;
           if (!bad && s < p)
@@ -96,7 +120,7 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
                     bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
           if (!zero1) tag = 0;
           st0 = bad ? CPI_BAD_INSTANCE : 0;
-          if (!st0 && (long long)(2 + nsub) * m > 16LL * A.words) st0 = CPI_BAD_PLAN;
+          if (!kGrid && !st0 && (long long)(2 + nsub) * m > 16LL * A.words) st0 = CPI_BAD_PLAN;
           if (!st0 && (p > W || m > CP_MAX_MB || nsub > CP_MAX_SUB)) st0 = CPI_OVERFLOW;
           wq = tw / (nsub > 0 ? nsub : 1);
           wr = tw % (nsub > 0 ? nsub : 1);
@@ -135,6 +159,8 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
       }
 #pragma unroll
       for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(GFULL, u, d, W);
+      // sweep: a greedy candidate with t_w < n_sub (reading Q12) is skipped -- no key, cand_ms -1
+      const unsigned b_skip = kGrid ? __ballot_sync(GFULL, fresh && s < p && tw < nsub) : 0u;
       const unsigned b_inst = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_INSTANCE);
       const unsigned b_plan = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_PLAN);
       const unsigned b_over = __ballot_sync(GFULL, fresh && st0 == CPI_OVERFLOW);
@@ -145,7 +171,10 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
                  : (b_plan & segmask) ? CPI_BAD_PLAN
                  : (b_over & segmask) ? CPI_OVERFLOW : 0;
         if (!st && u >= (long long)GINF) st = CPI_OVERFLOW;      // int32 horizon guard (Q21)
-        if (st) {
+        if (kGrid) {
+          if (st == CPI_OVERFLOW && s == 0) atomicMin(A.keys + item, KEY_OVER);
+          if (st || (b_skip & segmask)) need = true;
+        } else if (st) {
           if (s == 0) {
             A.makespan[item] = -1;
             if (A.peak_mem) A.peak_mem[item] = -1;
@@ -210,9 +239,11 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
       // emit the 2-bit entry; a full word goes straight to global memory
       const uint32_t code = pF ? CP_OP_F : (pD ? CP_OP_D : CP_OP_W);
       const uint32_t w1 = emitw | (code << ((pos & 15) << 1));
-      const bool flush = go & ((pos & 15) == 15);
-      if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
-      emitw = go ? (flush ? 0u : w1) : emitw;
+      if (!kGrid) {
+        const bool flush = go & ((pos & 15) == 15);
+        if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
+        emitw = go ? (flush ? 0u : w1) : emitw;
+      }
       const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
       const bool gW = go & pW;
       clk = gmadd(gi, end - clk, clk);
@@ -252,7 +283,18 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
   #pragma unroll
         for (int d = 1; d < W; d <<= 1) { const int t = __shfl_up_sync(GFULL, xf, d, W); if (s >= d) xf = gmax(xf, t); }
         if (idle) {
-          if (!complete && (b_ring & segmask)) {
+          if (kGrid) {
+            // one (point, candidate) task: its makespan and the point's packed argmin key.  The
+            // host sizes R to the lead bound, so a full ring cannot occur (it would mark the point
+            // unevaluated rather than guess); the greedy never deadlocks or exceeds memory (Q15).
+            if (s == 0) {
+              if (!complete) atomicMin(A.keys + item, KEY_OVER);
+              else if (!(b_mem & segmask)) {
+                if (A.cand_ms) A.cand_ms[item * 5 + cand] = ms;
+                atomicMin(A.keys + item, ((unsigned long long)ms << 8) | (unsigned)cand);
+              }
+            }
+          } else if (!complete && (b_ring & segmask)) {
             // ring capacity reached (host under-sized R): re-run in the global-ring fix-up pass
             if (s == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
           } else {
@@ -279,9 +321,9 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
   }
 }
 
-template <int W>
+template <int W, bool kGrid>
 static int launch_w(const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  const void* fn = (const void*)k_greedy_fast<W>;
+  const void* fn = (const void*)k_greedy_fast<W, kGrid>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
@@ -290,22 +332,29 @@ static int launch_w(const Args& a, int blocks, int threads, size_t smem, void* s
   return (int)cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
 }
 
-template <int W>
+template <int W, bool kGrid>
 static int bps_w(int threads, size_t smem) {
-  const void* fn = (const void*)k_greedy_fast<W>;
+  const void* fn = (const void*)k_greedy_fast<W, kGrid>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;
   return n > 0 ? n : 1;
 }
 
-int launch_greedy_fast(int W, const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  return W == 8 ? launch_w<8>(a, blocks, threads, smem, stream)
-                : (W == 16 ? launch_w<16>(a, blocks, threads, smem, stream) : launch_w<32>(a, blocks, threads, smem, stream));
+int launch_greedy_fast(int W, bool grid, const Args& a, int blocks, int threads, size_t smem, void* stream) {
+  if (grid)
+    return W == 8 ? launch_w<8, true>(a, blocks, threads, smem, stream)
+                  : (W == 16 ? launch_w<16, true>(a, blocks, threads, smem, stream)
+                             : launch_w<32, true>(a, blocks, threads, smem, stream));
+  return W == 8 ? launch_w<8, false>(a, blocks, threads, smem, stream)
+                : (W == 16 ? launch_w<16, false>(a, blocks, threads, smem, stream)
+                           : launch_w<32, false>(a, blocks, threads, smem, stream));
 }
 
-int greedy_fast_blocks_per_sm(int W, int threads, size_t smem) {
-  return W == 8 ? bps_w<8>(threads, smem) : (W == 16 ? bps_w<16>(threads, smem) : bps_w<32>(threads, smem));
+int greedy_fast_blocks_per_sm(int W, bool grid, int threads, size_t smem) {
+  if (grid)
+    return W == 8 ? bps_w<8, true>(threads, smem) : (W == 16 ? bps_w<16, true>(threads, smem) : bps_w<32, true>(threads, smem));
+  return W == 8 ? bps_w<8, false>(threads, smem) : (W == 16 ? bps_w<16, false>(threads, smem) : bps_w<32, false>(threads, smem));
 }
 
 }  // namespace cpk
