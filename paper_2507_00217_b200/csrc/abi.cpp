@@ -309,9 +309,9 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
   if (lo == hi) return CP_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned long long* ukeys = reinterpret_cast<unsigned long long*>(keys);
-  unsigned long long* counters = static_cast<unsigned long long*>(ws);   // two task counters per p-class
+  unsigned long long* counters = static_cast<unsigned long long*>(ws);   // four task counters per p-class (kCtrlBytes = 32 counters)
   if (cpk::launch_sweep_init(ukeys, cand_ms, lo, hi, stream) != cudaSuccess) return CP_ECUDA;
-  if (cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 16, st) != cudaSuccess) return CP_ECUDA;
+  if (cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 32, st) != cudaSuccess) return CP_ECUDA;
   // p is the slowest axis: one contiguous block of points per p-class; each class gets its own
   // segment width W and ring size, and the classes run concurrently on forked streams
   const long long per_pp = np / g->n_pp_n;
@@ -344,19 +344,30 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
     a.cand_ms = cand_ms;
     const int p = g->n_pp_vals[ip];
     // greedy candidates (n_sub 1/2/4): k_greedy_fast on synthesized instances, rings sized to the
-    // lead bound (rounded to a power of two) so they cannot fill; static candidates (GPipe, 1F1B)
-    // and anything the fast path cannot hold in shared memory: the generic engine
+    // lead bound (rounded to a power of two) so they cannot fill.  Ring size sets residency, so
+    // tasks whose own bound is <= 32 run in a launch with 32-slot rings and only the rest in one
+    // sized to the class maximum.  Static candidates (GPipe, 1F1B) and anything the fast path
+    // cannot hold in shared memory: the generic engine.
     unsigned engine_mask = g->cand_mask & 31u;
     const unsigned greedy_mask = engine_mask & 0x1cu;
     if (greedy_mask && !getenv_nofast()) {
       const int Wd = p <= 8 ? 8 : (p <= 16 ? 16 : 32);
-      cpk::Args ag = a;
-      ag.grid.cand_mask = greedy_mask;
-      ag.sweep_counter = counters + 2 * c + 1;
-      ag.ring_slots = 1 << lg2_ceil(sweep_ring_slots(g, p));
-      ag.smem_words_per_warp = (cpk::kGreedyTableWords + 2 * ag.ring_slots * 32 + 3) & ~3;
-      const size_t per_warp = (size_t)ag.smem_words_per_warp * 4;
-      if (per_warp <= kMaxSmemPerBlock) {
+      const int lead_max = sweep_ring_slots(g, p);
+      // tiers of lead bound: [0, 32], (32, 64], (64, lead_max]
+      const int edge[3] = {32, 64, CP_MAX_MB};
+      int ntier = 1;
+      while (ntier < 3 && lead_max > edge[ntier - 1]) ++ntier;
+      const size_t big_warp = (size_t)((cpk::kGreedyTableWords + 2 * (1 << lg2_ceil(lead_max)) * 32 + 3) & ~3) * 4;
+      bool ok = big_warp <= kMaxSmemPerBlock;
+      for (int tier = 0; tier < ntier && ok; ++tier) {
+        cpk::Args ag = a;
+        ag.grid.cand_mask = greedy_mask;
+        ag.sweep_counter = counters + 4 * c + 1 + tier;
+        ag.tier_lo = tier == 0 ? 0 : edge[tier - 1] + 1;
+        ag.tier_hi = tier == ntier - 1 ? CP_MAX_MB : edge[tier];
+        ag.ring_slots = 1 << lg2_ceil(std::min(lead_max, ag.tier_hi));
+        ag.smem_words_per_warp = (cpk::kGreedyTableWords + 2 * ag.ring_slots * 32 + 3) & ~3;
+        const size_t per_warp = (size_t)ag.smem_words_per_warp * 4;
         const int wpb = per_warp * 2 <= kMaxSmemPerBlock ? 2 : 1, threads = 32 * wpb;
         const size_t smem = per_warp * wpb;
         const int bps = cpk::greedy_fast_blocks_per_sm(Wd, true, threads, smem);
@@ -364,12 +375,12 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
         const long long need = ((a1 - a0) * __builtin_popcount(greedy_mask) + segs - 1) / segs;
         const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
         if (cpk::launch_greedy_fast(Wd, true, ag, blocks, threads, smem, cs) != cudaSuccess) rc = CP_ECUDA;
-        engine_mask &= ~greedy_mask;
       }
+      if (ok) engine_mask &= ~greedy_mask;
     }
     if (!rc && engine_mask) {
       a.grid.cand_mask = engine_mask;
-      a.sweep_counter = counters + 2 * c;
+      a.sweep_counter = counters + 4 * c;
       a.seg_lg = lg2_ceil(p);
       a.ring_slots = sweep_ring_slots(g, p);
       rc = launch_pass(cpk::MODE_SWEEP, false, a, (a1 - a0) * __builtin_popcount(engine_mask), 32 >> a.seg_lg, cs);

@@ -48,6 +48,7 @@ struct Args {
   unsigned long long* keys;
   unsigned long long* sweep_counter;   // dynamic task counter of a sweep launch (workspace)
   int32_t* cand_ms;
+  int32_t tier_lo, tier_hi;            // sweep greedy: only tasks whose ring lead bound is in [lo, hi]
   cp_grid grid;
 };
 

@@ -159,8 +159,17 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
       }
 #pragma unroll
       for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(GFULL, u, d, W);
-      // sweep: a greedy candidate with t_w < n_sub (reading Q12) is skipped -- no key, cand_ms -1
-      const unsigned b_skip = kGrid ? __ballot_sync(GFULL, fresh && s < p && tw < nsub) : 0u;
+      // sweep: a greedy candidate with t_w < n_sub (reading Q12) is skipped -- no key, cand_ms -1;
+      // a task whose ring lead bound min(m, max_s floor(M_L/m_f)) lies outside this
+      // launch's tier is left to the launch sized for it
+      unsigned b_skip = 0u;
+      if (kGrid) {
+        int lead = (fresh && s < p && mf > 0) ? mlim / mf : 0;
+#pragma unroll
+        for (int d = 1; d < W; d <<= 1) lead = gmax(lead, __shfl_xor_sync(GFULL, lead, d, W));
+        lead = gmin(lead, m);
+        b_skip = __ballot_sync(GFULL, fresh && ((s < p && tw < nsub) || lead < A.tier_lo || lead > A.tier_hi));
+      }
       const unsigned b_inst = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_INSTANCE);
       const unsigned b_plan = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_PLAN);
       const unsigned b_over = __ballot_sync(GFULL, fresh && st0 == CPI_OVERFLOW);
