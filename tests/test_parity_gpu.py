@@ -423,6 +423,22 @@ def test_fast_paths_ring_overflow_fixup(O):
         assert ms[i] == O.simulate(b.item(0), c[i], l_[i])["makespan"]
 
 
+def test_sweep_ring_tier_edges(O):
+    """Greedy sweep tasks run in ring-size tiers by lead bound min(m, floor(M_L/m_f)) (<= 32,
+    <= 64, rest; DESIGN.md §7 Sweep).  Memory scales chosen so the bound is exactly 31, 32, 33, 63,
+    64, 65 and 96/128 at p = 16: every point and candidate checked against the oracle."""
+    from workloads.core import Grid
+    base = K.uniform_instance(16, 8, 2, 100, 120, 80)
+    grid = Grid(base=base, n_dc=2, pp_vals=[16], mb_vals=[96, 128], lat=np.array([0, 150]), bw=np.array([0, 60]),
+                mlim_x1000=np.array([1938, 2000, 2063, 3938, 4000, 4063, 8000]), tdp=np.array([0]),
+                cand_mask=0b11111)
+    leads = sorted({min(m, ((x * 16 * 2 + 500) // 1000) // 2) for m in (96, 128) for x in grid.mlim_x1000})
+    assert leads == [31, 32, 33, 63, 64, 65, 96, 128], leads
+    keys, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
+
+
 def test_sweep_edge_grids(O):
     """Sweep grids with more DCs than stages (p = 2, 3 with 4 DCs), a ZeRO-1 base with allgather
     times, DP tails, and a candidate subset (1F1B + greedy n_sub = 2 only)."""
