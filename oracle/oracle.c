@@ -44,12 +44,13 @@ int64_t or_reserve_window(or_link* L, int64_t t_ready, int64_t width) {
 
 /* ------------------------------------------------------------------------- */
 /* Instance invariants: SPEC.md:46-50 (durations > 0, delays >= 0, m_f > 0,
- * m_d,m_w <= 0, sum 0, m_lim >= m_f) and Q12 (t_w >= n_sub).                  */
+ * m_d,m_w <= 0, sum 0, m_lim >= m_f) and Q12 (every block >= n_sub ticks, so each of
+ * its n_sub sub-blocks (Alg. 1 :398-403) lasts at least one tick).     */
 int32_t or_validate_instance(const or_inst* I) {
   if (I->p < 1 || I->p > OR_MAXP || I->m < 1 || I->n_sub < 1) return OR_ST_BAD_INSTANCE;
   for (int s = 0; s < I->p; ++s) {
     if (I->t_f[s] <= 0 || I->t_d[s] <= 0 || I->t_w[s] <= 0) return OR_ST_BAD_INSTANCE;
-    if (I->t_w[s] < I->n_sub) return OR_ST_BAD_INSTANCE;
+    if (I->t_f[s] < I->n_sub || I->t_d[s] < I->n_sub || I->t_w[s] < I->n_sub) return OR_ST_BAD_INSTANCE;
     if (I->m_f[s] <= 0 || I->m_d[s] > 0 || I->m_w[s] > 0) return OR_ST_BAD_INSTANCE;
     if (I->m_f[s] + I->m_d[s] + I->m_w[s] != 0) return OR_ST_BAD_INSTANCE;
     if (I->m_lim[s] < I->m_f[s]) return OR_ST_BAD_INSTANCE;

@@ -442,7 +442,8 @@ int32_t cp_validate_instance(const cp_inst_v1* I, char* msg, size_t msg_len) {
   if (I->n_sub < 1) return fail(CPI_BAD_INSTANCE, "n_sub < 1", -1);
   for (int s = 0; s < I->n_pp; ++s) {
     if (I->t_f[s] <= 0 || I->t_d[s] <= 0 || I->t_w[s] <= 0) return fail(CPI_BAD_INSTANCE, "durations must be > 0", s);
-    if (I->t_w[s] < I->n_sub) return fail(CPI_BAD_INSTANCE, "t_w < n_sub (integer sub-blocks)", s);
+    if (I->t_f[s] < I->n_sub || I->t_d[s] < I->n_sub || I->t_w[s] < I->n_sub)
+      return fail(CPI_BAD_INSTANCE, "a block shorter than n_sub ticks (every sub-block >= 1 tick, reading Q12)", s);
     if (I->m_f[s] <= 0 || I->m_d[s] > 0 || I->m_w[s] > 0) return fail(CPI_BAD_INSTANCE, "memory delta signs", s);
     if ((long long)I->m_f[s] + I->m_d[s] + I->m_w[s] != 0) return fail(CPI_BAD_INSTANCE, "memory deltas do not sum to zero", s);
     if (I->m_lim[s] < I->m_f[s]) return fail(CPI_BAD_INSTANCE, "m_lim < m_f", s);

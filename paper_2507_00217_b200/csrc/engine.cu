@@ -125,6 +125,22 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
 #define POK(off, tag) true
 #endif
 
+  // Output rows r = s, s + W, ... < stage_stride that this lane finishes for an item: zero stats
+  // for rows no lane owns (r >= W); greedy: len and every plan word past the emitted entries zeroed
+  // (the row's own words up to `used` are written by the caller), so outputs are fully defined.
+  auto finish_rows = [&](long long it, int used) {
+    if (kMode == MODE_SWEEP) return;
+    for (int r = s; r < A.stage_stride; r += W) {
+      const long long rb = it * A.stage_stride + r;
+      if (A.stage_stats && r != s) *reinterpret_cast<int4*>(A.stage_stats + rb * 4) = make_int4(0, 0, 0, 0);
+      if (kMode == MODE_GREEDY) {
+        const int u = r == s ? used : 0;
+        for (int k = (u + 15) >> 4; k < A.words; ++k) A.ops[(it * A.words + k) * A.stage_stride + r] = 0u;
+        A.len[rb] = (uint16_t)u;
+      }
+    }
+  };
+
   auto item_of = [&](long long t) -> long long {
     if (A.from_list) return (t < *(volatile int32_t*)A.ovf_count) ? (long long)A.ovf_list[t] : -1;
     return t < A.n_items ? t : -1;
@@ -206,7 +222,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           // instance invariants (readings Q10, Q12)
           bool bad = c.p < 1 || c.p > CP_MAX_STAGES || c.m < 1 || c.nsub < 1;
           if (!bad && s < c.p) {
-            bad = !(c.tf > 0 && c.td > 0 && c.tw > 0 && c.tw >= c.nsub && c.mf > 0 && c.md <= 0 && c.mw <= 0 &&
+            bad = !(c.tf >= c.nsub && c.td >= c.nsub && c.tw >= c.nsub && c.nsub >= 1 && c.mf > 0 && c.md <= 0 && c.mw <= 0 &&
                     (long long)c.mf + c.md + c.mw == 0 && c.mlim >= c.mf && c.tdp >= 0 && c.tagate >= 0 &&
                     c.latF >= 0 && c.bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
           }
@@ -252,11 +268,13 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         }
         for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(FULL, u, d, W);
         // sweep: candidate statically infeasible (GPipe peak m*m_f, 1F1B peak min(p-s,m)*m_f (Z5),
-        // greedy t_w < n_sub (Q12)) or masked out -> skipped (its cand_ms stays -1, no key)
+        // greedy with a block shorter than n_sub ticks (Q12)) or masked out -> skipped (its cand_ms
+        // stays -1, no key)
         bool skip_lane = false;
         if (kMode == MODE_SWEEP && just_loaded && s < c.p)
           skip_lane = cand == 0 ? (long long)c.m * c.mf > c.mlim
-                                : (cand == 1 ? (long long)imin(c.p - s, c.m) * c.mf > c.mlim : c.tw < c.nsub);
+                                : (cand == 1 ? (long long)imin(c.p - s, c.m) * c.mf > c.mlim
+                                             : (c.tf < c.nsub || c.td < c.nsub || c.tw < c.nsub));
         const unsigned b_skip = __ballot_sync(FULL, skip_lane || (kMode == MODE_SWEEP && just_loaded &&
                                                                  !((A.grid.cand_mask >> cand) & 1u)));
         const unsigned b_inst = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_INSTANCE);
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
             }
             if (A.stage_stats && s < A.stage_stride)
               *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = make_int4(0, 0, 0, 0);
-            if (kMode == MODE_GREEDY && s < A.stage_stride) A.len[item * A.stage_stride + s] = 0;
+            finish_rows(item, 0);
             need_load = true;
           }
         }
@@ -521,9 +539,9 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
             } else if (own && (pos & 15)) {
               A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
             }
-            if (CHK(item, n_it, 11)) A.len[item * A.stage_stride + s] = (uint16_t)(own ? pos : 0);
             emitw = 0;
           }
+          finish_rows(item, (kMode == MODE_GREEDY && s < c.p) ? pos : 0);
           need_load = true;
         }
         if (use_tma && need_load) { cur_buf ^= 1; plan_off = cur_buf * PW * 32 + lane; }

@@ -68,6 +68,19 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
   int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0;
   int linkF = 0, linkB = 0, pos = 0, last_fd = 0;
   uint32_t emitw = 0;
+  // Output rows r = s, s + W, ... < stage_stride of an item: len, every plan word past the emitted
+  // entries zeroed (outputs are fully defined, whatever the caller's buffer held) and, for rows no
+  // lane owns, zero stats.  The row's own partial last word is written by the caller.
+  auto finish_rows = [&](long long it, int used, bool stats_own) {
+    if (kGrid) return;
+    for (int r = s; r < A.stage_stride; r += W) {
+      const int u = r == s ? used : 0;
+      const long long rb = it * A.stage_stride + r;
+      for (int k = (u + 15) >> 4; k < A.words; ++k) A.ops[(it * A.words + k) * A.stage_stride + r] = 0u;
+      A.len[rb] = (uint16_t)u;
+      if (A.stage_stats && (r != s || stats_own)) *reinterpret_cast<int4*>(A.stage_stats + rb * 4) = make_int4(0, 0, 0, 0);
+    }
+  };
   long long item = -1;
   int cand = 0;                                        // sweep: candidate id (2/3/4 = greedy n_sub 1/2/4)
   bool need = true, done = false;
@@ -115,7 +128,7 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
           }
           bool bad = p < 1 || p > CP_MAX_STAGES || m < 1 || nsub < 1;
           if (!bad && s < p)
-            bad = !(tf > 0 && td > 0 && tw > 0 && tw >= nsub && mf > 0 && md <= 0 && mw <= 0 &&
+            bad = !(tf >= nsub && td >= nsub && tw >= nsub && nsub >= 1 && mf > 0 && md <= 0 && mw <= 0 &&
                     (long long)mf + md + mw == 0 && mlim >= mf && tdp >= 0 && tag >= 0 && latF >= 0 &&
                     bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
           if (!zero1) tag = 0;
@@ -159,7 +172,8 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
       }
 #pragma unroll
       for (int d = 1; d < W; d <<= 1) u += __shfl_xor_sync(GFULL, u, d, W);
-      // sweep: a greedy candidate with t_w < n_sub (reading Q12) is skipped -- no key, cand_ms -1;
+      // sweep: a greedy candidate with a block shorter than n_sub ticks (reading Q12) is skipped --
+      // no key, cand_ms -1;
       // a task whose ring lead bound min(m, max_s floor(M_L/m_f)) lies outside this
       // launch's tier is left to the launch sized for it
       unsigned b_skip = 0u;
@@ -168,7 +182,8 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
 #pragma unroll
         for (int d = 1; d < W; d <<= 1) lead = gmax(lead, __shfl_xor_sync(GFULL, lead, d, W));
         lead = gmin(lead, m);
-        b_skip = __ballot_sync(GFULL, fresh && ((s < p && tw < nsub) || lead < A.tier_lo || lead > A.tier_hi));
+        b_skip = __ballot_sync(GFULL, fresh && ((s < p && (tf < nsub || td < nsub || tw < nsub)) ||
+                                                 lead < A.tier_lo || lead > A.tier_hi));
       }
       const unsigned b_inst = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_INSTANCE);
       const unsigned b_plan = __ballot_sync(GFULL, fresh && st0 == CPI_BAD_PLAN);
@@ -189,9 +204,7 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
             if (A.peak_mem) A.peak_mem[item] = -1;
             A.status[item] = st;
           }
-          if (A.stage_stats && s < A.stage_stride)
-            *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = make_int4(0, 0, 0, 0);
-          if (s < A.stage_stride) A.len[item * A.stage_stride + s] = 0;
+          finish_rows(item, 0, true);             // len 0, every word 0, stats 0
           need = true;
         }
       }
@@ -317,10 +330,8 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
               const int4 v = (complete && on) ? make_int4(Pf + xf, clk, m * (tf + td + tw), peak) : make_int4(0, 0, 0, 0);
               *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = v;
             }
-            if (s < A.stage_stride) {
-              if (on && (pos & 15)) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
-              A.len[item * A.stage_stride + s] = (uint16_t)(on ? pos : 0);
-            }
+            if (on && (pos & 15) && s < A.stage_stride) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
+            finish_rows(item, on ? pos : 0, false);
           }
           need = true;
         }

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args
     }
     bool bad = p < 1 || p > CP_MAX_STAGES || m < 1 || nsub < 1;
     if (!bad && s < p)
-      bad = !(tf > 0 && td > 0 && tw > 0 && tw >= nsub && mf > 0 && md <= 0 && mw <= 0 &&
+      bad = !(tf >= nsub && td >= nsub && tw >= nsub && nsub >= 1 && mf > 0 && md <= 0 && mw <= 0 &&
               (long long)mf + md + mw == 0 && mlim >= mf && tdp >= 0 && tag >= 0 && latF >= 0 && bwF >= 0 &&
               latbs >= 0 && bwbs >= 0);
     if (!zero1) tag = 0;

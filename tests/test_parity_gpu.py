@@ -155,7 +155,9 @@ def test_bad_instances_and_overflow_guard(O):
         if k == 0: batch.t_f[i, s] = 0
         elif k == 1: batch.m_w[i, s] -= 1
         elif k == 2: batch.m_lim[i, s] = batch.m_f[i, s] - 1
-        elif k == 3: batch.t_w[i, s] = batch.n_sub[i] - 1 if batch.n_sub[i] > 1 else 0
+        elif k == 3:                                      # a block shorter than n_sub ticks (Q12)
+            fld = ("t_f", "t_d", "t_w")[int(rng.integers(3))]
+            getattr(batch, fld)[i, s] = batch.n_sub[i] - 1 if batch.n_sub[i] > 1 else 0
         elif k == 4 and batch.p[i] > 1: batch.lat_b[i, 0] = -1
         elif k == 5: batch.t_dp[i, s] = -5
     big = K.uniform_instance(4, 8, 2, 10**8, 10**8, 10**8)       # U = 9.6e9 >= 2^30

@@ -143,7 +143,8 @@ def random_instances(n, seed=SEED ^ 0x77, max_p=MAXP, max_m=24, max_cost=200, ma
         for fld in ("t_f", "t_d", "t_w"):
             v = rng.integers(1, max_cost + 1, size=p) if not uni else np.full(p, rng.integers(1, max_cost + 1))
             getattr(b, fld)[i, :p] = v
-        b.t_w[i, :p] = np.maximum(b.t_w[i, :p], ns)
+        for fld in ("t_f", "t_d", "t_w"):            # every sub-block >= 1 tick (reading Q12)
+            getattr(b, fld)[i, :p] = np.maximum(getattr(b, fld)[i, :p], ns)
         mf = rng.integers(1, 5, size=p)
         md = -rng.integers(0, mf + 1)
         b.m_f[i, :p], b.m_d[i, :p], b.m_w[i, :p] = mf, md, -mf - md
