@@ -369,9 +369,12 @@ def run_ours(args):
         }
         if ws == 1 and not args.no_cpu:
             cores = os.cpu_count() or 1
-            v, wall, nn = oracle_throughput(min(16000, 2000 * cores), cores)
+            v, wall, nn = oracle_throughput(min(32000, 2000 * cores), cores)
+            n1, t1 = _oracle_slice((list(range(2000)), 1))          # one host core
             line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                                    "sample": f"{nn} config-4 schedules (ids 0..), {cores} processes, {wall:.1f} s wall"}
+                                    "value_1core": n1 / t1,
+                                    "sample": f"{nn} config-4 schedules (ids 0..), {cores} processes, {wall:.1f} s wall "
+                                              f"({nn * t1 / n1:.1f} s of CPU work); 1-core: {n1} schedules in {t1:.1f} s"}
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
