@@ -433,6 +433,29 @@ void or_build_1f1b(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t ma
     len[s] = k;
   }
 }
+/* ZB-H1 (Table tab:ppschedules :472; "1F1B ordering with D/W split and W blocks
+ * deferred ... at unchanged peak activation memory"), reading Q31: stage s runs
+ *   warm-up   F x w,  w = min(p - s, m)
+ *   then for k = 0 .. m-1:  D_k,  W_{k-s} if k >= s,  F (the next one) if any remain
+ *   then the W blocks still owed (the last min(s, m)).
+ * Stage s defers its W blocks by s microbatches (stage 0 keeps W behind its D, the last stage
+ * fills its tear-down with them).                                                      */
+void or_build_zbh1(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen) {
+  for (int s = 0; s < p; ++s) {
+    int8_t* row = codes + (int64_t)s * maxlen;
+    int w = p - s; if (w > m) w = m;
+    int k = 0, nF = 0, nW = 0;
+    for (int i = 0; i < w; ++i) { row[k++] = OR_F; ++nF; }
+    for (int j = 0; j < m; ++j) {
+      row[k++] = OR_D;
+      if (j >= s) { row[k++] = OR_W; ++nW; }
+      if (nF < m) { row[k++] = OR_F; ++nF; }
+    }
+    while (nW < m) { row[k++] = OR_W; ++nW; }
+    len[s] = k;
+  }
+}
+
 void or_build_gpipe(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen) {
   for (int s = 0; s < p; ++s) {
     int k = 0;

@@ -96,6 +96,8 @@ int32_t or_greedy(const or_inst* I, int8_t* codes, int32_t* len, int32_t maxlen,
 /* Static builders (combined backward B). Return number of entries per stage written. */
 void or_build_1f1b(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
 void or_build_gpipe(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
+/* ZB-H1 (split D/W), reading Q31: maxlen >= 3m. */
+void or_build_zbh1(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
 
 /* Exhaustive optimum over all valid split plans with n_sub = 1 (tiny instances only).
  * Writes the best plan; returns number of complete (non-deadlocked) plans evaluated, -1 if too large. */

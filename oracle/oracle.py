@@ -83,7 +83,7 @@ def lib():
             f.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32, P(OrResult), P(C.c_int64)]
         L.or_check_plan.restype = C.c_int32
         L.or_check_plan.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32]
-        for fn in ("or_build_1f1b", "or_build_gpipe"):
+        for fn in ("or_build_1f1b", "or_build_gpipe", "or_build_zbh1"):
             getattr(L, fn).argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
         L.or_enumerate_opt.restype = C.c_int64
         L.or_enumerate_opt.argtypes = [P(OrInst), C.c_int64, P(C.c_int8), P(C.c_int32), C.c_int32, P(OrResult)]
@@ -171,10 +171,10 @@ def check_plan(d, codes, lens=None) -> int:
 
 
 def build_static(kind: str, p: int, m: int):
-    maxlen = 2 * m
+    maxlen = 3 * m if kind == "zbh1" else 2 * m
     c = np.zeros((p, maxlen), dtype=np.int8)
     ln = np.zeros(p, dtype=np.int32)
-    fn = {"1f1b": lib().or_build_1f1b, "gpipe": lib().or_build_gpipe}[kind]
+    fn = {"1f1b": lib().or_build_1f1b, "gpipe": lib().or_build_gpipe, "zbh1": lib().or_build_zbh1}[kind]
     fn(p, m, c.ctypes.data_as(C.POINTER(C.c_int8)), ln.ctypes.data_as(C.POINTER(C.c_int32)), maxlen)
     return c, ln
 

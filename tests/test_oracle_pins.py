@@ -144,6 +144,56 @@ def test_Z6_greedy_matches_zbh1_closed_form(oracle_lib):
         assert r["status"] == 0 and r["makespan"] == (3 * m + p - 1) * f
 
 
+# --------------------------------------------------------------------------- ZB-H1 (reading Q31)
+def test_zbh1_closed_form_zero_delay(oracle_lib):
+    """ZB-H1's published bubble (p-1)(T_F + T_B - T_W) (Qi et al. via PAPER.md :443,
+    :472): makespan m(f+d+w) + (p-1)(f+d-w) at zero delay with uniform costs, m >= p and
+    w <= min(f, d); every built plan is valid (Q29)."""
+    rng = np.random.default_rng(31)
+    for _ in range(120):
+        p = int(rng.integers(1, 9))
+        m = int(rng.integers(p, 3 * p + 2))
+        d_, f = (int(x) for x in rng.integers(1, 200, size=2))
+        w = int(rng.integers(1, min(f, d_) + 1))
+        dd = inst(p, m, int(rng.integers(1, 5)), f, d_, w, mlim_x1000=1000)
+        c, l_ = oracle_lib.build_static("zbh1", p, m)
+        assert oracle_lib.check_plan(dd, c, l_) == 0
+        r = oracle_lib.simulate(dd, c, l_)
+        assert r["status"] == 0 and r["makespan"] == m * (f + d_ + w) + (p - 1) * (f + d_ - w), (p, m, f, d_, w)
+
+
+def test_zbh1_peak_memory_and_budget(oracle_lib):
+    """Q31 memory: with m >= p, stage s peaks at (p-s) m_f - s m_w, which never exceeds the 1F1B
+    device budget p m_f (Q9; "unchanged peak activation memory")."""
+    rng = np.random.default_rng(32)
+    for _ in range(80):
+        p = int(rng.integers(1, 9))
+        m = int(rng.integers(p, 3 * p + 2))
+        mf = int(rng.integers(1, 6))
+        md = -int(rng.integers(0, mf + 1))
+        mw = -mf - md
+        dd = inst(p, m, 1, 7, 5, 3, m_f=mf, m_d=md, m_w=mw, mlim_x1000=1000)
+        r = oracle_lib.simulate(dd, *oracle_lib.build_static("zbh1", p, m))
+        assert list(r["peak"]) == [(p - s) * mf - s * mw for s in range(p)]
+        assert max(r["peak"]) <= p * mf and r["status"] == 0
+
+
+def test_zbh1_vs_1f1b_and_greedy_zero_delay(oracle_lib):
+    """makespan(ZB-H1) <= makespan(1F1B) at zero delay, uniform, t_d = t_w; SPEC.md
+    acceptance 3 / PAPER.md :443: the greedy with the 1F1B memory budget matches ZB-H1 (n_pp in
+    {4, 8}, n_mb = 2 n_pp; exact here, Z6)."""
+    for p in (4, 8):
+        m = 2 * p
+        for f, b in ((100, 100), (60, 100), (100, 40)):
+            dd = inst(p, m, 2, f, b, b, mlim_x1000=1000)
+            z = oracle_lib.simulate(dd, *oracle_lib.build_static("zbh1", p, m))["makespan"]
+            one = oracle_lib.simulate(dd, *oracle_lib.build_static("1f1b", p, m))["makespan"]
+            assert z <= one
+        dd = inst(p, m, 2, 100, 100, 100, mlim_x1000=1000)
+        z = oracle_lib.simulate(dd, *oracle_lib.build_static("zbh1", p, m))["makespan"]
+        assert oracle_lib.greedy(dd)["makespan"] == z == (3 * m + p - 1) * 100
+
+
 def test_dp_tail_and_zero1_shift(oracle_lib):
     """DP overlap (PAPER.md:363): AR after the last W/B -> 1F1B zero delay ends at Z1 + T_dp;
     ZeRO-1 AG before the first F shifts everything by T_ag (uniform); zero volume = no change."""
