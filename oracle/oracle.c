@@ -603,13 +603,14 @@ uint64_t or_sweep_point(const or_grid* G, int64_t point, int64_t* cand_ms) {
   int32_t len[OR_MAXP];
   or_result r;
   uint64_t best = UINT64_MAX;
-  static const int nsub_of[5] = {0, 0, 1, 2, 4};
-  for (int c = 0; c < 5; ++c) {
+  static const int nsub_of[6] = {0, 0, 1, 2, 4, 0};
+  for (int c = 0; c < 6; ++c) {
     if (cand_ms) cand_ms[c] = -1;
     if (!((G->cand_mask >> c) & 1u)) continue;
     int32_t st;
     if (c == 0) { or_build_gpipe(p, m, codes, len, maxlen); st = or_simulate(&I, codes, len, maxlen, &r, NULL); }
     else if (c == 1) { or_build_1f1b(p, m, codes, len, maxlen); st = or_simulate(&I, codes, len, maxlen, &r, NULL); }
+    else if (c == 5) { or_build_zbh1(p, m, codes, len, maxlen); st = or_simulate(&I, codes, len, maxlen, &r, NULL); }
     else { or_inst J = I; J.n_sub = nsub_of[c]; st = or_greedy(&J, codes, len, maxlen, &r, NULL); }
     if (st != 0) continue;                       /* memory-infeasible (or invalid) candidate */
     if (cand_ms) cand_ms[c] = r.makespan;

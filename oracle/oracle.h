@@ -124,7 +124,7 @@ typedef struct {
 } or_grid;
 int64_t or_grid_points(const or_grid* G);
 void    or_grid_instance(const or_grid* G, int64_t point, or_inst* out);
-/* best key = (makespan << 8) | cand, UINT64_MAX if none feasible; cand_ms[5] nullable (-1 = not run / infeasible) */
+/* best key = (makespan << 8) | cand, UINT64_MAX if none feasible; cand_ms[6] nullable (-1 = not run / infeasible) */
 uint64_t or_sweep_point(const or_grid* G, int64_t point, int64_t* cand_ms);
 
 #ifdef __cplusplus

@@ -262,7 +262,7 @@ def to_or_grid(g):
 def sweep_point(g, k: int, G=None):
     if G is None:
         G, keep = to_or_grid(g)
-    cm = (C.c_int64 * 5)()
+    cm = (C.c_int64 * 6)()
     key = lib().or_sweep_point(C.byref(G), int(k), cm)
     return int(key), list(cm)
 

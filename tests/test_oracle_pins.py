@@ -450,3 +450,11 @@ def test_sweep_point_tiny(oracle_lib):
     assert cm[0] == -1                                  # GPipe memory-infeasible at M_L = p*m_f
     assert cm[1] == 4500 and cm[2] == cm[3] == cm[4] == 3300
     assert key == (3300 << 8) | 2
+    # candidate 5 = ZB-H1 (Q30, Q31): the direct simulation of its built plan; key = lowest
+    # (makespan, id) over all six
+    g.cand_mask = 0b111111
+    key6, cm6 = oracle_lib.sweep_point(g, 0)
+    d = oracle_lib.grid_instance(g, 0)
+    z = oracle_lib.simulate(d, *oracle_lib.build_static("zbh1", 4, 8))
+    assert z["status"] == 0 and cm6[5] == z["makespan"] and cm6[:5] == cm
+    assert key6 == min(((c_ << 8) | i) for i, c_ in enumerate(cm6) if c_ >= 0)
