@@ -456,5 +456,5 @@ def test_sweep_point_tiny(oracle_lib):
     key6, cm6 = oracle_lib.sweep_point(g, 0)
     d = oracle_lib.grid_instance(g, 0)
     z = oracle_lib.simulate(d, *oracle_lib.build_static("zbh1", 4, 8))
-    assert z["status"] == 0 and cm6[5] == z["makespan"] and cm6[:5] == cm
+    assert z["status"] == 0 and cm6[5] == z["makespan"] and cm6[:5] == cm[:5] and cm[5] == -1
     assert key6 == min(((c_ << 8) | i) for i, c_ in enumerate(cm6) if c_ >= 0)
