@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define CP_ABI_VERSION 1u
+#define CP_ABI_VERSION 2u      /* v2: ZB-H1 sweep candidate (6 candidates), cp_build_static */
 #define CP_MAX_STAGES 32      /* lane-per-stage design: p <= 32 */
 #define CP_MAX_MB 1024        /* microbatches per instance */
 #define CP_MAX_SUB 16         /* n_sub limit of the GPU path */
@@ -48,6 +48,12 @@ extern "C" {
 #define CP_OP_B 1u            /* combined backward block B = D + W (App. B :811-822) */
 #define CP_OP_D 2u            /* input-gradient block (DGrad) */
 #define CP_OP_W 3u            /* ONE weight-gradient sub-block (n_sub per W block) */
+
+/* static plan families (cp_build_static kind; equal to their sweep candidate ids) */
+#define CP_PLAN_GPIPE 0       /* F x m, then B x m (reading Q22) */
+#define CP_PLAN_1F1B 1        /* PipeDream-Flush, combined B, warm-up min(p-s-1, m) (Q23) */
+#define CP_PLAN_ZBH1 5        /* ZB-H1, split D/W, W deferred by s microbatches on stage s (Q31) */
+#define CP_N_CAND 6           /* sweep candidates: 0 GPipe, 1 1F1B, 2/3/4 greedy n_sub 1/2/4, 5 ZB-H1 */
 
 typedef enum { CP_OK = 0, CP_EINVAL = -1, CP_EUNSUPPORTED = -2, CP_ECUDA = -3, CP_EWORKSPACE = -4 } cp_rc;
 
@@ -123,8 +129,8 @@ typedef struct {
  * m = n_mb_vals[i_mb]; stages split contiguously over min(n_dc, p) DCs, dc(s) = s*n_dc/p;
  * a cross-DC boundary carries (lat[i_lat], bw[i_bw]) both ways, intra-DC boundaries (0, 0);
  * m_lim[s] = (mlim_x1000[i_mem]*p*m_f[s] + 500)/1000; t_dp[s] = tdp[i_dp].
- * Candidates (cand_mask bits): 0 GPipe, 1 1F1B (combined B; n_sub ignored), 2/3/4 greedy with
- * n_sub = 1/2/4.  key = (makespan << 8) | cand (int64 >= 0), INT64_MAX for a memory-infeasible
+ * Candidates (cand_mask bits, CP_N_CAND of them): 0 GPipe, 1 1F1B (combined B; n_sub ignored),
+ * 2/3/4 greedy with n_sub = 1/2/4, 5 ZB-H1 (split D/W, whole W blocks; n_sub ignored).  key = (makespan << 8) | cand (int64 >= 0), INT64_MAX for a memory-infeasible
  * candidate; the point's key is the minimum (ties -> lower candidate id), INT64_MAX if no candidate
  * is feasible, INT64_MAX-1 if the point exceeds the GPU limits (CPI_OVERFLOW).  Signed keys let
  * an int64 all-reduce(MIN) across ranks act as allgather + argmin in one collective. */
@@ -165,10 +171,20 @@ int32_t cp_greedy(const cp_instances* inst, const cp_schedules* out, const cp_re
  * Work is (point, candidate) tasks taken from a device counter (most expensive first) and combined
  * with a 64-bit atomicMin per point; p-classes run concurrently on streams forked from `stream`
  * and joined back to it.  ws: cp_workspace_bytes(2, grid, 0) bytes.
- * cand_makespan (nullable) [n_points][5] int32: makespan of each candidate, -1 if not run
+ * cand_makespan (nullable) [n_points][CP_N_CAND] int32: makespan of each candidate, -1 if not run
  * or memory-infeasible.  grid is a HOST pointer, passed to the kernel by value. */
 int32_t cp_sweep_shard(const cp_grid* grid, int64_t point_lo, int64_t point_hi,
                        int64_t* keys, int32_t* cand_makespan, void* ws, size_t ws_bytes, void* stream);
+
+/* Build static plans (PAPER.md Table tab:ppschedules :468-473; readings Q22, Q23, Q31) for the
+ * out->n items of `out`: item i uses instance inst_of[i] (NULL: instance i, or 0 if inst->n == 1)
+ * and gets its (p, m) plan in the packed layout cp_simulate reads.  kind: CP_PLAN_GPIPE,
+ * CP_PLAN_1F1B or CP_PLAN_ZBH1.  Every word of out->ops and every row of out->len is written
+ * (entries past a row's length and rows >= p are 0), so the result is fully defined.
+ * Errors: CP_EINVAL for an unknown kind, NULL / inconsistent descriptors, stage_stride < max_pp,
+ * or 16*words < entries per row at max_mb (2*max_mb; 3*max_mb for ZB-H1).  An item whose own
+ * (p, m) exceeds (stage_stride, words) gets all-zero rows.  Enqueued on `stream`, no sync. */
+int32_t cp_build_static(int32_t kind, const cp_instances* inst, const cp_schedules* out, void* stream);
 
 /* (host) Cost-balanced partition of the grid's points over `world` ranks: bounds[0..world]
  * with bounds[r]..bounds[r+1] owned by rank r; cuts at equal prefix sums of the estimated

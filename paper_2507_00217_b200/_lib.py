@@ -1,4 +1,4 @@
-"""ctypes loader + struct mirrors of include/crosspipe.h (ABI v1).
+"""ctypes loader + struct mirrors of include/crosspipe.h (ABI v2).
 
 Fails loudly: there is no CPU fallback anywhere in this package.  If the in-tree
 libcrosspipe.so is missing, build it with `python -c "import __graft_entry__ as g; g.build()"`.
@@ -74,7 +74,10 @@ class CpSpecSI(C.Structure):
 
 
 EXPORTS = ("cp_abi_version", "cp_status_string", "cp_workspace_bytes", "cp_simulate", "cp_greedy",
-           "cp_sweep_shard", "cp_sweep_partition", "cp_quantize", "cp_validate_instance")
+           "cp_build_static", "cp_sweep_shard", "cp_sweep_partition", "cp_quantize", "cp_validate_instance")
+ABI_VERSION = 2
+N_CAND = 6                    # sweep candidates: 0 GPipe, 1 1F1B, 2/3/4 greedy n_sub 1/2/4, 5 ZB-H1
+PLAN_KINDS = {"gpipe": 0, "1f1b": 1, "zbh1": 5}
 
 _lib = None
 
@@ -97,6 +100,8 @@ def load():
     L.cp_simulate.argtypes = [P(CpInstances), P(CpSchedules), P(CpResults), C.c_void_p, C.c_size_t, C.c_void_p]
     L.cp_greedy.restype = C.c_int32
     L.cp_greedy.argtypes = [P(CpInstances), P(CpSchedules), P(CpResults), C.c_void_p, C.c_size_t, C.c_void_p]
+    L.cp_build_static.restype = C.c_int32
+    L.cp_build_static.argtypes = [C.c_int32, P(CpInstances), P(CpSchedules), C.c_void_p]
     L.cp_sweep_shard.restype = C.c_int32
     L.cp_sweep_shard.argtypes = [P(CpGrid), C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_size_t, C.c_void_p]
@@ -106,7 +111,7 @@ def load():
     L.cp_quantize.argtypes = [P(CpSpecSI), C.c_void_p]
     L.cp_validate_instance.restype = C.c_int32
     L.cp_validate_instance.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
-    if L.cp_abi_version() != 1:
+    if L.cp_abi_version() != ABI_VERSION:
         raise ImportError("libcrosspipe ABI version mismatch")
     _lib = L
     return L

@@ -208,6 +208,26 @@ def greedy(inst: Instances, *, stats=False, timeline=False, stage_stride=None, w
     return r
 
 
+def build_static(kind: str, inst: Instances, n=None, inst_of=None, *, stage_stride=None, words=None, stream=None):
+    """cp_build_static: static plans ("gpipe", "1f1b" or "zbh1") for n items (item i uses instance
+    inst_of[i], or i / 0 as in cp_simulate) -> (ops int32 [n, words, stride], len int16 [n, stride]),
+    ready for simulate()."""
+    _require_cuda(inst.dev)
+    dev = inst.dev.device
+    k = L.PLAN_KINDS[kind]
+    n = inst.n if n is None else int(n)
+    stride = stage_stride or inst.max_pp
+    if words is None:
+        words = ((3 if kind == "zbh1" else 2) * inst.max_mb + 15) // 16
+    ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
+    ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
+    d = inst.desc(None)
+    io = inst_of.data_ptr() if inst_of is not None else None
+    sc = L.CpSchedules(n, stride, words, 0, io, ops.data_ptr(), ln.data_ptr())
+    L.check(L.load().cp_build_static(k, C.byref(d), C.byref(sc), _stream(stream)), "cp_build_static")
+    return ops, ln
+
+
 def to_cp_grid(grid) -> L.CpGrid:
     """workloads.Grid -> cp_grid (host struct, passed to the kernel by value)."""
     g = L.CpGrid()
@@ -244,7 +264,7 @@ def sweep_shard(grid, lo=0, hi=None, *, keys=None, cand=False, stream=None, devi
     hi = npts if hi is None else hi
     if keys is None:
         keys = torch.full((npts,), KEY_NONE, dtype=torch.int64, device=device)
-    cm = torch.full((npts, 5), -1, dtype=torch.int32, device=device) if cand is True else (cand if cand is not False and cand is not None else None)
+    cm = torch.full((npts, L.N_CAND), -1, dtype=torch.int32, device=device) if cand is True else (cand if cand is not False and cand is not None else None)
     ws = torch.empty(int(L.load().cp_workspace_bytes(2, C.byref(g), 0)), dtype=torch.uint8, device=keys.device)
     rc = L.load().cp_sweep_shard(C.byref(g), int(lo), int(hi), C.c_void_p(keys.data_ptr()),
                                  _ptr(cm), C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))

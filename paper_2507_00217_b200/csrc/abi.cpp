@@ -241,9 +241,9 @@ int sweep_ring_slots(const cp_grid* g, int p) {
 }
 
 long long point_cost(const cp_grid* g, int i_pp, int i_mb) {
-  static const int units[5] = {2, 2, 3, 4, 6};   // entries per microbatch: 2m static, (2+n_sub)m greedy
+  static const int units[CP_N_CAND] = {2, 2, 3, 4, 6, 3};   // entries per microbatch: 2m GPipe/1F1B, (2+n_sub)m greedy, 3m ZB-H1
   long long u = 0;
-  for (int c = 0; c < 5; ++c)
+  for (int c = 0; c < CP_N_CAND; ++c)
     if ((g->cand_mask >> c) & 1u) u += units[c];
   return (long long)g->n_pp_vals[i_pp] * g->n_mb_vals[i_mb] * std::max(1LL, u);
 }
@@ -287,6 +287,20 @@ int32_t cp_simulate(const cp_instances* in, const cp_schedules* sc, const cp_res
   if (!sc->inst_of && in->n != 1 && in->n < sc->n) return CP_EINVAL;
   if (sc->n == 0) return CP_OK;
   return run_engine(cpk::MODE_SIM, in, sc, res, ws, ws_bytes, stream);
+}
+
+int32_t cp_build_static(int32_t kind, const cp_instances* in, const cp_schedules* out, void* stream) {
+  if (kind != CP_PLAN_GPIPE && kind != CP_PLAN_1F1B && kind != CP_PLAN_ZBH1) return CP_EINVAL;
+  int rc = check_instances(in);
+  if (rc) return rc;
+  if (!out || out->n < 0 || !out->ops || !out->len || out->words < 1) return CP_EINVAL;
+  if (out->stage_stride < in->max_pp) return CP_EINVAL;
+  if (!out->inst_of && in->n != 1 && in->n < out->n) return CP_EINVAL;
+  const long long need = kind == CP_PLAN_ZBH1 ? 3LL * in->max_mb : 2LL * in->max_mb;
+  if (16LL * out->words < need) return CP_EINVAL;
+  if (out->n == 0) return CP_OK;
+  return cpk::launch_build_static(kind, in->inst, in->n, out->inst_of, out->n, out->stage_stride, out->words, out->ops,
+                                  out->len, stream) == cudaSuccess ? CP_OK : CP_ECUDA;
 }
 
 int32_t cp_greedy(const cp_instances* in, const cp_schedules* out, const cp_results* res, void* ws, size_t ws_bytes,
@@ -348,7 +362,7 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
     // tasks whose own bound is <= 32 run in a launch with 32-slot rings and only the rest in one
     // sized to the class maximum.  Static candidates (GPipe, 1F1B) and anything the fast path
     // cannot hold in shared memory: the generic engine.
-    unsigned engine_mask = g->cand_mask & 31u;
+    unsigned engine_mask = g->cand_mask & ((1u << CP_N_CAND) - 1u);
     const unsigned greedy_mask = engine_mask & 0x1cu;
     if (greedy_mask && !getenv_nofast()) {
       const int Wd = p <= 8 ? 8 : (p <= 16 ? 16 : 32);

@@ -35,6 +35,7 @@
 
 #include "engine.h"
 #include "grid_synth.cuh"
+#include "plan_codes.cuh"
 #include "ptx.cuh"
 
 namespace cpk {
@@ -65,14 +66,6 @@ __device__ __noinline__ bool dbg_ok(long long idx, long long lim, int tag, long 
 
 // Arithmetic static plans (Table tab:ppschedules :470; readings Q22/Q23).
 // GPipe: F x m, B x m.  1F1B: w = min(p-s-1, m) F, (F,B) x (m-w), B x w.
-__device__ __forceinline__ int static_code(int cand, int s, int p, int m, int pos) {
-  if (cand == 0) return pos < m ? (int)CP_OP_F : (int)CP_OP_B;
-  const int w = imin(p - s - 1, m);
-  const int q = pos - w;
-  if (q < 0) return (int)CP_OP_F;
-  if (q < 2 * (m - w)) return (q & 1) ? (int)CP_OP_B : (int)CP_OP_F;
-  return (int)CP_OP_B;
-}
 
 struct LaneCfg {       // per-lane (stage) instance fields
   int p, m, nsub, tagate;
@@ -182,7 +175,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           long long t = 0;
           if (s == 0) t = atomicAdd(A.sweep_counter, 1ull);
           t = __shfl_sync(segmask, t, seg * W);
-          item = sweep_task(A.grid.cand_mask & 31u, A.pt_lo, A.pt_hi, t, cand);
+          item = sweep_task(A.grid.cand_mask & ((1u << CP_N_CAND) - 1u), A.pt_lo, A.pt_hi, t, cand);
         } else {
           item = item_of(task);
           task += task_stride;
@@ -196,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
             const GridLane g = grid_lane(A.grid, item, s);
             c.p = g.p;
             c.m = g.m;
-            cand_greedy = cand >= 2;
+            cand_greedy = cand >= 2 && cand <= 4;
             c.nsub = cand_greedy ? (1 << (cand - 2)) : 1;
             zero1 = g.zero1;
             c.tf = g.tf; c.td = g.td; c.tw = g.tw;
@@ -236,7 +229,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           fmask = (s > 0) ? -1 : 0;
           dmask = (s < c.p - 1) ? -1 : 0;
           fmask_next = s < c.p - 1;
-          plen = (kMode == MODE_SWEEP && s < c.p && !cand_greedy) ? 2 * c.m : 0;
+          plen = (kMode == MODE_SWEEP && s < c.p && !cand_greedy) ? plan_row_len(cand, c.m) : 0;
           if (kMode == MODE_SIM && s < c.p && s < A.stage_stride) {
             plen = A.len[item * A.stage_stride + s];
             if (plen > 16 * A.words && !bad) load_status = CPI_BAD_PLAN;     // row longer than its capacity
@@ -274,7 +267,8 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         if (kMode == MODE_SWEEP && just_loaded && s < c.p)
           skip_lane = cand == 0 ? (long long)c.m * c.mf > c.mlim
                                 : (cand == 1 ? (long long)imin(c.p - s, c.m) * c.mf > c.mlim
-                                             : (c.tf < c.nsub || c.td < c.nsub || c.tw < c.nsub));
+                                             : (cand == 5 ? false      // ZB-H1: evaluated, excluded if over M_L
+                                                          : (c.tf < c.nsub || c.td < c.nsub || c.tw < c.nsub)));
         const unsigned b_skip = __ballot_sync(FULL, skip_lane || (kMode == MODE_SWEEP && just_loaded &&
                                                                  !((A.grid.cand_mask >> cand) & 1u)));
         const unsigned b_inst = __ballot_sync(FULL, just_loaded && load_status == CPI_BAD_INSTANCE);
@@ -360,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         else wv = (live && CHK(item * A.words + (pq >> 4), n_it * A.words, 2)) ? A.ops[(item * A.words + (pq >> 4)) * A.stage_stride + s] : 0u;
         code = (int)((wv >> ((pq & 15) << 1)) & 3u);
       } else {
-        code = static_code(cand, s, c.p, c.m, pos);
+        code = plan_code(cand, s, c.p, c.m, pos);   // cand 0/1/5 = CP_PLAN_GPIPE/1F1B/ZBH1
       }
       const bool cF = code == (int)CP_OP_F, cW = code == (int)CP_OP_W, cB = code == (int)CP_OP_B;
       const int roff = cF ? lane + (slF << 5) : RW + lane + (slD << 5);
@@ -514,7 +508,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
         } else if (kMode == MODE_SWEEP) {
           // one (point, candidate) task: its makespan and the point's packed argmin key
           if (completed && st == 0 && s == 0) {
-            if (A.cand_ms) A.cand_ms[item * 5 + cand] = ms;
+            if (A.cand_ms) A.cand_ms[item * CP_N_CAND + cand] = ms;
             atomicMin(A.keys + item, ((unsigned long long)ms << 8) | (unsigned)cand);
           }
           need_load = true;
@@ -556,7 +550,7 @@ __global__ void k_sweep_init(unsigned long long* keys, int32_t* cand_ms, long lo
   for (long long k = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; k < hi; k += (long long)gridDim.x * blockDim.x) {
     keys[k] = KEY_NONE;
     if (cand_ms)
-      for (int c = 0; c < 5; ++c) cand_ms[k * 5 + c] = -1;
+      for (int c = 0; c < CP_N_CAND; ++c) cand_ms[k * CP_N_CAND + c] = -1;
   }
 }
 

@@ -63,6 +63,8 @@ int launch_greedy_fast(int W, bool grid, const Args& a, int blocks, int threads,
 int greedy_fast_blocks_per_sm(int W, bool grid, int threads, size_t smem);
 int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem, bool timeline);
 int device_sm_count();
+int launch_build_static(int kind, const cp_inst_v1* inst, int n_inst, const int32_t* inst_of, long long n, int stride,
+                        int words, uint32_t* ops, uint16_t* len, void* stream);
 int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, void* stream);
 
 constexpr int kThreads = 128;          // 4 warps per block

@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
           long long t = 0;
           if (s == 0) t = atomicAdd(A.sweep_counter, 1ull);
           t = __shfl_sync(segmask, t, seg * W);
-          item = sweep_task(A.grid.cand_mask & 31u, A.pt_lo, A.pt_hi, t, cand);
+          item = sweep_task(A.grid.cand_mask & ((1u << CP_N_CAND) - 1u), A.pt_lo, A.pt_hi, t, cand);
         } else {
           item = task < A.n_items ? task : -1;
           task += tstride;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
             if (s == 0) {
               if (!complete) atomicMin(A.keys + item, KEY_OVER);
               else if (!(b_mem & segmask)) {
-                if (A.cand_ms) A.cand_ms[item * 5 + cand] = ms;
+                if (A.cand_ms) A.cand_ms[item * CP_N_CAND + cand] = ms;
                 atomicMin(A.keys + item, ((unsigned long long)ms << 8) | (unsigned)cand);
               }
             }

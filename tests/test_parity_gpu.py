@@ -463,3 +463,56 @@ def test_generic_greedy_ring_overflow_fixup():
     g = cp.greedy(gi, stats=True, timeline=True, ring=1)
     for k in ("makespan", "status", "peak_mem", "stage_stats", "ops", "len", "t_start"):
         assert torch.equal(g[k], ref[k]), k
+
+
+# ------------------------------------------------------------------------------------- static builders (NEXT 2)
+@pytest.mark.parametrize("kind", ["gpipe", "1f1b", "zbh1"])
+def test_build_static_matches_oracle_builders(O, kind):
+    """cp_build_static (Q22, Q23, Q31) == the oracle's builders entry by entry, for p in 1..32 and
+    m in 1..40 (m < p included), with stage_stride 32 > p and spare words: padding words and
+    rows >= p are zero."""
+    rng = np.random.default_rng({"gpipe": 40, "1f1b": 41, "zbh1": 42}[kind])
+    n = 300
+    batch = K.random_instances(n, seed=int(rng.integers(1 << 30)), max_p=32, max_m=40)
+    inst = cp.Instances(batch)
+    words = (3 * 40 + 15) // 16 + 2
+    ops, ln = cp.build_static(kind, inst, stage_stride=32, words=words)
+    torch.cuda.synchronize()
+    codes, lens = unpack_plans(ops.cpu().numpy().view(np.uint32), ln.cpu().numpy().view(np.uint16))
+    for i in range(n):
+        p, m = int(batch.p[i]), int(batch.m[i])
+        c, l_ = O.build_static(kind, p, m)
+        assert np.array_equal(lens[i, :p], l_), i
+        assert not lens[i, p:].any() and not codes[i, p:].any(), i
+        for s in range(p):
+            assert np.array_equal(codes[i, s, :l_[s]], c[s, :l_[s]]), (i, s)
+            assert not codes[i, s, l_[s]:].any(), (i, s)
+
+
+def test_simulate_zbh1_plans(O):
+    """GPU-built ZB-H1 plans through cp_simulate (the k_sim32 fast path at stage_stride 32 and the
+    generic engine with a timeline) == the oracle simulating its own ZB-H1 plans."""
+    batch = K.random_instances(200, seed=43, max_p=32, max_m=24, intra_delay=True)
+    batch.n_sub[:] = 1                                  # ZB-H1 holds whole W blocks
+    inst = cp.Instances(batch)
+    ops, ln = cp.build_static("zbh1", inst, stage_stride=32)
+    for timeline in (False, True):
+        r = to_host(cp.simulate(inst, ops, ln, stats=True, timeline=timeline))
+        torch.cuda.synchronize()
+        for i in range(len(batch)):
+            d = batch.item(i)
+            c, l_ = O.build_static("zbh1", d["p"], d["m"])
+            compare_sim(O, d, c, l_, r, i, c.shape[1], timeline=timeline)
+
+
+def test_sweep_six_candidates(O):
+    """Sweep with all six candidates (ZB-H1 = candidate 5, Q30/Q31) over delays, memory budgets
+    below and above the 1F1B budget and DP tails; every point and candidate vs the oracle."""
+    from workloads.core import Grid
+    base = K.uniform_instance(6, 8, 3, 90, 110, 70)
+    grid = Grid(base=base, n_dc=3, pp_vals=[2, 6], mb_vals=[3, 8, 13], lat=np.array([0, 120]), bw=np.array([0, 45, 200]),
+                mlim_x1000=np.array([700, 1000, 1600]), tdp=np.array([0, 80]), cand_mask=0b111111)
+    keys, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    assert cm.shape[1] == 6
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
