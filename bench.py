@@ -317,7 +317,8 @@ def run_ours(args):
     sweeps = None
     if not args.no_sweep:
         sweeps = {}
-        for name, grid, ncand in (("config2", K.gpt16_grid(), 3), ("config5", K.full_sweep_grid(), 5)):
+        for name, grid, ncand in (("config2", K.gpt16_grid(), 3), ("config5", K.full_sweep_grid(), 5),
+                                  ("e1_delay_sensitivity", K.e1_grid(), 6)):
             cg = cp.to_cp_grid(grid)
             bounds = cp.sweep_partition(grid, ws, cgrid=cg)
             for _ in range(2):

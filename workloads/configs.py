@@ -55,6 +55,20 @@ def tiny_grid(f=100) -> InstanceBatch:
     return InstanceBatch.concat([tiny(a, b, f) for a in r for b in r])
 
 
+def e1_grid(f=T_F, steps=33, top=4.0) -> Grid:
+    """E1, the delay-sensitivity study of PAPER.md §5.1 (Fig. pre_delay_sensitivity, :474-499):
+    4 stages over 2 DCs (2 stages each), 8 microbatches, uniform F = D = W = T_F, memory budget
+    of 1F1B ("dynamic schedules ... with the same memory limits as their static counterparts
+    (e.g., CrossUD mirrors 1F1B)"), T_lat/T_F and T_bw/T_F each on `steps` values in [0, top];
+    all six sweep candidates (GPipe, 1F1B, greedy n_sub 1/2/4, ZB-H1)."""
+    base = uniform_instance(4, 8, 2, f, f, f)
+    r = np.linspace(0.0, top, steps)
+    ticks = np.floor(r * f + 0.5).astype(np.int64)
+    return Grid(base=base, n_dc=2, pp_vals=[4], mb_vals=[8], lat=ticks, bw=ticks.copy(),
+                mlim_x1000=np.array([1000], np.int64), tdp=np.array([0], np.int64), cand_mask=0b111111,
+                name="e1_delay_sensitivity")
+
+
 # ---------------------------------------------------------------------------------------
 # config 2 -- GPT-style 16 stages over 2 DCs, 32 microbatches, 64 latencies x 64 bandwidths
 def gpt16_grid() -> Grid:

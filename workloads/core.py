@@ -105,7 +105,7 @@ class Grid:
     bw: np.ndarray                       # cross-DC window ticks (beta * msg)
     mlim_x1000: np.ndarray               # m_lim[s] = (x * p * m_f[s] + 500) // 1000
     tdp: np.ndarray                      # DP allreduce ticks
-    cand_mask: int = 0b11111             # bit0 GPipe, bit1 1F1B, bit2..4 greedy n_sub = 1,2,4
+    cand_mask: int = 0b11111             # bit0 GPipe, bit1 1F1B, bit2..4 greedy n_sub = 1,2,4, bit5 ZB-H1
     name: str = ""
     extra: dict = field(default_factory=dict)
 
