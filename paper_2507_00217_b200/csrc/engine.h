@@ -68,6 +68,11 @@ int launch_build_static(int kind, const cp_inst_v1* inst, int n_inst, const int3
 int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, void* stream);
 
 constexpr int kThreads = 128;          // 4 warps per block
+// fast-path kernels launch 2-warp blocks; their residency is set by shared memory (about 9 such
+// blocks per SM), so the launch bound lets ptxas spend up to 113 registers instead of
+// rematerializing addresses and flags inside the round (measured: greedy round 169 -> 154 SASS)
+constexpr int kFastThreads = 64;
+constexpr int kFastMinBlocks = 9;
 constexpr int kFixWarps = 148 * 4;     // warps of a global-ring (fix-up) launch
 constexpr int kGreedyTableWords = 768;   // k_greedy_fast per-warp parameter table: [6 entries][32 lanes] int4
 constexpr int kSim32TableWords = 1024;  // k_sim32 per-warp parameter tables: 2 x [4 codes][32 lanes] int4

@@ -35,8 +35,21 @@ __device__ __forceinline__ int gmadd(int g, int d, int x) {
 // kGrid = true : cp_sweep_shard's greedy candidates -- (point, candidate) tasks from a device
 //                counter, instances synthesized from the grid (grid_synth.cuh), no plan output;
 //                the candidate's makespan and the point's packed argmin key out.
+// Output rows r = s, s + W, ... < stage_stride of an item: len, every plan word past the emitted
+// entries zeroed (outputs are fully defined, whatever the caller's buffer held) and, for rows no
+// lane owns, zero stats.  The row's own partial last word is written by the caller.
+__device__ __noinline__ void greedy_finish_rows(const Args& A, long long it, int s, int W, int used, bool stats_own) {
+  for (int r = s; r < A.stage_stride; r += W) {
+    const int u = r == s ? used : 0;
+    const long long rb = it * A.stage_stride + r;
+    for (int k = (u + 15) >> 4; k < A.words; ++k) A.ops[(it * A.words + k) * A.stage_stride + r] = 0u;
+    A.len[rb] = (uint16_t)u;
+    if (A.stage_stats && (r != s || stats_own)) *reinterpret_cast<int4*>(A.stage_stats + rb * 4) = make_int4(0, 0, 0, 0);
+  }
+}
+
 template <int W, bool kGrid>
-__global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant__ Args A) {
+__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(const __grid_constant__ Args A) {
   extern __shared__ __align__(128) int32_t smem[];
   constexpr int NSEG = 32 / W;
   const int lane = threadIdx.x & 31;
@@ -68,18 +81,9 @@ __global__ void __launch_bounds__(kThreads) k_greedy_fast(const __grid_constant_
   int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0;
   int linkF = 0, linkB = 0, pos = 0, last_fd = 0;
   uint32_t emitw = 0;
-  // Output rows r = s, s + W, ... < stage_stride of an item: len, every plan word past the emitted
-  // entries zeroed (outputs are fully defined, whatever the caller's buffer held) and, for rows no
-  // lane owns, zero stats.  The row's own partial last word is written by the caller.
+  // (out of line: inlined, this rare-path code changed the round's register allocation)
   auto finish_rows = [&](long long it, int used, bool stats_own) {
-    if (kGrid) return;
-    for (int r = s; r < A.stage_stride; r += W) {
-      const int u = r == s ? used : 0;
-      const long long rb = it * A.stage_stride + r;
-      for (int k = (u + 15) >> 4; k < A.words; ++k) A.ops[(it * A.words + k) * A.stage_stride + r] = 0u;
-      A.len[rb] = (uint16_t)u;
-      if (A.stage_stats && (r != s || stats_own)) *reinterpret_cast<int4*>(A.stage_stats + rb * 4) = make_int4(0, 0, 0, 0);
-    }
+    if (!kGrid) greedy_finish_rows(A, it, s, W, used, stats_own);
   };
   long long item = -1;
   int cand = 0;                                        // sweep: candidate id (2/3/4 = greedy n_sub 1/2/4)

@@ -16,6 +16,12 @@
 #include "engine.h"
 #include "ptx.cuh"
 
+#ifdef SIM32_MINB
+#define SIM32_LB kFastThreads, SIM32_MINB
+#else
+#define SIM32_LB kThreads
+#endif
+
 namespace cpk {
 
 namespace {
@@ -32,7 +38,7 @@ __device__ __forceinline__ int madd(int g, int d, int x) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads) k_sim32(const __grid_constant__ Args A) {
+__global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args A) {
   extern __shared__ __align__(128) int32_t smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
