@@ -319,16 +319,16 @@ def run_ours(args):
         sweeps = {}
         for name, grid, ncand in (("config2", K.gpt16_grid(), 3), ("config5", K.full_sweep_grid(), 5),
                                   ("e1_delay_sensitivity", K.e1_grid(), 6)):
-            cg = cp.to_cp_grid(grid)
-            bounds = cp.sweep_partition(grid, ws, cgrid=cg)
+            # blocked ownership (cp_sweep_shard_rank): every rank evaluates its slice of every (p, m)
+            # block, then one all_reduce(MIN) of the keys inside the timed region
             for _ in range(2):
-                keys, _ = cpd.sweep(grid, bounds=bounds)
+                keys, _ = cpd.sweep(grid)
             sw_steps = 3
             barrier(ws)
             b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             b0.record(stream)
             for _ in range(sw_steps):
-                keys, _ = cpd.sweep(grid, bounds=bounds)
+                keys, _ = cpd.sweep(grid)
             b1.record(stream)
             torch.cuda.synchronize()
             sms = max_over_ranks(b0.elapsed_time(b1) / sw_steps, ws)

@@ -186,6 +186,15 @@ int32_t cp_sweep_shard(const cp_grid* grid, int64_t point_lo, int64_t point_hi,
  * (p, m) exceeds (stage_stride, words) gets all-zero rows.  Enqueued on `stream`, no sync. */
 int32_t cp_build_static(int32_t kind, const cp_instances* inst, const cp_schedules* out, void* stream);
 
+/* Evaluate the points owned by `rank` of `world` under blocked ownership: every (n_pp, n_mb) block
+ * of inner = n_lat*n_bw*n_mem*n_dp consecutive points is cut into `world` contiguous slices,
+ * slice r = [inner*r/world, inner*(r+1)/world), and rank r owns slice r of every block.  Every
+ * rank so gets the same mix of (p, m) work and all p-classes run concurrently on each GPU (the
+ * contiguous ranges of cp_sweep_partition hold few classes per rank).  Initializes and writes
+ * keys / cand_makespan of the owned points only; same ws and semantics as cp_sweep_shard. */
+int32_t cp_sweep_shard_rank(const cp_grid* grid, int32_t rank, int32_t world, int64_t* keys,
+                            int32_t* cand_makespan, void* ws, size_t ws_bytes, void* stream);
+
 /* (host) Cost-balanced partition of the grid's points over `world` ranks: bounds[0..world]
  * with bounds[r]..bounds[r+1] owned by rank r; cuts at equal prefix sums of the estimated
  * cost p*m*sum_{cand}(2 + n_sub(cand)). */

@@ -74,7 +74,8 @@ class CpSpecSI(C.Structure):
 
 
 EXPORTS = ("cp_abi_version", "cp_status_string", "cp_workspace_bytes", "cp_simulate", "cp_greedy",
-           "cp_build_static", "cp_sweep_shard", "cp_sweep_partition", "cp_quantize", "cp_validate_instance")
+           "cp_build_static", "cp_sweep_shard", "cp_sweep_shard_rank", "cp_sweep_partition", "cp_quantize",
+           "cp_validate_instance")
 ABI_VERSION = 2
 N_CAND = 6                    # sweep candidates: 0 GPipe, 1 1F1B, 2/3/4 greedy n_sub 1/2/4, 5 ZB-H1
 PLAN_KINDS = {"gpipe": 0, "1f1b": 1, "zbh1": 5}
@@ -105,6 +106,9 @@ def load():
     L.cp_sweep_shard.restype = C.c_int32
     L.cp_sweep_shard.argtypes = [P(CpGrid), C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_size_t, C.c_void_p]
+    L.cp_sweep_shard_rank.restype = C.c_int32
+    L.cp_sweep_shard_rank.argtypes = [P(CpGrid), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_size_t, C.c_void_p]
     L.cp_sweep_partition.restype = C.c_int32
     L.cp_sweep_partition.argtypes = [P(CpGrid), C.c_int32, P(C.c_int64)]
     L.cp_quantize.restype = C.c_int32

@@ -272,6 +272,23 @@ def sweep_shard(grid, lo=0, hi=None, *, keys=None, cand=False, stream=None, devi
     return keys, cm
 
 
+def sweep_shard_rank(grid, rank: int, world: int, *, keys=None, cand=False, stream=None, device="cuda", cgrid=None):
+    """cp_sweep_shard_rank: the points rank `rank` of `world` owns under blocked ownership (slice
+    `rank` of every (p, m) block).  Returns (keys int64 [n_points], cand_ms or None); keys of
+    points not owned are INT64_MAX when `keys` is allocated here."""
+    _require_cuda()
+    g = cgrid if cgrid is not None else to_cp_grid(grid)
+    npts = grid.n_points
+    if keys is None:
+        keys = torch.full((npts,), KEY_NONE, dtype=torch.int64, device=device)
+    cm = torch.full((npts, L.N_CAND), -1, dtype=torch.int32, device=device) if cand is True else (cand if cand is not False and cand is not None else None)
+    ws = torch.empty(int(L.load().cp_workspace_bytes(2, C.byref(g), 0)), dtype=torch.uint8, device=keys.device)
+    rc = L.load().cp_sweep_shard_rank(C.byref(g), int(rank), int(world), C.c_void_p(keys.data_ptr()), _ptr(cm),
+                                      C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
+    L.check(rc, "cp_sweep_shard_rank")
+    return keys, cm
+
+
 def sweep_partition(grid, world: int, cgrid=None):
     g = cgrid if cgrid is not None else to_cp_grid(grid)
     b = (C.c_int64 * (world + 1))()

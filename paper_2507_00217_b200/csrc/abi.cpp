@@ -313,47 +313,86 @@ int32_t cp_greedy(const cp_instances* in, const cp_schedules* out, const cp_resu
   return run_engine(cpk::MODE_GREEDY, in, out, res, ws, ws_bytes, stream);
 }
 
-int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, int32_t* cand_ms, void* ws,
-                       size_t ws_bytes, void* stream) {
-  int rc = check_grid(g);
-  if (rc) return rc;
+// Evaluate a point set: contiguous points [lo, hi) (own_hi == own_lo), or the blocked ownership of
+// cp_sweep_shard_rank: slice [own_lo, own_hi) of every (n_pp, n_mb) block of `inner` points.
+// Streams forked from `parent` on demand (one per launch) and joined back to it in join(); each
+// stream is released by the runtime once its queued work completes.
+struct Forker {
+  cudaStream_t parent;
+  cudaEvent_t fork = nullptr;
+  cudaStream_t sub[40] = {};
+  int n = 0;
+  explicit Forker(cudaStream_t p) : parent(p) {}
+  bool used_parent = false;
+  // the first launch runs on the parent itself (a single-launch call creates no stream); the fork
+  // point is recorded before it, so later launches do not wait for it
+  cudaStream_t next() {
+    if (!fork) {
+      if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return parent;
+      cudaEventRecord(fork, parent);
+    }
+    if (!used_parent) { used_parent = true; return parent; }
+    if (n == 40) return parent;
+    if (cudaStreamCreateWithFlags(&sub[n], cudaStreamNonBlocking) != cudaSuccess) return parent;
+    cudaStreamWaitEvent(sub[n], fork, 0);
+    return sub[n++];
+  }
+  void join() {
+    for (int i = 0; i < n; ++i) {
+      cudaEvent_t j;
+      if (cudaEventCreateWithFlags(&j, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(j, sub[i]);
+        cudaStreamWaitEvent(parent, j, 0);
+        cudaEventDestroy(j);
+      }
+      cudaStreamDestroy(sub[i]);
+    }
+    if (fork) cudaEventDestroy(fork);
+    n = 0;
+    fork = nullptr;
+    used_parent = false;
+  }
+};
+
+static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_lo, int own_hi, int64_t* keys,
+                         int32_t* cand_ms, void* ws, void* stream) {
+  int rc = CP_OK;
   const long long np = grid_points(g);
-  if (!keys || lo < 0 || hi < lo || hi > np) return CP_EINVAL;
-  if (!ws || ws_bytes < kCtrlBytes) return CP_EWORKSPACE;
-  if (lo == hi) return CP_OK;
+  const bool blocked = own_hi > own_lo;
+  const long long inner = (long long)g->n_lat * g->n_bw * g->n_mem * g->n_dp;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   unsigned long long* ukeys = reinterpret_cast<unsigned long long*>(keys);
   unsigned long long* counters = static_cast<unsigned long long*>(ws);   // four task counters per p-class (kCtrlBytes = 32 counters)
-  if (cpk::launch_sweep_init(ukeys, cand_ms, lo, hi, stream) != cudaSuccess) return CP_ECUDA;
+  if (cpk::launch_sweep_init(ukeys, cand_ms, blocked ? 0 : lo, blocked ? (long long)g->n_pp_n * g->n_mb_n : hi, inner,
+                             own_lo, own_hi, stream) != cudaSuccess)
+    return CP_ECUDA;
   if (cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 32, st) != cudaSuccess) return CP_ECUDA;
   // p is the slowest axis: one contiguous block of points per p-class; each class gets its own
   // segment width W and ring size, and the classes run concurrently on forked streams
   const long long per_pp = np / g->n_pp_n;
   int cls[8], ncls = 0;
-  for (int ip = 0; ip < g->n_pp_n; ++ip)
-    if (std::max<long long>(lo, ip * per_pp) < std::min<long long>(hi, (ip + 1) * per_pp)) cls[ncls++] = ip;
-  cudaEvent_t fork = nullptr;
-  cudaStream_t sub[8] = {};
-  cudaEvent_t join[8] = {};
-  const bool forked = ncls > 1;
-  if (forked) {
-    if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return CP_ECUDA;
-    cudaEventRecord(fork, st);
-  }
+  // largest p first: its launches hold the longest tasks (a launch ends on its longest task), so
+  // they are enqueued first and take the SMs before the cheaper classes fill them
+  for (int ip = g->n_pp_n - 1; ip >= 0; --ip)
+    if (blocked || std::max<long long>(lo, ip * per_pp) < std::min<long long>(hi, (ip + 1) * per_pp)) cls[ncls++] = ip;
+  // every launch (greedy tier or static-candidate engine pass) gets its own stream forked from, and
+  // joined back to, the caller's: a launch ends on its longest task, so launches that queue behind
+  // each other would add those tails up
+  Forker fk(st);
   for (int c = 0; c < ncls; ++c) {
     const int ip = cls[c];
-    const long long a0 = std::max<long long>(lo, ip * per_pp), a1 = std::min<long long>(hi, (ip + 1) * per_pp);
-    cudaStream_t cs = st;
-    if (forked) {
-      cudaStreamCreateWithFlags(&sub[c], cudaStreamNonBlocking);
-      cudaStreamWaitEvent(sub[c], fork, 0);
-      cs = sub[c];
-    }
+    // this class's point set: its points within [lo, hi), or its blocks with the owned slice
+    const long long a0 = blocked ? (long long)ip * g->n_mb_n : std::max<long long>(lo, ip * per_pp);
+    const long long a1 = blocked ? (long long)(ip + 1) * g->n_mb_n : std::min<long long>(hi, (ip + 1) * per_pp);
+    const long long npts = blocked ? (a1 - a0) * (long long)(own_hi - own_lo) : a1 - a0;
     cpk::Args a;
     std::memset(&a, 0, sizeof(a));
     a.grid = *g;
     a.pt_lo = a0;
     a.pt_hi = a1;
+    a.blk_inner = inner;
+    a.own_lo = own_lo;
+    a.own_hi = own_hi;
     a.keys = ukeys;
     a.cand_ms = cand_ms;
     const int p = g->n_pp_vals[ip];
@@ -386,9 +425,9 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
         const size_t smem = per_warp * wpb;
         const int bps = cpk::greedy_fast_blocks_per_sm(Wd, true, threads, smem);
         const long long segs = (long long)(32 / Wd) * wpb;
-        const long long need = ((a1 - a0) * __builtin_popcount(greedy_mask) + segs - 1) / segs;
+        const long long need = (npts * __builtin_popcount(greedy_mask) + segs - 1) / segs;
         const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
-        if (cpk::launch_greedy_fast(Wd, true, ag, blocks, threads, smem, cs) != cudaSuccess) rc = CP_ECUDA;
+        if (cpk::launch_greedy_fast(Wd, true, ag, blocks, threads, smem, fk.next()) != cudaSuccess) rc = CP_ECUDA;
       }
       if (ok) engine_mask &= ~greedy_mask;
     }
@@ -397,24 +436,36 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
       a.sweep_counter = counters + 4 * c;
       a.seg_lg = lg2_ceil(p);
       a.ring_slots = sweep_ring_slots(g, p);
-      rc = launch_pass(cpk::MODE_SWEEP, false, a, (a1 - a0) * __builtin_popcount(engine_mask), 32 >> a.seg_lg, cs);
-    }
-    if (forked) {
-      cudaEventCreateWithFlags(&join[c], cudaEventDisableTiming);
-      cudaEventRecord(join[c], cs);
-      cudaStreamWaitEvent(st, join[c], 0);
+      rc = launch_pass(cpk::MODE_SWEEP, false, a, npts * __builtin_popcount(engine_mask), 32 >> a.seg_lg, fk.next());
     }
     if (rc) break;
   }
-  if (forked) {
-    cudaEventDestroy(fork);
-    for (int c = 0; c < ncls; ++c) {
-      if (join[c]) cudaEventDestroy(join[c]);
-      if (sub[c]) cudaStreamDestroy(sub[c]);     // released once its queued work completes
-    }
-  }
+  fk.join();
   if (rc) return rc;
   return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
+}
+
+int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, int32_t* cand_ms, void* ws,
+                       size_t ws_bytes, void* stream) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  const long long np = grid_points(g);
+  if (!keys || lo < 0 || hi < lo || hi > np) return CP_EINVAL;
+  if (!ws || ws_bytes < kCtrlBytes) return CP_EWORKSPACE;
+  if (lo == hi) return CP_OK;
+  return sweep_run(g, lo, hi, 0, 0, keys, cand_ms, ws, stream);
+}
+
+int32_t cp_sweep_shard_rank(const cp_grid* g, int32_t rank, int32_t world, int64_t* keys, int32_t* cand_ms, void* ws,
+                            size_t ws_bytes, void* stream) {
+  int rc = check_grid(g);
+  if (rc) return rc;
+  if (!keys || world < 1 || rank < 0 || rank >= world) return CP_EINVAL;
+  if (!ws || ws_bytes < kCtrlBytes) return CP_EWORKSPACE;
+  const long long inner = (long long)g->n_lat * g->n_bw * g->n_mem * g->n_dp;
+  const int own_lo = (int)(inner * rank / world), own_hi = (int)(inner * (rank + 1) / world);
+  if (own_lo == own_hi) return CP_OK;
+  return sweep_run(g, 0, 0, own_lo, own_hi, keys, cand_ms, ws, stream);
 }
 
 int32_t cp_sweep_partition(const cp_grid* g, int32_t world, int64_t* bounds) {

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   long long item = -1;
   auto ROK = [&](int off, int tag) -> bool { return dbg_ok(kRingGlobal ? off : wbase + off, kRingGlobal ? 2LL * RW : s_lim, tag, item); };
   auto POK = [&](int off, int tag) -> bool { return dbg_ok(pbase + off, s_lim, tag, item); };
-  const long long n_it = kMode == MODE_SWEEP ? A.pt_hi : A.n_items;
+  const long long n_it = kMode == MODE_SWEEP ? (A.own_hi > A.own_lo ? A.pt_hi * A.blk_inner : A.pt_hi) : A.n_items;
 #else
   long long item = -1;
 #define ROK(off, tag) true
@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
           long long t = 0;
           if (s == 0) t = atomicAdd(A.sweep_counter, 1ull);
           t = __shfl_sync(segmask, t, seg * W);
-          item = sweep_task(A.grid.cand_mask & ((1u << CP_N_CAND) - 1u), A.pt_lo, A.pt_hi, t, cand);
+          item = sweep_task(A.grid.cand_mask & ((1u << CP_N_CAND) - 1u), SweepSet{A.pt_lo, A.pt_hi, A.blk_inner, A.own_lo, A.own_hi},
+                        t, cand);
         } else {
           item = item_of(task);
           task += task_stride;
@@ -545,19 +546,23 @@ __global__ void __launch_bounds__(kThreads) k_engine(const __grid_constant__ Arg
   }
 }
 
-// sweep shard initialisation: keys of the range = INT64_MAX, candidate makespans = -1
-__global__ void k_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi) {
-  for (long long k = lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; k < hi; k += (long long)gridDim.x * blockDim.x) {
+// sweep shard initialisation: keys of the launch's point set = INT64_MAX, candidate makespans = -1
+__global__ void k_sweep_init(unsigned long long* keys, int32_t* cand_ms, SweepSet q) {
+  const long long n = sweep_npts(q);
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+    const long long k = sweep_point_of(q, j);
     keys[k] = KEY_NONE;
     if (cand_ms)
       for (int c = 0; c < CP_N_CAND; ++c) cand_ms[k * CP_N_CAND + c] = -1;
   }
 }
 
-int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, void* stream) {
-  const long long n = hi - lo;
+int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, long long inner, int own_lo,
+                      int own_hi, void* stream) {
+  const SweepSet q{lo, hi, inner, own_lo, own_hi};
+  const long long n = sweep_npts(q);
   const int blocks = (int)std::min<long long>(1024, (n + 255) / 256);
-  k_sweep_init<<<blocks > 0 ? blocks : 1, 256, 0, (cudaStream_t)stream>>>(keys, cand_ms, lo, hi);
+  k_sweep_init<<<blocks > 0 ? blocks : 1, 256, 0, (cudaStream_t)stream>>>(keys, cand_ms, q);
   return (int)cudaGetLastError();
 }
 

@@ -49,6 +49,10 @@ struct Args {
   unsigned long long* sweep_counter;   // dynamic task counter of a sweep launch (workspace)
   int32_t* cand_ms;
   int32_t tier_lo, tier_hi;            // sweep greedy: only tasks whose ring lead bound is in [lo, hi]
+  // sweep point set: contiguous [pt_lo, pt_hi) if own_hi == own_lo; otherwise blocked ownership:
+  // blocks [pt_lo, pt_hi) of blk_inner points, slice [own_lo, own_hi) of each (cp_sweep_shard_rank)
+  int64_t blk_inner;
+  int32_t own_lo, own_hi;
   cp_grid grid;
 };
 
@@ -65,7 +69,8 @@ int engine_blocks_per_sm(Mode mode, bool ring_global, int threads, size_t smem, 
 int device_sm_count();
 int launch_build_static(int kind, const cp_inst_v1* inst, int n_inst, const int32_t* inst_of, long long n, int stride,
                         int words, uint32_t* ops, uint16_t* len, void* stream);
-int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, void* stream);
+int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, long long inner, int own_lo,
+                      int own_hi, void* stream);
 
 constexpr int kThreads = 128;          // 4 warps per block
 // fast-path kernels launch 2-warp blocks; their residency is set by shared memory (about 9 such

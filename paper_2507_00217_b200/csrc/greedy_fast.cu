@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(co
           long long t = 0;
           if (s == 0) t = atomicAdd(A.sweep_counter, 1ull);
           t = __shfl_sync(segmask, t, seg * W);
-          item = sweep_task(A.grid.cand_mask & ((1u << CP_N_CAND) - 1u), A.pt_lo, A.pt_hi, t, cand);
+          item = sweep_task(A.grid.cand_mask & ((1u << CP_N_CAND) - 1u), SweepSet{A.pt_lo, A.pt_hi, A.blk_inner, A.own_lo, A.own_hi},
+                        t, cand);
         } else {
           item = task < A.n_items ? task : -1;
           task += tstride;

@@ -50,12 +50,27 @@ __device__ __forceinline__ GridLane grid_lane(const cp_grid& G, long long point,
   return g;
 }
 
+// A launch's point set: contiguous [lo, hi) when own_hi == own_lo; otherwise the blocked ownership
+// of cp_sweep_shard_rank -- blocks [lo, hi) of `inner` consecutive points, slice [own_lo, own_hi)
+// of each.  sweep_npts counts it, sweep_point_of maps index j (0 <= j < npts) to a point.
+struct SweepSet {
+  long long lo, hi, inner;
+  int own_lo, own_hi;
+};
+__host__ __device__ __forceinline__ long long sweep_npts(const SweepSet& q) {
+  return q.own_hi > q.own_lo ? (q.hi - q.lo) * (long long)(q.own_hi - q.own_lo) : q.hi - q.lo;
+}
+__host__ __device__ __forceinline__ long long sweep_point_of(const SweepSet& q, long long j) {
+  if (q.own_hi <= q.own_lo) return q.lo + j;
+  const long long span = q.own_hi - q.own_lo;
+  return (q.lo + j / span) * q.inner + q.own_lo + j % span;
+}
+
 // (point, candidate) of sweep task t: active candidates of `mask` as the slowest axis, visited in
 // reverse so the most expensive tasks (highest candidate id, largest m) start first and
 // neighbouring segments of a warp get the same candidate.  Returns the point (or -1).
-__device__ __forceinline__ long long sweep_task(unsigned mask, long long pt_lo, long long pt_hi, long long t,
-                                                int& cand) {
-  const long long npts = pt_hi - pt_lo;
+__device__ __forceinline__ long long sweep_task(unsigned mask, const SweepSet& q, long long t, int& cand) {
+  const long long npts = sweep_npts(q);
   const long long ntask = npts * __popc(mask);
   if (t >= ntask) return -1;
   const long long tid = ntask - 1 - t;
@@ -63,7 +78,7 @@ __device__ __forceinline__ long long sweep_task(unsigned mask, long long pt_lo, 
   unsigned mm = mask;
   while (ci-- > 0) mm &= mm - 1;       // ci-th set bit of the mask
   cand = __ffs(mm) - 1;
-  return pt_lo + tid % npts;
+  return sweep_point_of(q, tid % npts);
 }
 
 }  // namespace cpk

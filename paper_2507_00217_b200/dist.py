@@ -18,20 +18,26 @@ def world():
     return 0, 1
 
 
-def sweep(grid, *, cand=False, group=None, stream=None, bounds=None, shard_fn=None):
-    """cp_sweep(grid) = cost-balanced shard on every rank + all_reduce(MIN) of the int64 keys.
+def sweep(grid, *, cand=False, group=None, stream=None, bounds=None, shard_fn=None, blocked=True):
+    """cp_sweep(grid) = one shard per rank + all_reduce(MIN) of the int64 keys.
 
-    Returns (keys [n_points] on every rank, cand_ms of the local shard or None).  `shard_fn`
-    (grid, lo, hi) -> (keys, cand_ms) replaces the CUDA shard (tests drive the host logic on CPU)."""
+    Default: blocked ownership (cp_sweep_shard_rank; every rank evaluates its slice of every (p, m)
+    block, so all ranks carry the same mix of work).  `bounds` (or blocked=False) selects contiguous
+    point ranges instead (cp_sweep_partition's cost-balanced cuts).  Returns (keys [n_points] on
+    every rank, cand_ms of the local shard or None).  `shard_fn` (grid, lo, hi) -> (keys, cand_ms)
+    replaces the CUDA shard (tests drive the host logic on CPU; contiguous ranges)."""
     rank, ws = world()
     cg = api.to_cp_grid(grid)
-    if bounds is None:
-        bounds = api.sweep_partition(grid, ws, cgrid=cg)
-    lo, hi = bounds[rank], bounds[rank + 1]
-    if shard_fn is None:
-        keys, cm = api.sweep_shard(grid, lo, hi, cand=cand, stream=stream, cgrid=cg)
+    if shard_fn is None and bounds is None and blocked:
+        keys, cm = api.sweep_shard_rank(grid, rank, ws, cand=cand, stream=stream, cgrid=cg)
     else:
-        keys, cm = shard_fn(grid, lo, hi)
+        if bounds is None:
+            bounds = api.sweep_partition(grid, ws, cgrid=cg)
+        lo, hi = bounds[rank], bounds[rank + 1]
+        if shard_fn is None:
+            keys, cm = api.sweep_shard(grid, lo, hi, cand=cand, stream=stream, cgrid=cg)
+        else:
+            keys, cm = shard_fn(grid, lo, hi)
     if ws > 1:
         dist.all_reduce(keys, op=dist.ReduceOp.MIN, group=group)
     return keys, cm

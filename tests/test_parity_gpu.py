@@ -289,10 +289,14 @@ def test_sweep_config5_sample_and_shards(O):
     for world in (2, 4, 8):
         b = cp.sweep_partition(grid, world)
         acc = torch.full((grid.n_points,), cp.KEY_NONE, dtype=torch.int64, device="cuda")
+        acc_r = acc.clone()
         for rk in range(world):
             kr, _ = cp.sweep_shard(grid, b[rk], b[rk + 1])
             acc = torch.minimum(acc, kr)
+            kb, _ = cp.sweep_shard_rank(grid, rk, world)          # blocked ownership
+            acc_r = torch.minimum(acc_r, kb)
         assert torch.equal(acc.cpu(), torch.from_numpy(full_h)), world
+        assert torch.equal(acc_r.cpu(), torch.from_numpy(full_h)), ("rank shards", world)
 
 
 # ------------------------------------------------------------------------------------- config 4 at full size
