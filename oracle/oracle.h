@@ -89,6 +89,12 @@ int32_t or_check_plan(const or_inst* I, const int8_t* codes, const int32_t* len,
 int32_t or_simulate(const or_inst* I, const int8_t* codes, const int32_t* len, int32_t maxlen,
                     or_result* R, int64_t* t_start);
 
+/* Wave traversal pattern (NEXT 1, reading Q32): 2 model chunks per stage in a V.  Plan entries
+ * are type | (chunk << 2).  Static check and DAG simulation as or_check_plan / or_simulate.   */
+int32_t or_check_plan_wave(const or_inst* I, const int8_t* codes, const int32_t* len, int32_t maxlen);
+int32_t or_simulate_wave(const or_inst* I, const int8_t* codes, const int32_t* len, int32_t maxlen,
+                         or_result* R, int64_t* t_start);
+
 /* Alg. 1 greedy CrossUD(Sub).  Writes plan (codes/len) and timeline; returns status. */
 int32_t or_greedy(const or_inst* I, int8_t* codes, int32_t* len, int32_t maxlen,
                   or_result* R, int64_t* t_start);

@@ -77,12 +77,14 @@ def lib():
         L.or_reserve_window.argtypes = [P(OrLink), C.c_int64, C.c_int64]
         L.or_link_init.argtypes = [P(OrLink)]
         L.or_link_free.argtypes = [P(OrLink)]
-        for fn in ("or_simulate", "or_greedy"):
+        for fn in ("or_simulate", "or_greedy", "or_simulate_wave"):
             f = getattr(L, fn)
             f.restype = C.c_int32
             f.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32, P(OrResult), P(C.c_int64)]
         L.or_check_plan.restype = C.c_int32
         L.or_check_plan.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32]
+        L.or_check_plan_wave.restype = C.c_int32
+        L.or_check_plan_wave.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32]
         for fn in ("or_build_1f1b", "or_build_gpipe", "or_build_zbh1"):
             getattr(L, fn).argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
         L.or_enumerate_opt.restype = C.c_int64
@@ -144,6 +146,28 @@ def simulate(d, codes, lens=None, timeline=False) -> dict:
     if timeline:
         out["t_start"] = ts
     return out
+
+
+def simulate_wave(d, codes, lens=None, timeline=False) -> dict:
+    """Wave-pattern plan (entries type | chunk << 2), reading Q32."""
+    L = lib()
+    p = int(d["p"])
+    c, ln, maxlen = _codes_arr(codes, lens, p)
+    inst, res = to_or_inst(d), OrResult()
+    ts = np.zeros((p, maxlen), dtype=np.int64) if timeline else None
+    L.or_simulate_wave(C.byref(inst), c.ctypes.data_as(C.POINTER(C.c_int8)), ln.ctypes.data_as(C.POINTER(C.c_int32)),
+                       maxlen, C.byref(res), ts.ctypes.data_as(C.POINTER(C.c_int64)) if timeline else None)
+    out = _result(res, p)
+    if timeline:
+        out["t_start"] = ts
+    return out
+
+
+def check_plan_wave(d, codes, lens=None) -> int:
+    p = int(d["p"])
+    c, ln, maxlen = _codes_arr(codes, lens, p)
+    return lib().or_check_plan_wave(C.byref(to_or_inst(d)), c.ctypes.data_as(C.POINTER(C.c_int8)),
+                                    ln.ctypes.data_as(C.POINTER(C.c_int32)), maxlen)
 
 
 def greedy(d, timeline=False) -> dict:

@@ -121,6 +121,94 @@ def fp_simulate(d, codes):
     return {"deadlock": True, "makespan": -1, "start": st}
 
 
+def fp_simulate_wave(d, codes):
+    """Wave pattern (reading Q32) as the least fixed point of the §3.5 start-time equations.
+
+    codes[s] = entries type | chunk << 2.  Per microbatch: F0 runs s -> s+1, turns to F1 on the
+    last stage, F1 runs s -> s-1, the loss on stage 0 starts D1, D1 runs s -> s+1, turns to D0 on
+    the last stage, D0 runs s -> s-1; W after the D of its chunk.  Each directed link carries its
+    producer's messages in plan order through one FIFO clock (messages of both chunks share it).
+    """
+    p, m, ns = d["p"], d["m"], d["n_sub"]
+    ops = []
+    for s in range(p):
+        cF, cD, cW = [0, 0], [0, 0], [0, 0]
+        row = []
+        for x in codes[s]:
+            t, c = int(x) & 3, (int(x) >> 2) & 1
+            if t == F:
+                row.append((F, c, cF[c], 0)); cF[c] += 1
+            elif t in (B, D):
+                row.append((t, c, cD[c], 0)); cD[c] += 1
+            else:
+                row.append((W, c, cW[c] // ns, cW[c] % ns)); cW[c] += 1
+        ops.append(row)
+    pos = [{(t if t != B else D, c, j, q): k for k, (t, c, j, q) in enumerate(ops[s])} for s in range(p)]
+    st = [[0] * len(ops[s]) for s in range(p)]
+    horizon = 1
+    for s in range(p):
+        horizon += sum(_dur(d, s, t, q) for (t, c, j, q) in ops[s]) + int(d["t_ag"][s])
+    for s in range(p - 1):
+        horizon += 2 * m * int(d["lat_f"][s] + d["bw_f"][s] + d["lat_b"][s] + d["bw_b"][s])
+
+    def link(end_s, s, right):
+        """arrival times of the messages stage s sends right (F0, D1) or left (F1, D0)."""
+        bw = int(d["bw_f"][s] if right else d["bw_b"][s - 1])
+        lat = int(d["lat_f"][s] if right else d["lat_b"][s - 1])
+        clk, arr = None, {}
+        for k, (t, c, j, q) in enumerate(ops[s]):
+            if t == W:
+                continue
+            goes_right = (t == F and c == 0) or (t != F and c == 1)
+            if goes_right != right:
+                continue
+            r = end_s[k]
+            ws = r if (bw == 0 or clk is None) else max(r, clk)
+            if bw > 0:
+                clk = ws + bw
+            arr[(F if t == F else D, c, j)] = ws + bw + lat
+        return arr
+
+    for _ in range(20 * sum(len(o) for o in ops) + 10):
+        end = [[st[s][k] + _dur(d, s, ops[s][k][0], ops[s][k][3]) for k in range(len(ops[s]))] for s in range(p)]
+        right = [link(end[s], s, True) if s < p - 1 else {} for s in range(p)]
+        left = [link(end[s], s, False) if s > 0 else {} for s in range(p)]
+        changed = False
+        for s in range(p):
+            for k, (t, c, j, q) in enumerate(ops[s]):
+                v = end[s][k - 1] if k > 0 else 0
+                own = lambda key: end[s][pos[s][key]]
+                # stage s hears F0 / D1 on s-1's rightward link, F1 / D0 on s+1's leftward link
+                if t == F:
+                    if c == 0:
+                        v = max(v, right[s - 1][(F, 0, j)]) if s > 0 else v
+                    else:
+                        v = max(v, own((F, 0, j, 0))) if s == p - 1 else max(v, left[s + 1][(F, 1, j)])
+                    if d["zero1"]:
+                        v = max(v, int(d["t_ag"][s]))
+                elif t in (B, D):
+                    if c == 1:
+                        v = max(v, own((F, 1, j, 0))) if s == 0 else max(v, right[s - 1][(D, 1, j)])
+                    else:
+                        v = max(v, own((D, 1, j, 0))) if s == p - 1 else max(v, left[s + 1][(D, 0, j)])
+                else:
+                    v = max(v, own((D, c, j, 0)))
+                if v != st[s][k]:
+                    st[s][k] = v
+                    changed = True
+                if v > horizon:
+                    return {"deadlock": True, "makespan": -1, "start": st}
+        if not changed:
+            mk = 0
+            for s in range(p):
+                le = end[s][-1]
+                mk = max(mk, le, le + int(d["t_dp"][s]))
+                if d["zero1"]:
+                    mk = max(mk, int(d["t_ag"][s]))
+            return {"deadlock": False, "makespan": mk, "start": st}
+    return {"deadlock": True, "makespan": -1, "start": st}
+
+
 def random_valid_plan(d, rng, p_w_first=0.3):
     """Random split plan (n_sub as in d) by a combinatorial random token game:
     uniformly pick a stage with an executable op (inputs produced, memory fits),

@@ -11,7 +11,7 @@ import os
 import numpy as np
 import pytest
 
-from tests.helpers_independent import brute_force_opt, bubble, fp_simulate, random_valid_plan
+from tests.helpers_independent import B, D, F, W, brute_force_opt, bubble, fp_simulate, random_valid_plan
 from workloads import configs as K
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -458,3 +458,57 @@ def test_sweep_point_tiny(oracle_lib):
     z = oracle_lib.simulate(d, *oracle_lib.build_static("zbh1", 4, 8))
     assert z["status"] == 0 and cm6[5] == z["makespan"] and cm6[:5] == cm[:5] and cm[5] == -1
     assert key6 == min(((c_ << 8) | i) for i, c_ in enumerate(cm6) if c_ >= 0)
+
+
+# --------------------------------------------------------------------------- Wave pattern (reading Q32)
+def test_wave_equals_fixed_point_formulation(oracle_lib):
+    """The oracle's Wave DAG simulation (Kahn order, first-fit link windows) == the least fixed
+    point of the §3.5 start-time equations over the Wave data flow with FIFO links
+    (helpers_independent.fp_simulate_wave), start tick by start tick, on random valid plans
+    (split and combined, n_sub 1-4, delays, ZeRO-1, DP tails)."""
+    from tests.helpers_independent import fp_simulate_wave
+    from workloads.wave import random_wave_plan
+    rng = np.random.default_rng(320)
+    for _ in range(150):
+        b = K.random_instances(1, seed=int(rng.integers(1 << 30)), max_p=6, max_m=5, intra_delay=True)
+        d = b.item(0)
+        rows = random_wave_plan(d["p"], d["m"], d["n_sub"], rng, combined=bool(rng.random() < 0.25))
+        r = oracle_lib.simulate_wave(d, rows, timeline=True)
+        f = fp_simulate_wave(d, rows)
+        assert r["status"] & ~2 == 0 and r["makespan"] == f["makespan"]
+        for s in range(d["p"]):
+            assert list(r["t_start"][s][:len(rows[s])]) == f["start"][s]
+
+
+def test_wave_single_microbatch_four_crossings(oracle_lib):
+    """One microbatch, every stage F0 F1 D1 D0 W1 W0: the chain F0 out, F1 back, D1 out, D0 back
+    crosses every boundary four times ("4 for Wave and 2 for UD"), so the makespan
+    is 2p(t_f + t_d) + 2 t_w + 2 sum_b(lat_f + bw_f + lat_b + bw_b)."""
+    rng = np.random.default_rng(321)
+    for _ in range(60):
+        p, n_dc = int(rng.integers(1, 9)), int(rng.integers(1, 5))
+        f, dd_, w = (int(x) for x in rng.integers(1, 100, size=3))
+        lat, bw, latb, bwb = (int(x) for x in rng.integers(0, 80, size=4))
+        d = inst(p, 1, n_dc, f, dd_, w, lat=lat, bw=bw, lat_b=latb, bw_b=bwb, mlim_x1000=10**6)
+        rows = [[F, F | 4, D | 4, D, W | 4, W] for _ in range(p)]
+        r = oracle_lib.simulate_wave(d, rows)
+        cross = sum(int(d["lat_f"][b] + d["bw_f"][b] + d["lat_b"][b] + d["bw_b"][b]) for b in range(p - 1))
+        assert r["status"] == 0 and r["makespan"] == 2 * p * (f + dd_) + 2 * w + 2 * cross
+
+
+def test_wave_plan_rules_and_deadlock(oracle_lib):
+    """Q29 per chunk: F count m, D+B count m, W = n_sub * D with the prefix rule, no B/D mixing,
+    codes < 8; a turn-around taken in the wrong order (F1 before F0 on the last stage) deadlocks."""
+    d = inst(3, 2, 1, 5, 5, 5, mlim_x1000=10**6)
+    good = [[F, F, F | 4, F | 4, D | 4, D | 4, D, D, W | 4, W | 4, W, W] for _ in range(3)]
+    assert oracle_lib.check_plan_wave(d, good) == 0
+    assert oracle_lib.simulate_wave(d, good)["status"] == 0
+    bad_count = [r[:] for r in good]; bad_count[1] = bad_count[1][:-1] + [W | 4]
+    bad_prefix = [r[:] for r in good]; bad_prefix[0] = [W] + bad_prefix[0][:-1]
+    bad_mix = [r[:] for r in good]; bad_mix[2] = [F, F, F | 4, F | 4, B | 4, B | 4, D, D, W, W]
+    bad_code = [r[:] for r in good]; bad_code[0][0] = 9
+    for plan in (bad_count, bad_prefix, bad_mix, bad_code):
+        assert oracle_lib.check_plan_wave(d, plan) == 4 and oracle_lib.simulate_wave(d, plan)["status"] == 4
+    cyc = [r[:] for r in good]
+    cyc[2] = [F | 4, F, F, F | 4, D | 4, D | 4, D, D, W | 4, W | 4, W, W]
+    assert oracle_lib.simulate_wave(d, cyc)["status"] == 1
