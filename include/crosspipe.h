@@ -102,8 +102,10 @@ typedef struct {
 typedef struct {
   int32_t n;                  /* number of schedules */
   int32_t stage_stride;       /* >= max_pp */
-  int32_t words;              /* words per stage row: capacity 16*words entries */
-  int32_t _pad;
+  int32_t words;              /* words per stage row: capacity 16*words entries (8*words if entry_bits 4) */
+  int32_t entry_bits;         /* 0 or 2: UD plans, 2-bit entries (above).  4 (cp_simulate only): Wave plans
+                                 (reading Q32), 4-bit entries type | chunk << 2, 8 per word LSB-first, same
+                                 [n][words][stage_stride] order; needs max_pp <= 32 and max_mb <= 256 */
   const int32_t* inst_of;     /* [n] instance of schedule i; NULL: instance i (or 0 if instances.n == 1) */
   uint32_t* ops;              /* [n][words][stage_stride]; input of cp_simulate, output of cp_greedy */
   uint16_t* len;              /* [n][stage_stride] entries per stage row */

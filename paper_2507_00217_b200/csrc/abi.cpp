@@ -278,6 +278,54 @@ size_t cp_workspace_bytes(int32_t which, const void* desc, int64_t n_items) {
   return ws_sim_greedy(in, n_items);
 }
 
+// Wave plans (reading Q32): k_wave32, one item per warp.  A first pass with small occupancy-gated
+// rings; items that stall on a full ring are re-run by a second pass with rings of n_mb slots.
+int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* res, void* ws, size_t ws_bytes,
+             void* stream) {
+  const long long n = sc->n;
+  if (in->max_mb > 256 || sc->stage_stride < in->max_pp) return CP_EUNSUPPORTED;
+  if (ws_bytes < ws_sim_greedy(in, n) || !ws) return CP_EWORKSPACE;
+  cpk::Args a;
+  std::memset(&a, 0, sizeof(a));
+  a.inst = in->inst;
+  a.inst_of = sc->inst_of;
+  a.n_inst = in->n;
+  a.n_items = n;
+  a.ops = sc->ops;
+  a.len = sc->len;
+  a.stage_stride = sc->stage_stride;
+  a.words = sc->words;
+  a.makespan = res->makespan;
+  a.peak_mem = res->peak_mem;
+  a.status = res->status;
+  a.stage_stats = res->stage_stats;
+  a.t_start = res->t_start;
+  a.len_stride = res->len_stride;
+  a.best_key = reinterpret_cast<unsigned long long*>(res->best_key);
+  a.index_base = res->index_base;
+  char* base = static_cast<char*>(ws);
+  a.ovf_count = reinterpret_cast<int32_t*>(base);
+  a.ovf_list = reinterpret_cast<int32_t*>(base + kCtrlBytes);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(a.ovf_count, 0, sizeof(int32_t), st) != cudaSuccess) return CP_ECUDA;
+  const int sms = cpk::device_sm_count();
+  for (int pass = 0; pass < 2; ++pass) {
+    a.from_list = pass;
+    a.ring_slots = pass == 0 ? fast_ring_slots(in) : 1 << lg2_ceil(in->max_mb);
+    a.plan_words = sc->words + 1;                       // one spare row: finished lanes read past their row
+    a.smem_words_per_warp = (4 * a.ring_slots * 32 + a.plan_words * 32 + 3) & ~3;
+    const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
+    if (per_warp > kMaxSmemPerBlock) return CP_EUNSUPPORTED;
+    const int wpb = per_warp * 2 <= kMaxSmemPerBlock ? 2 : 1, threads = 32 * wpb;
+    const size_t smem = per_warp * wpb;
+    const int bps = cpk::wave32_blocks_per_sm(threads, smem);
+    const long long need = pass == 0 ? (n + wpb - 1) / wpb : (long long)cpk::kFixWarps / wpb;
+    const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
+    if (cpk::launch_wave32(a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+  }
+  return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
+}
+
 int32_t cp_simulate(const cp_instances* in, const cp_schedules* sc, const cp_results* res, void* ws, size_t ws_bytes,
                     void* stream) {
   int rc = check_instances(in);
@@ -285,7 +333,9 @@ int32_t cp_simulate(const cp_instances* in, const cp_schedules* sc, const cp_res
   if (!sc || !res || sc->n < 0 || !sc->ops || !sc->len || !res->makespan || !res->status) return CP_EINVAL;
   if (sc->stage_stride < in->max_pp || sc->words < 1 || (res->t_start && res->len_stride < 1)) return CP_EINVAL;
   if (!sc->inst_of && in->n != 1 && in->n < sc->n) return CP_EINVAL;
+  if (sc->entry_bits != 0 && sc->entry_bits != 2 && sc->entry_bits != 4) return CP_EINVAL;
   if (sc->n == 0) return CP_OK;
+  if (sc->entry_bits == 4) return run_wave(in, sc, res, ws, ws_bytes, stream);
   return run_engine(cpk::MODE_SIM, in, sc, res, ws, ws_bytes, stream);
 }
 

@@ -60,6 +60,8 @@ struct Args {
 int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int threads, size_t smem, void* stream);
 // fast path of cp_simulate (sim32.cu): one item per warp, stage_stride 32, smem plans (TMA), no timeline
 int launch_sim32(const Args& a, int blocks, int threads, size_t smem, void* stream);
+int launch_wave32(const Args& a, int blocks, int threads, size_t smem, void* stream);
+int wave32_blocks_per_sm(int threads, size_t smem);
 int sim32_blocks_per_sm(int threads, size_t smem);
 // fast path of cp_greedy (greedy_fast.cu): compile-time segment width W in {8, 16, 32}, no timeline
 // grid = false: cp_greedy; grid = true: the greedy candidates of cp_sweep_shard

@@ -520,3 +520,74 @@ def test_sweep_six_candidates(O):
     torch.cuda.synchronize()
     assert cm.shape[1] == 6
     check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
+
+
+# ------------------------------------------------------------------------------------- Wave pattern (NEXT 1)
+def _wave_batch(n, seed, max_p, max_m, combined_frac=0.25):
+    from workloads.wave import pack_wave_plans, random_wave_plan
+    rng = np.random.default_rng(seed)
+    batch = K.random_instances(n, seed=seed, max_p=max_p, max_m=max_m, intra_delay=True)
+    plans = [random_wave_plan(int(batch.p[i]), int(batch.m[i]), int(batch.n_sub[i]), rng,
+                              combined=bool(rng.random() < combined_frac)) for i in range(n)]
+    ops, ln = pack_wave_plans(plans, stage_stride=32)
+    return batch, plans, ops, ln
+
+
+def check_wave(O, batch, plans, r, timeline):
+    for i, pl in enumerate(plans):
+        d = batch.item(i)
+        w = O.simulate_wave(d, pl, timeline=timeline)
+        p = d["p"]
+        assert int(r["status"][i]) == w["status"], (i, int(r["status"][i]), w["status"])
+        assert int(r["makespan"][i]) == w["makespan"], (i, int(r["makespan"][i]), w["makespan"])
+        assert int(r["peak_mem"][i]) == w["peak_mem"], i
+        if w["makespan"] >= 0:
+            ss = r["stage_stats"][i]
+            assert np.array_equal(ss[:p, 0], w["first_start"]) and np.array_equal(ss[:p, 1], w["last_end"]), i
+            assert np.array_equal(ss[:p, 2], w["busy"]) and np.array_equal(ss[:p, 3], w["peak"]), i
+            if timeline:
+                for s in range(p):
+                    L = len(pl[s])
+                    assert np.array_equal(r["t_start"][i][s, :L], w["t_start"][s, :L]), (i, s)
+
+
+@pytest.mark.parametrize("max_p,seed", [(32, 50), (8, 51), (3, 52)])
+def test_simulate_wave_random_plans(O, max_p, seed):
+    """Wave plans (reading Q32) through cp_simulate (k_wave32) == the oracle's Wave DAG, status,
+    makespan, peak, per-stage stats and every start tick; split and combined plans, n_sub 1-4,
+    delays, ZeRO-1, DP tails."""
+    batch, plans, ops, ln = _wave_batch(120, seed, max_p, 10)
+    inst = cp.Instances(batch)
+    o, l_ = plans_to_device(ops, ln)
+    r = to_host(cp.simulate(inst, o, l_, stats=True, timeline=True, wave=True))
+    check_wave(O, batch, plans, r, timeline=True)
+
+
+def test_simulate_wave_ring_fixup_and_invalid(O):
+    """A 1-slot first-pass ring forces the second pass (rings of n_mb slots) without changing any
+    result; corrupted plans (counts, W before its D, stray chunk bits) report BAD_PLAN and a turn-
+    around taken in the wrong order deadlocks, as in the oracle."""
+    batch, plans, ops, ln = _wave_batch(80, 53, 16, 12, combined_frac=0.0)
+    rng = np.random.default_rng(54)
+    for i in range(0, 80, 4):
+        s = int(rng.integers(batch.p[i]))
+        k = int(rng.integers(4))
+        row = plans[i][s]
+        if k == 0:
+            row[-1] = row[-1] ^ 4                        # W of the other chunk: counts break
+        elif k == 1:
+            j = row.index(next(x for x in row if (x & 3) == 3)); row.insert(0, row.pop(j))   # W first
+        elif k == 2:
+            row[0] = row[0] | 8                          # stray bit
+        elif batch.p[i] > 1:
+            pl = plans[i][int(batch.p[i]) - 1]           # last stage: F1 before F0 -> cycle
+            a, b = pl.index(0), pl.index(4); pl[a], pl[b] = 4, 0
+    from workloads.wave import pack_wave_plans
+    ops, ln = pack_wave_plans(plans, stage_stride=32)
+    inst = cp.Instances(batch)
+    o, l_ = plans_to_device(ops, ln)
+    ref = to_host(cp.simulate(inst, o, l_, stats=True, wave=True))
+    small = to_host(cp.simulate(inst, o, l_, stats=True, wave=True, ring=1))
+    for k in ("status", "makespan", "peak_mem", "stage_stats"):
+        assert np.array_equal(ref[k], small[k]), k
+    check_wave(O, batch, plans, ref, timeline=False)
