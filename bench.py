@@ -312,6 +312,31 @@ def run_ours(args):
                   "workload": "config3: 1e5 instances/GPU, p=16, 2 DCs, m=32, n_sub 1/2/4, memory x DP x ZeRO-1 grid",
                   "ms_per_launch": gms / gsteps, "status_ok": bool((g["status"] == 0).all().item())}
 
+    # ---------------- secondary: Wave-pattern evaluation (NEXT 1, reading Q32): 2e5 random valid Wave
+    # plans per GPU of one p=32 / 4-DC / m=32 instance (two chunks: 192 entries per stage, as config 4)
+    wave = None
+    if not args.no_wave:
+        wb = K.wave_instance()
+        winst = cp.Instances(wb)
+        nw = args.n_wave or 200_000
+        wops, wln = PL.wave_plans_device(32, 32, 1, nw, seed=K.PERTURB_SEED ^ 0x3A, id0=rank * nw, q=1, stride=32)
+        for _ in range(3):
+            wr = cp.simulate(winst, wops, wln, best=True, wave=True)
+        wsteps = max(1, min(args.steps, 5))
+        barrier(ws)
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(stream)
+        for _ in range(wsteps):
+            wr = cp.simulate(winst, wops, wln, best=True, wave=True)
+        v1.record(stream)
+        torch.cuda.synchronize()
+        wms = max_over_ranks(v0.elapsed_time(v1), ws)
+        wave = {"value": ws * nw * wsteps / (wms / 1e3), "unit": "evals/s",
+                "workload": "Wave (2 chunks, V): 2e5 random valid plans/GPU of one p=32, 4-DC, m=32 instance "
+                            "(L=T_F, T_bw=T_F/2), makespan + peak memory + argmin",
+                "ms_per_launch": wms / wsteps, "status_ok": bool((wr["status"] == 0).all().item())}
+        del wops, wln
+
     # ---------------- secondary: sweeps (config 2 on one GPU's shard, config 5 sharded over all
     # ranks with one all_reduce(MIN) of the packed keys inside the timed region)
     sweeps = None
@@ -365,6 +390,7 @@ def run_ours(args):
             "gpu_launches": 2 * args.steps,
             "clocks": clk,
             "greedy": greedy,
+            "wave": wave,
             "sweep": sweeps,
             "best_schedule": {"makespan_ticks": best >> 32, "index": best & 0xFFFFFFFF, "all_status_ok": status_ok},
         }
@@ -392,6 +418,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="schedules per GPU (default 1e6)")
     ap.add_argument("--n-greedy", type=int, default=0)
     ap.add_argument("--no-greedy", action="store_true")
+    ap.add_argument("--n-wave", type=int, default=0, help="Wave plans per GPU (default 2e5)")
+    ap.add_argument("--no-wave", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--chunks", type=int, default=8, help="e2e host pipeline chunks")

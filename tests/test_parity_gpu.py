@@ -591,3 +591,25 @@ def test_simulate_wave_ring_fixup_and_invalid(O):
     for k in ("status", "makespan", "peak_mem", "stage_stats"):
         assert np.array_equal(ref[k], small[k]), k
     check_wave(O, batch, plans, ref, timeline=False)
+
+
+def test_wave_bench_size_sampled(O):
+    """The bench's Wave workload (p=32, 4 DCs, m=32; device-generated plans == host-generated plans)
+    in the bench launch configuration; 30 sampled plans checked against the oracle."""
+    from workloads.wave import unpack_wave_plans
+    b = K.wave_instance()
+    n = 20_000
+    ops, ln = PL.wave_plans_device(32, 32, 1, n, seed=K.PERTURB_SEED ^ 0x3A, q=1, stride=32)
+    r = to_host(cp.simulate(cp.Instances(b), ops, ln, stats=True, best=True, wave=True))
+    idx = np.random.default_rng(19).choice(n, 30, replace=False)
+    hops, hln = PL.wave_plans_host(32, 32, 1, n, seed=K.PERTURB_SEED ^ 0x3A, q=1, stride=32)
+    assert np.array_equal(hops.view(np.int32), ops.cpu().numpy()) and np.array_equal(hln.view(np.int16), ln.cpu().numpy())
+    codes, lens = unpack_wave_plans(hops, hln)
+    d = b.item(0)
+    for i in idx:
+        w = O.simulate_wave(d, [list(codes[i, s, :lens[i, s]]) for s in range(32)])
+        assert int(r["status"][i]) == w["status"] and int(r["makespan"][i]) == w["makespan"], i
+        assert int(r["peak_mem"][i]) == w["peak_mem"], i
+    ok = r["status"] == 0
+    best = int(r["best_key"][0])
+    assert best >> 32 == int(r["makespan"][ok].min())

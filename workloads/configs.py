@@ -125,6 +125,13 @@ def perturbed_instance() -> InstanceBatch:
 PERTURB_SEED = SEED ^ 0x4
 
 
+def wave_instance() -> InstanceBatch:
+    """Wave bench instance (NEXT 1): config 4's setup (p=32, 4 DCs, L = T_F, T_bw = T_F/2) with m = 32, so
+    each stage runs 2 chunks x 3 x 32 = 192 entries as in config 4; memory budget 3x the 1F1B device
+    peak (two chunks' activations)."""
+    return uniform_instance(32, 32, 4, T_F, T_F, T_F, lat=T_F, bw=T_F // 2, mlim_x1000=3000)
+
+
 # ---------------------------------------------------------------------------------------
 # config 5 -- full sweep: 4 DCs, 8-32 stages, 8-128 mb, latency x bandwidth x memory grid
 def full_sweep_grid(tick_s=1e-5) -> Grid:

@@ -68,6 +68,64 @@ __host__ __device__ static int gen_plan(int p, int m, int nsub, const int32_t* m
   return 0;
 }
 
+// Wave pattern (reading Q32): the same round-synchronous token game over the Wave data flow (F0
+// needs F0 of s-1; F1 needs F1 of s+1, or the own F0 on the last stage; D1 needs D1 of s-1, or the
+// own F1 on stage 0; D0 needs D0 of s+1, or the own D1 on the last stage; W sub-blocks of chunk c
+// need a D of chunk c).  No memory gating, so the game cannot get stuck.  Preference: D (chunk 1
+// first) > F (chunk 0 first) > W, or with probability q/4 a uniformly random executable entry.
+// Output: 4-bit entries type | chunk << 2, 8 per word, word-major / stage-minor.
+__host__ __device__ static int gen_wave_plan(int p, int m, int nsub, uint64_t seed, uint64_t id, int q, uint32_t* ops,
+                                             uint16_t* len, int words, int stride) {
+  const int total = 2 * (2 + nsub) * m;
+  if (p < 1 || p > GEN_MAXP || m < 1 || nsub < 1 || total > 8 * words) return 2;
+  int nF[2][GEN_MAXP], nD[2][GEN_MAXP], nW[2][GEN_MAXP], pF[2][GEN_MAXP], pD[2][GEN_MAXP];
+  uint32_t cur[GEN_MAXP];
+  for (int s = 0; s < p; ++s) {
+    cur[s] = 0;
+    for (int c = 0; c < 2; ++c) nF[c][s] = nD[c][s] = nW[c][s] = 0;
+  }
+  for (uint64_t r = 0;; ++r) {
+    for (int s = 0; s < p; ++s)
+      for (int c = 0; c < 2; ++c) { pF[c][s] = nF[c][s]; pD[c][s] = nD[c][s]; }
+    bool progress = false, done = true;
+    for (int s = 0; s < p; ++s) {
+      const int k = nF[0][s] + nF[1][s] + nD[0][s] + nD[1][s] + nW[0][s] + nW[1][s];
+      if (k == total) continue;
+      done = false;
+      int cand[6], nx = 0;                       // entry codes, in preference order
+      if (nD[1][s] < m && (s == 0 ? nF[1][s] > nD[1][s] : pD[1][s - 1] > nD[1][s])) cand[nx++] = 2 | 4;
+      if (nD[0][s] < m && (s == p - 1 ? nD[1][s] > nD[0][s] : pD[0][s + 1] > nD[0][s])) cand[nx++] = 2;
+      if (nF[0][s] < m && (s == 0 || pF[0][s - 1] > nF[0][s])) cand[nx++] = 0;
+      if (nF[1][s] < m && (s == p - 1 ? nF[0][s] > nF[1][s] : pF[1][s + 1] > nF[1][s])) cand[nx++] = 4;
+      if (nW[1][s] < nsub * nD[1][s]) cand[nx++] = 3 | 4;
+      if (nW[0][s] < nsub * nD[0][s]) cand[nx++] = 3;
+      if (nx == 0) continue;
+      const uint64_t u = gen_mix(seed ^ gen_mix(id ^ ((uint64_t)s << 40) ^ (r << 8) ^ 0x57ull));
+      const int x = ((int)(u & 3u) < q) ? cand[(int)((u >> 8) % (uint64_t)nx)] : cand[0];
+      const int t = x & 3, c = x >> 2;
+      if (t == 0) nF[c][s]++;
+      else if (t == 2) nD[c][s]++;
+      else nW[c][s]++;
+      cur[s] |= (uint32_t)x << ((k & 7) * 4);
+      if ((k & 7) == 7 || k + 1 == total) { ops[(k >> 3) * stride + s] = cur[s]; cur[s] = 0; }
+      progress = true;
+    }
+    if (done) break;
+    if (!progress) return 1;
+  }
+  for (int s = 0; s < p; ++s) len[s] = (uint16_t)total;
+  return 0;
+}
+
+__global__ void k_gen_wave(int p, int m, int nsub, uint64_t seed, uint64_t id0, int q, long long n, int words,
+                           int stride, uint32_t* ops, uint16_t* len, int32_t* err) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (gen_wave_plan(p, m, nsub, seed, id0 + (uint64_t)i, q, ops + i * (long long)words * stride,
+                    len + i * (long long)stride, words, stride))
+    atomicAdd(err, 1);
+}
+
 struct GenArgs {
   int p, m, nsub, q, words, stride;
   int32_t mf[GEN_MAXP], md[GEN_MAXP], mw[GEN_MAXP], mlim[GEN_MAXP];
@@ -94,6 +152,24 @@ int cpgen_plans_host(int p, int m, int nsub, const int32_t* mf, const int32_t* m
     err += gen_plan(p, m, nsub, mf, md, mw, mlim, seed, id0 + (uint64_t)i, q, ops + i * (long long)words * stride,
                     len + i * (long long)stride, words, stride) != 0;
   return err;
+}
+
+// Wave plans (host / device, identical for the same ids)
+int cpgen_wave_plans_host(int p, int m, int nsub, uint64_t seed, uint64_t id0, int q, long long n, uint32_t* ops,
+                          uint16_t* len, int words, int stride) {
+  int err = 0;
+  for (long long i = 0; i < n; ++i)
+    err += gen_wave_plan(p, m, nsub, seed, id0 + (uint64_t)i, q, ops + i * (long long)words * stride,
+                         len + i * (long long)stride, words, stride) != 0;
+  return err;
+}
+int cpgen_wave_plans_device(int p, int m, int nsub, uint64_t seed, uint64_t id0, int q, long long n, uint32_t* ops,
+                            uint16_t* len, int words, int stride, int32_t* err, void* stream) {
+  const int threads = 128;
+  const long long blocks = (n + threads - 1) / threads;
+  k_gen_wave<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(p, m, nsub, seed, id0, q, n, words, stride, ops,
+                                                                      len, err);
+  return (int)cudaGetLastError();
 }
 
 // device: same plans into device buffers (err: device int32, caller-zeroed)

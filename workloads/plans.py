@@ -36,6 +36,13 @@ def lib():
         L.cpgen_plans_device.argtypes = [C.c_int, C.c_int, C.c_int, P32, P32, P32, P32, C.c_uint64, C.c_uint64,
                                          C.c_int, C.c_longlong, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                          C.c_void_p, C.c_void_p]
+        L.cpgen_wave_plans_host.restype = C.c_int
+        L.cpgen_wave_plans_host.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_longlong,
+                                            C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.cpgen_wave_plans_device.restype = C.c_int
+        L.cpgen_wave_plans_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
+                                              C.c_longlong, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
+                                              C.c_void_p]
         _lib = L
     return _lib
 
@@ -81,4 +88,38 @@ def plans_device(batch, n, seed, id0=0, q=1, stride=None, i=0, device="cuda"):
         raise RuntimeError(f"cpgen launch failed: {rc}")
     if int(err.item()):
         raise RuntimeError(f"plan generator failed on {int(err.item())} plans")
+    return ops, ln
+
+
+def wave_words(p, m, n_sub=1):
+    return (2 * (2 + n_sub) * m + 7) // 8
+
+
+def wave_plans_host(p, m, n_sub, n, seed, id0=0, q=1, stride=None):
+    """n random valid Wave plans (reading Q32), 4-bit entries (host).  Returns (ops uint32 [n, words, stride],
+    len uint16 [n, stride])."""
+    stride = stride or p
+    words = wave_words(p, m, n_sub)
+    ops = np.zeros((n, words, stride), dtype=np.uint32)
+    ln = np.zeros((n, stride), dtype=np.uint16)
+    err = lib().cpgen_wave_plans_host(p, m, n_sub, seed, id0, q, n, ops.ctypes.data, ln.ctypes.data, words, stride)
+    if err:
+        raise RuntimeError(f"wave plan generator failed on {err} plans")
+    return ops, ln
+
+
+def wave_plans_device(p, m, n_sub, n, seed, id0=0, q=1, stride=None, device="cuda"):
+    """Same Wave plans generated on the GPU.  Returns torch tensors."""
+    import torch
+    stride = stride or p
+    words = wave_words(p, m, n_sub)
+    ops = torch.zeros((n, words, stride), dtype=torch.int32, device=device)
+    ln = torch.zeros((n, stride), dtype=torch.int16, device=device)
+    err = torch.zeros(1, dtype=torch.int32, device=device)
+    rc = lib().cpgen_wave_plans_device(p, m, n_sub, seed, id0, q, n, ops.data_ptr(), ln.data_ptr(), words, stride,
+                                       err.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    if rc:
+        raise RuntimeError(f"cpgen launch failed: {rc}")
+    if int(err.item()):
+        raise RuntimeError(f"wave plan generator failed on {int(err.item())} plans")
     return ops, ln
