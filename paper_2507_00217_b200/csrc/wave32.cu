@@ -23,9 +23,14 @@ namespace {
 constexpr int32_t WINF = 1 << 30;
 constexpr unsigned WFULL = 0xffffffffu;
 __device__ __forceinline__ int wmx(int a, int b) { return a > b ? a : b; }
+__device__ __forceinline__ int wmadd(int g, int d, int x) {   // x + g*d on the FMA pipe
+  int r;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(g), "r"(d), "r"(x));
+  return r;
+}
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads) k_wave32(const __grid_constant__ Args A) {
+__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const __grid_constant__ Args A) {
   extern __shared__ __align__(16) int32_t smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -72,27 +77,32 @@ __global__ void __launch_bounds__(kThreads) k_wave32(const __grid_constant__ Arg
     if (__any_sync(WFULL, bad)) st = CPI_BAD_INSTANCE;
     else if (__any_sync(WFULL, plen > 8 * A.words)) st = CPI_BAD_PLAN;
     else if (m > CP_MAX_MB || ns > CP_MAX_SUB || u >= (long long)WINF) st = CPI_OVERFLOW;
-    // stage this lane's row and check Q29 per chunk (counts, W prefix rule, codes < 8)
+    // stage this lane's row and check Q29's count and mixing rules per chunk, and codes < 8, with
+    // nibble popcounts over the words; the W-prefix rule stays dynamic (a W ahead of its D stalls
+    // and the non-completion path classifies the item)
     bool bplan = false;
     if (!st && s < p) {
-      int cF[2] = {0, 0}, cB[2] = {0, 0}, cD[2] = {0, 0}, cW[2] = {0, 0};
+      int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};          // per entry value type | chunk << 2
       for (int k = 0; k * 8 < plen; ++k) {
         const uint32_t w = A.ops[(item * A.words + k) * A.stage_stride + s];
         smem[iP + (k << 5)] = (int32_t)w;
         const int n = plen - 8 * k < 8 ? plen - 8 * k : 8;
-        for (int e = 0; e < n; ++e) {
-          const uint32_t x = (w >> (4 * e)) & 15u;
-          const int ty = x & 3, ch = (x >> 2) & 1;
-          if (x & 8u) bplan = true;
-          if (ty == CP_OP_F) ++cF[ch];
-          else if (ty == CP_OP_B) ++cB[ch];
-          else if (ty == CP_OP_D) ++cD[ch];
-          else { ++cW[ch]; if (cW[ch] > ns * cD[ch]) bplan = true; }
+        const uint32_t vm = (n == 8 ? 0xffffffffu : ((1u << (4 * n)) - 1u)) & 0x11111111u;
+        if ((w >> 3) & vm) bplan = true;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint32_t t = w ^ (0x11111111u * (uint32_t)v);
+          cnt[v] += __popc(~(t | (t >> 1) | (t >> 2) | (t >> 3)) & vm);
         }
       }
-      for (int ch = 0; ch < 2; ++ch)
-        if (cF[ch] != m || cB[ch] + cD[ch] != m || cW[ch] != ns * cD[ch]) bplan = true;
-      if (cB[0] + cB[1] > 0 && cD[0] + cD[1] + cW[0] + cW[1] > 0) bplan = true;
+      for (int ch = 0; ch < 2; ++ch) {
+        const int cF = cnt[4 * ch + CP_OP_F], cB = cnt[4 * ch + CP_OP_B], cD = cnt[4 * ch + CP_OP_D];
+        const int cW = cnt[4 * ch + CP_OP_W];
+        if (cF != m || cB + cD != m || cW != ns * cD) bplan = true;
+      }
+      if (cnt[CP_OP_B] + cnt[4 + CP_OP_B] > 0 &&
+          cnt[CP_OP_D] + cnt[4 + CP_OP_D] + cnt[CP_OP_W] + cnt[4 + CP_OP_W] > 0)
+        bplan = true;
     }
     if (!st && __any_sync(WFULL, bplan)) st = CPI_BAD_PLAN;
     if (st) {
@@ -111,68 +121,85 @@ __global__ void __launch_bounds__(kThreads) k_wave32(const __grid_constant__ Arg
     const int mL = s > 0 ? -1 : 0, mR = s < p - 1 ? -1 : 0;
     const bool sendR = s < p - 1, sendL = s > 0 && s < p;
     const int wq = tw / ns, wr = tw % ns;
-    int clk = tag, mem = 0, peak = 0, busy = 0, first = 0, pos = 0;
-    int nF0 = 0, nF1 = 0, nD0 = 0, nD1 = 0, w0 = 0, w1 = 0, lkR = 0, lkL = 0;
+    int clk = tag, mem = 0, peak = 0, pos = 0, lkR = 0, lkL = 0;
+    // packed counts: aP = nF0 | nD1 << 16 (streams sent right), bP = nF1 | nD0 << 16 (sent left),
+    // wP = W sub-blocks of chunk 0 | chunk 1 << 16
+    int aP = 0, bP = 0, wP = 0;
+    int lm = s == 0 ? 0xffff : 0, rm = s == p - 1 ? 0xffff : 0;      // no producer / no consumer
+    asm("mov.b32 %0, %0;" : "+r"(lm));
+    asm("mov.b32 %0, %0;" : "+r"(rm));
+    const bool last = s == p - 1, first_s = s == 0;
     __syncwarp();
     for (;;) {
-      const int aP = nF0 | (nD1 << 16), bP = nF1 | (nD0 << 16);     // right-going / left-going counts
       const int la = __shfl_up_sync(WFULL, aP, 1), lb = __shfl_up_sync(WFULL, bP, 1);
       const int ra = __shfl_down_sync(WFULL, aP, 1), rb = __shfl_down_sync(WFULL, bP, 1);
+      const int nF0 = aP & 0xffff, nD1 = aP >> 16, nF1 = bP & 0xffff, nD0 = bP >> 16;
+      // the four ring heads, addressed by the consumer's own counts
+      const int hF0 = smem[iF0 + ((nF0 & Rm) << 5)] & mL, hD1 = smem[iD1 + ((nD1 & Rm) << 5)] & mL;
+      const int hF1 = smem[iF1 + ((nF1 & Rm) << 5)] & mR, hD0 = smem[iD0 + ((nD0 & Rm) << 5)] & mR;
       const uint32_t wv = (uint32_t)smem[iP + ((pos >> 3) << 5)];
       const uint32_t x = (wv >> ((pos & 7) << 2)) & 15u;
       const int ty = x & 3, ch = (x >> 2) & 1;
-      const bool isF = ty == CP_OP_F, isW = ty == CP_OP_W, isB = ty == CP_OP_B, isDB = !isF && !isW;
+      const bool isF = ty == CP_OP_F, isW = ty == CP_OP_W, isB = ty == CP_OP_B, isDB = !isF & !isW;
       // readiness: input produced (or the own turn-around / loss), room in the consumer's ring
-      const bool rF0 = (s == 0 || (la & 0xffff) > nF0) && (!sendR || nF0 - (ra & 0xffff) < R);
-      const bool rD1 = (s == 0 ? nF1 > nD1 : (la >> 16) > nD1) && (!sendR || nD1 - (ra >> 16) < R);
-      const bool rF1 = (s == p - 1 ? nF0 > nF1 : (rb & 0xffff) > nF1) && (!sendL || nF1 - (lb & 0xffff) < R);
-      const bool rD0 = (s == p - 1 ? nD1 > nD0 : (rb >> 16) > nD0) && (!sendL || nD0 - (lb >> 16) < R);
-      const int wc = ch ? w1 : w0, ndc = ch ? nD1 : nD0;
+      const bool rF0 = (((la & 0xffff) | lm) > nF0) & (nF0 - ((ra & 0xffff) | rm) < R);
+      const bool rD1 = ((first_s ? nF1 : (la >> 16)) > nD1) & (nD1 - ((ra >> 16) | rm) < R);
+      const bool rF1 = ((last ? nF0 : (rb & 0xffff)) > nF1) & (nF1 - ((lb & 0xffff) | lm) < R);
+      const bool rD0 = ((last ? nD1 : (rb >> 16)) > nD0) & (nD0 - ((lb >> 16) | lm) < R);
+      const int wc = ch ? (wP >> 16) : (wP & 0xffff), ndc = ch ? nD1 : nD0;
       const bool rW = wc < ns * ndc;
-      const bool go = (pos < plen) && (isF ? (ch ? rF1 : rF0) : (isW ? rW : (ch ? rD1 : rD0)));
-      // input arrival: F0 / D1 from the left rings, F1 / D0 from the right rings; W: none
-      int avail = 0;
-      if (isF && ch == 0) avail = smem[iF0 + ((nF0 & Rm) << 5)] & mL;
-      else if (isF) avail = smem[iF1 + ((nF1 & Rm) << 5)] & mR;
-      else if (isDB && ch == 1) avail = smem[iD1 + ((nD1 & Rm) << 5)] & mL;
-      else if (isDB) avail = smem[iD0 + ((nD0 & Rm) << 5)] & mR;
+      const bool rdy = isF ? (ch ? rF1 : rF0) : (isW ? rW : (ch ? rD1 : rD0));
+      const bool go = (pos < plen) & rdy;
+      const bool right = (isF & (ch == 0)) | (isDB & (ch == 1));   // F0, D1 go right; F1, D0 go left
+      const int avail = isW ? 0 : (isF ? (ch ? hF1 : hF0) : (ch ? hD1 : hD0));
       const int start = wmx(clk, avail);
       const int k = wc % ns;
       const int dur = isF ? tf : (isW ? wq + (k < wr ? 1 : 0) : (isB ? td + tw : td));
       const int dm = isF ? mf : (isW ? (k == ns - 1 ? mw : 0) : (isB ? md + mw : md));
       const int end = start + dur;
-      const bool right = (isF && ch == 0) || (isDB && ch == 1);   // F0, D1 go right; F1, D0 go left
       const int nl = wmx(end, right ? lkR : lkL) + (right ? bwR : bwL);   // FIFO link clock (App. X1)
-      if (go && !isW && (right ? sendR : sendL)) {
-        const int col = (isF ? (ch ? iF1 : iF0) : (ch ? iD1 : iD0)) + (right ? 1 : -1);
-        const int cnt = isF ? (ch ? nF1 : nF0) : (ch ? nD1 : nD0);
-        smem[col + ((cnt & Rm) << 5)] = nl + (right ? latR : latL);
-      }
-      if (go) {
-        if (A.t_start && pos < A.len_stride) A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
-        if (pos == 0) first = start;
-        clk = end;
-        busy += dur;
-        mem += dm;
-        peak = wmx(peak, mem);
-        if (right && !isW) lkR = nl;
-        else if (!isW) lkL = nl;
-        if (isF) { if (ch) ++nF1; else ++nF0; }
-        else if (isW) { if (ch) ++w1; else ++w0; }
-        else { if (ch) ++nD1; else ++nD0; }
-        ++pos;
-      }
+      // message into the consumer's ring: same stream, slot = this block's count, column +-1
+      const int cnt = isF ? (ch ? nF1 : nF0) : (ch ? nD1 : nD0);
+      const int col = (isF ? (ch ? iF1 : iF0) : (ch ? iD1 : iD0)) + (right ? 1 : -1);
+      if (go & !isW & (right ? sendR : sendL)) smem[col + ((cnt & Rm) << 5)] = nl + (right ? latR : latL);
+      if (A.t_start && go && pos < A.len_stride)
+        A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
+      const int gi = go ? 1 : 0;
+      clk = wmadd(gi, end - clk, clk);
+      mem = wmadd(gi, dm, mem);
+      peak = wmx(peak, mem);
+      const int gL = (go & !isW & right) ? 1 : 0, gLl = (go & !isW & !right) ? 1 : 0;
+      lkR = wmadd(gL, nl - lkR, lkR);
+      lkL = wmadd(gLl, nl - lkL, lkL);
+      // count increments: F0 +1 / D1 +65536 into aP, F1 +1 / D0 +65536 into bP, W into wP
+      const int inc = (isF ? 1 : 65536);
+      aP = wmadd((go & !isW & right) ? 1 : 0, inc, aP);
+      bP = wmadd((go & !isW & !right) ? 1 : 0, inc, bP);
+      wP = wmadd((go & isW) ? 1 : 0, ch ? 65536 : 1, wP);
+      pos = wmadd(gi, 1, pos);
       __syncwarp();
       if (!__any_sync(WFULL, go)) break;
     }
+    const int nF0 = aP & 0xffff, nD1 = aP >> 16, nF1 = bP & 0xffff, nD0 = bP >> 16;
     // no lane progressed: complete, a cyclic wait on full rings (-> second pass), or deadlock
-    const int aP = nF0 | (nD1 << 16), bP = nF1 | (nD0 << 16);
     const int lb = __shfl_up_sync(WFULL, bP, 1), ra = __shfl_down_sync(WFULL, aP, 1);
     const bool ring_full = (sendR && (nF0 - (ra & 0xffff) >= R || nD1 - (ra >> 16) >= R)) ||
                            (sendL && (nF1 - (lb & 0xffff) >= R || nD0 - (lb >> 16) >= R));
     const bool complete = !__any_sync(WFULL, s < p && pos < plen);
+    // cannot continue: a W ahead of its D (prefix rule) reports BAD_PLAN -> scan the rest of the row
+    bool badc = false;
+    if (!complete && s < p) {
+      int cw[2] = {wP & 0xffff, wP >> 16}, cdd[2] = {nD0, nD1};
+      for (int k = pos; k < plen && !badc; ++k) {
+        const uint32_t x2 = ((uint32_t)smem[iP + ((k >> 3) << 5)] >> ((k & 7) << 2)) & 15u;
+        const int t2 = x2 & 3, c2 = (x2 >> 2) & 1;
+        if (t2 == CP_OP_W) { badc = cw[c2] >= ns * cdd[c2]; ++cw[c2]; }
+        else if (t2 != CP_OP_F) ++cdd[c2];
+      }
+    }
     int st2;
-    if (!complete && __any_sync(WFULL, ring_full) && !A.from_list) st2 = -1;
+    if (__any_sync(WFULL, badc)) st2 = CPI_BAD_PLAN;
+    else if (!complete && __any_sync(WFULL, ring_full) && !A.from_list) st2 = -1;
     else if (!complete) st2 = CPI_DEADLOCK;
     else st2 = __any_sync(WFULL, s < p && peak > mlim) ? CPI_MEM_EXCEEDED : 0;
     if (st2 == -1) {
@@ -184,17 +211,29 @@ __global__ void __launch_bounds__(kThreads) k_wave32(const __grid_constant__ Arg
         pk = wmx(pk, __shfl_xor_sync(WFULL, pk, d));
       }
       if (lane == 0) {
-        A.makespan[item] = complete ? (long long)ms : -1LL;
-        if (A.peak_mem) A.peak_mem[item] = complete ? pk : -1;
+        const bool ok = complete && st2 != CPI_BAD_PLAN;
+        A.makespan[item] = ok ? (long long)ms : -1LL;
+        if (A.peak_mem) A.peak_mem[item] = ok ? pk : -1;
         A.status[item] = st2;
         if (A.best_key && st2 == 0)
           atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)(item + A.index_base));
       }
-      if (A.stage_stats)
+      if (A.stage_stats) {
+        // a completed valid row ran every block once: busy = 2m (t_f + t_d + t_w); every row starts
+        // with F0 of microbatch 0, whose path is chunk 0's forward: first[s] = max(t_ag[s], first[s-1]
+        // + t_f + bw + lat of s-1), the max-plus prefix P_s + max_{k<=s}(ag_k - P_k)
+        const int cfw = s < p ? tf + bwR + latR : 0;
+        int Pp = cfw;
+        for (int d = 1; d < 32; d <<= 1) { const int t2 = __shfl_up_sync(WFULL, Pp, d); if (s >= d) Pp += t2; }
+        Pp -= cfw;
+        int xq = (s < p ? tag : 0) - Pp;
+        for (int d = 1; d < 32; d <<= 1) { const int t2 = __shfl_up_sync(WFULL, xq, d); if (s >= d) xq = wmx(xq, t2); }
+        const int busy = 2 * m * (tf + td + tw);
         for (int r = s; r < A.stage_stride; r += 32) {
-          const int4 v = (complete && r == s && s < p) ? make_int4(first, clk, busy, peak) : make_int4(0, 0, 0, 0);
+          const int4 v = (complete && r == s && s < p) ? make_int4(Pp + xq, clk, busy, peak) : make_int4(0, 0, 0, 0);
           *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + r) * 4) = v;
         }
+      }
     }
     __syncwarp();
   }
