@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "engine.h"
 
 namespace cpk {
@@ -38,11 +40,16 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
   const int PW = A.plan_words;                         // staged words per row (>= A.words)
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  // per-warp smem (words): [rF0][rD1][rF1][rD0] (R*32 each) [plan PW*32]
+  // per-warp smem (words): [tabA 8*32 int4][tabB 8*32 int4][rF0][rD1][rF1][rD0] (R*32 each)
+  //                        [zero row 32][plan PW*32]
   const int wbase = wib * A.smem_words_per_warp;
-  const int iF0 = wbase + lane, iD1 = iF0 + RW, iF1 = iD1 + RW, iD0 = iF1 + RW;
-  const int iP = iD0 + RW;
-  for (int k = lane; k < 4 * RW; k += 32) smem[wbase + k] = 0;
+  int4* const tabA = reinterpret_cast<int4*>(smem + wbase) + lane;          // [entry][lane]
+  int4* const tabB = reinterpret_cast<int4*>(smem + wbase + 1024) + lane;
+  const int rb0 = wbase + 2048;
+  const int iF0 = rb0 + lane, iD1 = iF0 + RW, iF1 = iD1 + RW, iD0 = iF1 + RW;
+  const int iZ = iD0 + RW;                             // zero row: inputs of W and of missing producers
+  const int iP = iZ + 32;
+  for (int k = lane; k < 4 * RW + 32; k += 32) smem[rb0 + k] = 0;
   __syncwarp();
 
   for (long long t = gwarp; ; t += nwarps) {
@@ -117,10 +124,32 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
       __syncwarp();
       continue;
     }
-    // the last stage's right rings and stage 0's left rings have no producer in this item: masks
-    const int mL = s > 0 ? -1 : 0, mR = s < p - 1 ? -1 : 0;
     const bool sendR = s < p - 1, sendL = s > 0 && s < p;
     const int wq = tw / ns, wr = tw % ns;
+    // parameter tables, entry x = type | chunk << 2:
+    //   tabA[x] = {duration, memory delta, link bw, latency} (W: first sub-block / whole W if n_sub 1)
+    //   tabB[x] = {input ring column (zero row without a producer), slot mask, output column at the
+    //             consumer (0: no message), 1 if the message goes right}
+    {
+      const int hasL = s > 0, hasR = s < p - 1;
+      const int tW = ns == 1 ? tw : wq, mW = ns == 1 ? mw : 0;
+      tabA[0 * 32] = make_int4(tf, mf, bwR, latR);
+      tabA[1 * 32] = make_int4(td + tw, md + mw, bwL, latL);
+      tabA[2 * 32] = make_int4(td, md, bwL, latL);
+      tabA[3 * 32] = make_int4(tW, mW, 0, 0);
+      tabA[4 * 32] = make_int4(tf, mf, bwL, latL);
+      tabA[5 * 32] = make_int4(td + tw, md + mw, bwR, latR);
+      tabA[6 * 32] = make_int4(td, md, bwR, latR);
+      tabA[7 * 32] = make_int4(tW, mW, 0, 0);
+      tabB[0 * 32] = make_int4(hasL ? iF0 : iZ, hasL ? Rm : 0, sendR ? iF0 + 1 : 0, 1);
+      tabB[1 * 32] = make_int4(hasR ? iD0 : iZ, hasR ? Rm : 0, sendL ? iD0 - 1 : 0, 0);
+      tabB[2 * 32] = tabB[1 * 32];
+      tabB[3 * 32] = make_int4(iZ, 0, 0, 0);
+      tabB[4 * 32] = make_int4(hasR ? iF1 : iZ, hasR ? Rm : 0, sendL ? iF1 - 1 : 0, 0);
+      tabB[5 * 32] = make_int4(hasL ? iD1 : iZ, hasL ? Rm : 0, sendR ? iD1 + 1 : 0, 1);
+      tabB[6 * 32] = tabB[5 * 32];
+      tabB[7 * 32] = tabB[3 * 32];
+    }
     int clk = tag, mem = 0, peak = 0, pos = 0, lkR = 0, lkL = 0;
     // packed counts: aP = nF0 | nD1 << 16 (streams sent right), bP = nF1 | nD0 << 16 (sent left),
     // wP = W sub-blocks of chunk 0 | chunk 1 << 16
@@ -130,56 +159,61 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
     asm("mov.b32 %0, %0;" : "+r"(rm));
     const bool last = s == p - 1, first_s = s == 0;
     __syncwarp();
-    for (;;) {
-      const int la = __shfl_up_sync(WFULL, aP, 1), lb = __shfl_up_sync(WFULL, bP, 1);
-      const int ra = __shfl_down_sync(WFULL, aP, 1), rb = __shfl_down_sync(WFULL, bP, 1);
-      const int nF0 = aP & 0xffff, nD1 = aP >> 16, nF1 = bP & 0xffff, nD0 = bP >> 16;
-      // the four ring heads, addressed by the consumer's own counts
-      const int hF0 = smem[iF0 + ((nF0 & Rm) << 5)] & mL, hD1 = smem[iD1 + ((nD1 & Rm) << 5)] & mL;
-      const int hF1 = smem[iF1 + ((nF1 & Rm) << 5)] & mR, hD0 = smem[iD0 + ((nD0 & Rm) << 5)] & mR;
-      const uint32_t wv = (uint32_t)smem[iP + ((pos >> 3) << 5)];
-      const uint32_t x = (wv >> ((pos & 7) << 2)) & 15u;
-      const int ty = x & 3, ch = (x >> 2) & 1;
-      const bool isF = ty == CP_OP_F, isW = ty == CP_OP_W, isB = ty == CP_OP_B, isDB = !isF & !isW;
-      // readiness: input produced (or the own turn-around / loss), room in the consumer's ring
-      const bool rF0 = (((la & 0xffff) | lm) > nF0) & (nF0 - ((ra & 0xffff) | rm) < R);
-      const bool rD1 = ((first_s ? nF1 : (la >> 16)) > nD1) & (nD1 - ((ra >> 16) | rm) < R);
-      const bool rF1 = ((last ? nF0 : (rb & 0xffff)) > nF1) & (nF1 - ((lb & 0xffff) | lm) < R);
-      const bool rD0 = ((last ? nD1 : (rb >> 16)) > nD0) & (nD0 - ((lb >> 16) | lm) < R);
-      const int wc = ch ? (wP >> 16) : (wP & 0xffff), ndc = ch ? nD1 : nD0;
-      const bool rW = wc < ns * ndc;
-      const bool rdy = isF ? (ch ? rF1 : rF0) : (isW ? rW : (ch ? rD1 : rD0));
-      const bool go = (pos < plen) & rdy;
-      const bool right = (isF & (ch == 0)) | (isDB & (ch == 1));   // F0, D1 go right; F1, D0 go left
-      const int avail = isW ? 0 : (isF ? (ch ? hF1 : hF0) : (ch ? hD1 : hD0));
-      const int start = wmx(clk, avail);
-      const int k = wc % ns;
-      const int dur = isF ? tf : (isW ? wq + (k < wr ? 1 : 0) : (isB ? td + tw : td));
-      const int dm = isF ? mf : (isW ? (k == ns - 1 ? mw : 0) : (isB ? md + mw : md));
-      const int end = start + dur;
-      const int nl = wmx(end, right ? lkR : lkL) + (right ? bwR : bwL);   // FIFO link clock (App. X1)
-      // message into the consumer's ring: same stream, slot = this block's count, column +-1
-      const int cnt = isF ? (ch ? nF1 : nF0) : (ch ? nD1 : nD0);
-      const int col = (isF ? (ch ? iF1 : iF0) : (ch ? iD1 : iD0)) + (right ? 1 : -1);
-      if (go & !isW & (right ? sendR : sendL)) smem[col + ((cnt & Rm) << 5)] = nl + (right ? latR : latL);
-      if (A.t_start && go && pos < A.len_stride)
-        A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
-      const int gi = go ? 1 : 0;
-      clk = wmadd(gi, end - clk, clk);
-      mem = wmadd(gi, dm, mem);
-      peak = wmx(peak, mem);
-      const int gL = (go & !isW & right) ? 1 : 0, gLl = (go & !isW & !right) ? 1 : 0;
-      lkR = wmadd(gL, nl - lkR, lkR);
-      lkL = wmadd(gLl, nl - lkL, lkL);
-      // count increments: F0 +1 / D1 +65536 into aP, F1 +1 / D0 +65536 into bP, W into wP
-      const int inc = (isF ? 1 : 65536);
-      aP = wmadd((go & !isW & right) ? 1 : 0, inc, aP);
-      bP = wmadd((go & !isW & !right) ? 1 : 0, inc, bP);
-      wP = wmadd((go & isW) ? 1 : 0, ch ? 65536 : 1, wP);
-      pos = wmadd(gi, 1, pos);
-      __syncwarp();
-      if (!__any_sync(WFULL, go)) break;
-    }
+    auto rounds = [&](auto n1) {
+      constexpr bool kN1 = decltype(n1)::value;       // n_sub == 1: a W entry is a whole W block
+      for (;;) {
+        const int la = __shfl_up_sync(WFULL, aP, 1), lb = __shfl_up_sync(WFULL, bP, 1);
+        const int ra = __shfl_down_sync(WFULL, aP, 1), rb = __shfl_down_sync(WFULL, bP, 1);
+        const int nF0 = aP & 0xffff, nD1 = aP >> 16, nF1 = bP & 0xffff, nD0 = bP >> 16;
+        const uint32_t wv = (uint32_t)smem[iP + ((pos >> 3) << 5)];
+        const uint32_t x = (wv >> ((pos & 7) << 2)) & 7u;
+        const int4 ta = tabA[x << 5];
+        const int4 tb = tabB[x << 5];
+        const int ch = (int)(x >> 2);
+        const bool isF = (x & 3u) == CP_OP_F, isW = (x & 3u) == CP_OP_W;
+        // readiness: input produced (or the own turn-around / loss), room in the consumer's ring
+        const bool rF0 = (((la & 0xffff) | lm) > nF0) & (nF0 - ((ra & 0xffff) | rm) < R);
+        const bool rD1 = ((first_s ? nF1 : (la >> 16)) > nD1) & (nD1 - ((ra >> 16) | rm) < R);
+        const bool rF1 = ((last ? nF0 : (rb & 0xffff)) > nF1) & (nF1 - ((lb & 0xffff) | lm) < R);
+        const bool rD0 = ((last ? nD1 : (rb >> 16)) > nD0) & (nD0 - ((lb >> 16) | lm) < R);
+        const int wc = ch ? (wP >> 16) : (wP & 0xffff), ndc = ch ? nD1 : nD0;
+        const bool rW = kN1 ? wc < ndc : wc < ns * ndc;
+        const bool rdy = isF ? (ch ? rF1 : rF0) : (isW ? rW : (ch ? rD1 : rD0));
+        const bool go = (pos < plen) & rdy;
+        const bool right = tb.w != 0;                   // F0, D1 go right; F1, D0 go left
+        // the entry's own count of its stream addresses both its input slot and its message slot
+        const int cnt = ((right ? aP : bP) >> (isF ? 0 : 16)) & 0xffff;
+        const int start = wmx(clk, smem[tb.x + ((cnt & tb.y) << 5)]);
+        int dur = ta.x, dm = ta.y;
+        if (!kN1) {                                     // W sub-block k of its W block (Q12)
+          const int k = wc % ns;
+          dur = isW ? wq + (k < wr ? 1 : 0) : dur;
+          dm = isW ? (k == ns - 1 ? mw : 0) : dm;
+        }
+        const int end = start + dur;
+        const int nl = wmx(end, right ? lkR : lkL) + ta.z;   // FIFO link clock (App. X1)
+        if (go & (tb.z != 0)) smem[tb.z + ((cnt & Rm) << 5)] = nl + ta.w;
+        if (A.t_start && go && pos < A.len_stride)
+          A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
+        const int gi = go ? 1 : 0;
+        clk = wmadd(gi, end - clk, clk);
+        mem = wmadd(gi, dm, mem);
+        peak = wmx(peak, mem);
+        const int gR = (go & !isW & right) ? 1 : 0, gL = (go & !isW & !right) ? 1 : 0;
+        lkR = wmadd(gR, nl - lkR, lkR);
+        lkL = wmadd(gL, nl - lkL, lkL);
+        // count increments: F0 +1 / D1 +65536 into aP, F1 +1 / D0 +65536 into bP, W into wP
+        const int inc = isF ? 1 : 65536;
+        aP = wmadd(gR, inc, aP);
+        bP = wmadd(gL, inc, bP);
+        wP = wmadd((go & isW) ? 1 : 0, ch ? 65536 : 1, wP);
+        pos = wmadd(gi, 1, pos);
+        __syncwarp();
+        if (!__any_sync(WFULL, go)) break;
+      }
+    };
+    if (ns == 1) rounds(std::true_type{});
+    else rounds(std::false_type{});
     const int nF0 = aP & 0xffff, nD1 = aP >> 16, nF1 = bP & 0xffff, nD0 = bP >> 16;
     // no lane progressed: complete, a cyclic wait on full rings (-> second pass), or deadlock
     const int lb = __shfl_up_sync(WFULL, bP, 1), ra = __shfl_down_sync(WFULL, aP, 1);
