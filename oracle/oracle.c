@@ -425,6 +425,153 @@ int32_t or_simulate_wave(const or_inst* I, const int8_t* codes, const int32_t* l
   return R->status;
 }
 
+/* Loop pattern (fig:pptravesal :226-234; SPEC patterns module "Loop"; reading Q33), 2 chunks.
+ * Per microbatch j:  F(0,s) -> F(0,s+1);  F(0,p-1) -> F(1,0) over the wrap link p-1 -> 0;
+ *   F(1,s) -> F(1,s+1);  F(1,p-1) -> D(1,p-1) (loss);  D(1,s) -> D(1,s-1);
+ *   D(1,0) -> D(0,p-1) over the wrap link 0 -> p-1;  D(0,s) -> D(0,s-1);  D(c,s) -> W(c,s).
+ * Link s -> s+1 carries F(0), F(1) of stage s; link s+1 -> s carries D(0), D(1) of stage s+1; the
+ * wrap links carry F(0) of stage p-1 and D(1) of stage 0: one producer per directed link (the
+ * paper's alpha/beta are per device pair, :381), so App. X1's FIFO = first-fit still holds. */
+int32_t or_simulate_loop(const or_inst* I, const int8_t* codes, const int32_t* len, int32_t maxlen,
+                         or_result* R, int64_t* t_start) {
+  const int p = I->p, m = I->m, ns = I->n_sub;
+  memset(R, 0, sizeof(*R));
+  R->makespan = -1; R->peak_mem = -1;
+  int32_t st = or_validate_instance(I);
+  if (st) { R->status = st; return st; }
+  if (I->lat_f[p - 1] < 0 || I->bw_f[p - 1] < 0 || I->lat_b[p - 1] < 0 || I->bw_b[p - 1] < 0) {
+    R->status = OR_ST_BAD_INSTANCE;                           /* wrap link delays */
+    return R->status;
+  }
+  st = or_check_plan_wave(I, codes, len, maxlen);
+  if (st) { R->status = st; return st; }
+  int64_t off[OR_MAXP + 1]; off[0] = 0;
+  for (int s = 0; s < p; ++s) off[s + 1] = off[s] + len[s];
+  const int64_t NC = off[p];
+  const int64_t N = NC + 2 * p;              /* AG(s) = NC + s, AR(s) = NC + p + s */
+  int32_t* n_type  = (int32_t*)calloc(N, sizeof(int32_t));
+  int32_t* n_sub   = (int32_t*)calloc(N, sizeof(int32_t));
+  int64_t* dur     = (int64_t*)calloc(N, sizeof(int64_t));
+  int64_t* ready   = (int64_t*)calloc(N, sizeof(int64_t));
+  int64_t* start   = (int64_t*)calloc(N, sizeof(int64_t));
+  int64_t* end     = (int64_t*)calloc(N, sizeof(int64_t));
+  int32_t* indeg   = (int32_t*)calloc(N, sizeof(int32_t));
+  int32_t* ecount  = (int32_t*)calloc(N, sizeof(int32_t));
+  or_edge** out    = (or_edge**)calloc(N, sizeof(or_edge*));
+  int32_t* ecap    = (int32_t*)calloc(N, sizeof(int32_t));
+  /* [chunk][stage][mb] node index of F, of D (or B); W sub-blocks listed per (chunk, stage, mb) */
+  const int64_t PM = (int64_t)p * m;
+  int64_t* idxF = (int64_t*)malloc(sizeof(int64_t) * 2 * PM);
+  int64_t* idxD = (int64_t*)malloc(sizeof(int64_t) * 2 * PM);
+  int64_t* wkey = (int64_t*)malloc(sizeof(int64_t) * (NC + 1));  /* W entry -> (chunk, stage, mb) key */
+  int64_t* queue = (int64_t*)malloc(sizeof(int64_t) * N);
+  /* boundary s = link s -> (s+1) mod p (*_f) and its reverse (*_b); index p-1 is the wrap link */
+  or_link* linkR = (or_link*)malloc(sizeof(or_link) * p);
+  or_link* linkL = (or_link*)malloc(sizeof(or_link) * p);
+  for (int s = 0; s < p; ++s) { or_link_init(&linkR[s]); or_link_init(&linkL[s]); }
+#define ADD_EDGE(u, v, k, l) do { \
+    if (ecount[u] == ecap[u]) { ecap[u] = ecap[u] ? 2 * ecap[u] : 4; \
+      out[u] = (or_edge*)realloc(out[u], sizeof(or_edge) * ecap[u]); } \
+    out[u][ecount[u]].to = (int32_t)(v); out[u][ecount[u]].kind = (k); out[u][ecount[u]].link = (l); \
+    ecount[u]++; indeg[v]++; } while (0)
+#define KEY(ch, s, j) ((int64_t)(ch) * PM + (int64_t)(s) * m + (j))
+  {
+    for (int s = 0; s < p; ++s) {
+      int32_t cF[2] = {0, 0}, cD[2] = {0, 0}, cW[2] = {0, 0};
+      for (int k = 0; k < len[s]; ++k) {
+        int64_t u = off[s] + k;
+        int x = codes[(int64_t)s * maxlen + k], c = WV_CODE(x), ch = WV_CHUNK(x);
+        n_type[u] = x;
+        if (c == OR_F) { dur[u] = I->t_f[s]; idxF[KEY(ch, s, cF[ch])] = u; cF[ch]++; }
+        else if (c == OR_B) { dur[u] = I->t_d[s] + I->t_w[s]; idxD[KEY(ch, s, cD[ch])] = u; cD[ch]++; }
+        else if (c == OR_D) { dur[u] = I->t_d[s]; idxD[KEY(ch, s, cD[ch])] = u; cD[ch]++; }
+        else {
+          int32_t j = cW[ch] / ns, q = cW[ch] % ns;
+          n_sub[u] = q; dur[u] = sub_dur(I->t_w[s], ns, q); cW[ch]++;
+          wkey[u] = KEY(ch, s, j);
+        }
+      }
+    }
+  }
+  for (int64_t s = 0; s < p; ++s) {
+    n_type[NC + s] = -1; dur[NC + s] = I->zero1 ? I->t_ag[s] : 0;
+    n_type[NC + p + s] = -2; dur[NC + p + s] = I->t_dp[s];
+  }
+  for (int s = 0; s < p; ++s)                                   /* schedule dependencies */
+    for (int k = 0; k + 1 < len[s]; ++k) ADD_EDGE(off[s] + k, off[s] + k + 1, EK_SCHED, -1);
+  for (int s = 0; s < p; ++s) {
+    for (int j = 0; j < m; ++j) {
+      const int64_t f0 = idxF[KEY(0, s, j)], f1 = idxF[KEY(1, s, j)];
+      const int64_t d0 = idxD[KEY(0, s, j)], d1 = idxD[KEY(1, s, j)];
+      if (s < p - 1) ADD_EDGE(f0, idxF[KEY(0, s + 1, j)], EK_LINK_F, s);   /* chunk 0 forward */
+      else ADD_EDGE(f0, idxF[KEY(1, 0, j)], EK_LINK_F, p - 1);            /* wrap p-1 -> 0 */
+      if (s < p - 1) ADD_EDGE(f1, idxF[KEY(1, s + 1, j)], EK_LINK_F, s);   /* chunk 1 forward */
+      else ADD_EDGE(f1, d1, EK_LOCAL, -1);                              /* loss */
+      if (s > 0) ADD_EDGE(d1, idxD[KEY(1, s - 1, j)], EK_LINK_B, s - 1); /* chunk 1 backward */
+      else ADD_EDGE(d1, idxD[KEY(0, p - 1, j)], EK_LINK_B, p - 1);       /* wrap 0 -> p-1 */
+      if (s > 0) ADD_EDGE(d0, idxD[KEY(0, s - 1, j)], EK_LINK_B, s - 1); /* chunk 0 backward */
+    }
+    for (int k = 0; k < len[s]; ++k)                                      /* W sub-block after its D */
+      if (WV_CODE(n_type[off[s] + k]) == OR_W) ADD_EDGE(idxD[wkey[off[s] + k]], off[s] + k, EK_LOCAL, -1);
+    ADD_EDGE(NC + s, idxF[KEY(0, s, 0)], EK_LOCAL, -1);        /* ZeRO-1 AG before chunk 0's first F */
+    ADD_EDGE(NC + s, idxF[KEY(1, s, 0)], EK_LOCAL, -1);        /* ... and chunk 1's */
+    ADD_EDGE(off[s] + len[s] - 1, NC + p + s, EK_LOCAL, -1);    /* DP AR after the stage's last block */
+  }
+  int64_t qh = 0, qt = 0, done = 0;
+  for (int64_t u = 0; u < N; ++u) if (indeg[u] == 0) queue[qt++] = u;
+  while (qh < qt) {
+    int64_t u = queue[qh++];
+    start[u] = ready[u];
+    end[u] = start[u] + dur[u];
+    done++;
+    for (int32_t e = 0; e < ecount[u]; ++e) {
+      or_edge E = out[u][e];
+      int64_t c;
+      if (E.kind == EK_LINK_F)      c = or_reserve_window(&linkR[E.link], end[u], I->bw_f[E.link]) + I->lat_f[E.link];
+      else if (E.kind == EK_LINK_B) c = or_reserve_window(&linkL[E.link], end[u], I->bw_b[E.link]) + I->lat_b[E.link];
+      else                          c = end[u];
+      ready[E.to] = max64(ready[E.to], c);
+      if (--indeg[E.to] == 0) queue[qt++] = E.to;
+    }
+  }
+  if (done < N) {
+    R->status = OR_ST_DEADLOCK;
+  } else {
+    int64_t mk = 0, pk = 0;
+    for (int s = 0; s < p; ++s) {
+      int64_t mem = 0, peak = 0, busy = 0;
+      for (int k = 0; k < len[s]; ++k) {
+        int64_t u = off[s] + k;
+        int c = WV_CODE(n_type[u]);
+        if (c == OR_F) mem += I->m_f[s];
+        else if (c == OR_D) mem += I->m_d[s];
+        else if (c == OR_B) mem += I->m_d[s] + I->m_w[s];
+        else if (n_sub[u] == ns - 1) mem += I->m_w[s];
+        peak = max64(peak, mem);
+        busy += dur[u];
+        if (t_start) t_start[(int64_t)s * maxlen + k] = start[u];
+      }
+      R->first_start[s] = start[off[s]];
+      R->last_end[s] = end[off[s] + len[s] - 1];
+      R->busy[s] = busy;
+      R->peak[s] = peak;
+      if (peak > I->m_lim[s]) R->status |= OR_ST_MEM_EXCEEDED;
+      pk = max64(pk, peak);
+    }
+    for (int64_t u = 0; u < N; ++u) mk = max64(mk, end[u]);
+    R->makespan = mk;
+    R->peak_mem = pk;
+  }
+  for (int s = 0; s < p; ++s) { or_link_free(&linkR[s]); or_link_free(&linkL[s]); }
+  for (int64_t u = 0; u < N; ++u) free(out[u]);
+  free(n_type); free(n_sub); free(dur); free(ready); free(start); free(end); free(indeg); free(ecount);
+  free(out); free(ecap); free(idxF); free(idxD); free(wkey); free(queue);
+  free(linkR); free(linkL);
+#undef KEY
+#undef ADD_EDGE
+  return R->status;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Algorithm 1 with the §4.2.2 scheduling loop (:415-432).
  * Each stage keeps an explicit list of schedulable operations with T_avail.

@@ -95,6 +95,12 @@ int32_t or_check_plan_wave(const or_inst* I, const int8_t* codes, const int32_t*
 int32_t or_simulate_wave(const or_inst* I, const int8_t* codes, const int32_t* len, int32_t maxlen,
                          or_result* R, int64_t* t_start);
 
+/* Loop traversal pattern (reading Q33): 2 model chunks, chunk 1 starts on stage 0 where chunk 0
+ * left stage p-1, over the wrap-around link (boundary index p-1: lat_f/bw_f[p-1] is p-1 -> 0,
+ * lat_b/bw_b[p-1] is 0 -> p-1).  Plan entries and checks as for Wave.                     */
+int32_t or_simulate_loop(const or_inst* I, const int8_t* codes, const int32_t* len, int32_t maxlen,
+                         or_result* R, int64_t* t_start);
+
 /* Alg. 1 greedy CrossUD(Sub).  Writes plan (codes/len) and timeline; returns status. */
 int32_t or_greedy(const or_inst* I, int8_t* codes, int32_t* len, int32_t maxlen,
                   or_result* R, int64_t* t_start);

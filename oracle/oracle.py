@@ -77,7 +77,7 @@ def lib():
         L.or_reserve_window.argtypes = [P(OrLink), C.c_int64, C.c_int64]
         L.or_link_init.argtypes = [P(OrLink)]
         L.or_link_free.argtypes = [P(OrLink)]
-        for fn in ("or_simulate", "or_greedy", "or_simulate_wave"):
+        for fn in ("or_simulate", "or_greedy", "or_simulate_wave", "or_simulate_loop"):
             f = getattr(L, fn)
             f.restype = C.c_int32
             f.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32, P(OrResult), P(C.c_int64)]
@@ -156,6 +156,22 @@ def simulate_wave(d, codes, lens=None, timeline=False) -> dict:
     inst, res = to_or_inst(d), OrResult()
     ts = np.zeros((p, maxlen), dtype=np.int64) if timeline else None
     L.or_simulate_wave(C.byref(inst), c.ctypes.data_as(C.POINTER(C.c_int8)), ln.ctypes.data_as(C.POINTER(C.c_int32)),
+                       maxlen, C.byref(res), ts.ctypes.data_as(C.POINTER(C.c_int64)) if timeline else None)
+    out = _result(res, p)
+    if timeline:
+        out["t_start"] = ts
+    return out
+
+
+def simulate_loop(d, codes, lens=None, timeline=False) -> dict:
+    """Loop-pattern plan, 2 chunks (entries type | chunk << 2), reading Q33; boundary index p-1 of
+    lat_f/bw_f (p-1 -> 0) and lat_b/bw_b (0 -> p-1) is the wrap link."""
+    L = lib()
+    p = int(d["p"])
+    c, ln, maxlen = _codes_arr(codes, lens, p)
+    inst, res = to_or_inst(d), OrResult()
+    ts = np.zeros((p, maxlen), dtype=np.int64) if timeline else None
+    L.or_simulate_loop(C.byref(inst), c.ctypes.data_as(C.POINTER(C.c_int8)), ln.ctypes.data_as(C.POINTER(C.c_int32)),
                        maxlen, C.byref(res), ts.ctypes.data_as(C.POINTER(C.c_int64)) if timeline else None)
     out = _result(res, p)
     if timeline:
@@ -300,5 +316,5 @@ def grid_instance(g, k: int, G=None) -> dict:
     for k2 in ("t_f", "t_d", "t_w", "m_f", "m_d", "m_w", "m_lim", "t_dp", "t_ag"):
         d[k2] = np.array(getattr(o, k2)[:o.p])
     for k2 in ("lat_f", "bw_f", "lat_b", "bw_b"):
-        d[k2] = np.array(getattr(o, k2)[:max(o.p - 1, 0)])
+        d[k2] = np.array(getattr(o, k2)[:o.p])          # index p-1: the (unused) wrap link, 0
     return d

@@ -209,6 +209,100 @@ def fp_simulate_wave(d, codes):
     return {"deadlock": True, "makespan": -1, "start": st}
 
 
+def fp_simulate_loop(d, codes):
+    """Loop pattern, 2 chunks (reading Q33), as the least fixed point of the §3.5 equations.
+
+    Per microbatch: F0 runs s -> s+1 and wraps p-1 -> 0 into F1; F1 runs s -> s+1; the loss on the
+    last stage starts D1; D1 runs s -> s-1 and wraps 0 -> p-1 into D0; D0 runs s -> s-1; W after the
+    D of its chunk.  Stage s sends right (its link s -> s+1, or the wrap p-1 -> 0 with boundary
+    index p-1) and left (s -> s-1, or the wrap 0 -> p-1 with index p-1), one FIFO clock each.
+    """
+    p, m, ns = d["p"], d["m"], d["n_sub"]
+    ops = []
+    for s in range(p):
+        cF, cD, cW = [0, 0], [0, 0], [0, 0]
+        row = []
+        for x in codes[s]:
+            t, c = int(x) & 3, (int(x) >> 2) & 1
+            if t == F:
+                row.append((F, c, cF[c], 0)); cF[c] += 1
+            elif t in (B, D):
+                row.append((t, c, cD[c], 0)); cD[c] += 1
+            else:
+                row.append((W, c, cW[c] // ns, cW[c] % ns)); cW[c] += 1
+        ops.append(row)
+    pos = [{(t if t != B else D, c, j, q): k for k, (t, c, j, q) in enumerate(ops[s])} for s in range(p)]
+    st = [[0] * len(ops[s]) for s in range(p)]
+    horizon = 1
+    for s in range(p):
+        horizon += sum(_dur(d, s, t, q) for (t, c, j, q) in ops[s]) + int(d["t_ag"][s])
+        horizon += 2 * m * int(d["lat_f"][s] + d["bw_f"][s] + d["lat_b"][s] + d["bw_b"][s])
+
+    def link(end_s, s, right):
+        if right:
+            b = s                                        # s -> s+1, or the wrap p-1 -> 0
+            bw, lat = int(d["bw_f"][b]), int(d["lat_f"][b])
+        else:
+            b = s - 1 if s > 0 else p - 1                # s -> s-1, or the wrap 0 -> p-1
+            bw, lat = int(d["bw_b"][b]), int(d["lat_b"][b])
+        clk, arr = None, {}
+        for k, (t, c, j, q) in enumerate(ops[s]):
+            if t == W:
+                continue
+            if right != (t == F):
+                continue
+            if right and s == p - 1 and c == 1:          # the last stage's F1 feeds its own D1
+                continue
+            if not right and s == 0 and c == 0:          # stage 0's D0 ends the chain
+                continue
+            r = end_s[k]
+            ws = r if (bw == 0 or clk is None) else max(r, clk)
+            if bw > 0:
+                clk = ws + bw
+            arr[(F if t == F else D, c, j)] = ws + bw + lat
+        return arr
+
+    for _ in range(20 * sum(len(o) for o in ops) + 10):
+        end = [[st[s][k] + _dur(d, s, ops[s][k][0], ops[s][k][3]) for k in range(len(ops[s]))] for s in range(p)]
+        right = [link(end[s], s, True) for s in range(p)]
+        left = [link(end[s], s, False) for s in range(p)]
+        changed = False
+        for s in range(p):
+            for k, (t, c, j, q) in enumerate(ops[s]):
+                v = end[s][k - 1] if k > 0 else 0
+                own = lambda key: end[s][pos[s][key]]
+                if t == F:
+                    if s > 0:
+                        v = max(v, right[s - 1][(F, c, j)])
+                    elif c == 1:
+                        v = max(v, right[p - 1][(F, 0, j)])          # wrap p-1 -> 0
+                    if d["zero1"]:
+                        v = max(v, int(d["t_ag"][s]))
+                elif t in (B, D):
+                    if s < p - 1:
+                        v = max(v, left[s + 1][(D, c, j)])
+                    elif c == 1:
+                        v = max(v, own((F, 1, j, 0)))                 # loss
+                    else:
+                        v = max(v, left[0][(D, 1, j)])                # wrap 0 -> p-1
+                else:
+                    v = max(v, own((D, c, j, 0)))
+                if v != st[s][k]:
+                    st[s][k] = v
+                    changed = True
+                if v > horizon:
+                    return {"deadlock": True, "makespan": -1, "start": st}
+        if not changed:
+            mk = 0
+            for s in range(p):
+                le = end[s][-1]
+                mk = max(mk, le, le + int(d["t_dp"][s]))
+                if d["zero1"]:
+                    mk = max(mk, int(d["t_ag"][s]))
+            return {"deadlock": False, "makespan": mk, "start": st}
+    return {"deadlock": True, "makespan": -1, "start": st}
+
+
 def random_valid_plan(d, rng, p_w_first=0.3):
     """Random split plan (n_sub as in d) by a combinatorial random token game:
     uniformly pick a stage with an executable op (inputs produced, memory fits),

@@ -512,3 +512,60 @@ def test_wave_plan_rules_and_deadlock(oracle_lib):
     cyc = [r[:] for r in good]
     cyc[2] = [F | 4, F, F, F | 4, D | 4, D | 4, D, D, W | 4, W | 4, W, W]
     assert oracle_lib.simulate_wave(d, cyc)["status"] == 1
+
+
+# --------------------------------------------------------------------------- Loop pattern (reading Q33)
+def test_loop_equals_fixed_point_formulation(oracle_lib):
+    """The oracle's Loop DAG simulation == the least fixed point of the §3.5 equations over the Loop
+    data flow with FIFO links including the two wrap-around links (helpers_independent.
+    fp_simulate_loop), start tick by start tick, on random valid plans."""
+    from tests.helpers_independent import fp_simulate_loop
+    from workloads.wave import random_loop_plan
+    rng = np.random.default_rng(330)
+    for _ in range(150):
+        b = K.random_instances(1, seed=int(rng.integers(1 << 30)), max_p=6, max_m=5, intra_delay=True)
+        for fld in ("lat_f", "bw_f", "lat_b", "bw_b"):                 # the wrap link, boundary p-1
+            getattr(b, fld)[0, b.p[0] - 1] = int(rng.integers(0, 200)) if rng.random() < 0.7 else 0
+        d = b.item(0)
+        rows = random_loop_plan(d["p"], d["m"], d["n_sub"], rng, combined=bool(rng.random() < 0.25))
+        r = oracle_lib.simulate_loop(d, rows, timeline=True)
+        f = fp_simulate_loop(d, rows)
+        assert r["status"] & ~2 == 0 and r["makespan"] == f["makespan"]
+        for s in range(d["p"]):
+            assert list(r["t_start"][s][:len(rows[s])]) == f["start"][s]
+
+
+def test_loop_single_microbatch_six_crossings(oracle_lib):
+    """One microbatch, every stage F0 F1 D1 D0 W1 W0: F0 out, wrap, F1 out, D1 back, wrap, D0 back.
+    Every inner boundary is crossed four times and the wrap link twice, so with 2 DCs a microbatch
+    makes 6 cross-DC transfers ("6 per microbatch" for Loop): makespan =
+    2p(t_f + t_d) + 2 t_w + 2 sum_{b<p-1}(lat_f + bw_f + lat_b + bw_b) + (wrap lat + bw both ways)."""
+    rng = np.random.default_rng(331)
+    for _ in range(60):
+        p, n_dc = int(rng.integers(1, 9)), int(rng.integers(1, 5))
+        f, dd_, w = (int(x) for x in rng.integers(1, 100, size=3))
+        lat, bw, latb, bwb = (int(x) for x in rng.integers(0, 80, size=4))
+        b = K.uniform_instance(p, 1, n_dc, f, dd_, w, lat=lat, bw=bw, lat_b=latb, bw_b=bwb, mlim_x1000=10**6)
+        wrap = [int(x) for x in rng.integers(0, 90, size=4)]
+        b.lat_f[0, p - 1], b.bw_f[0, p - 1], b.lat_b[0, p - 1], b.bw_b[0, p - 1] = wrap
+        d = b.item(0)
+        rows = [[F, F | 4, D | 4, D, W | 4, W] for _ in range(p)]
+        r = oracle_lib.simulate_loop(d, rows)
+        inner = sum(int(d["lat_f"][s] + d["bw_f"][s] + d["lat_b"][s] + d["bw_b"][s]) for s in range(p - 1))
+        assert r["status"] == 0 and r["makespan"] == 2 * p * (f + dd_) + 2 * w + 2 * inner + sum(wrap)
+        if n_dc == 2 and p >= 2:
+            crossings = 2 * int(np.count_nonzero(d["lat_f"][:p - 1])) + 2 * int(np.count_nonzero(d["lat_b"][:p - 1])) + 2
+            assert lat == 0 or latb == 0 or crossings == 6
+
+
+def test_loop_deadlock_and_wrap_validation(oracle_lib):
+    """F1 before F0 on stage 0 closes a cycle through the wrap link (DEADLOCK); a negative wrap delay
+    is an invalid instance."""
+    d = inst(3, 1, 1, 5, 5, 5, mlim_x1000=10**6)
+    good = [[F, F | 4, D | 4, D, W | 4, W] for _ in range(3)]
+    assert oracle_lib.simulate_loop(d, good)["status"] == 0
+    cyc = [r[:] for r in good]
+    cyc[0] = [F | 4, F, D | 4, D, W | 4, W]
+    assert oracle_lib.simulate_loop(d, cyc)["status"] == 1
+    d["lat_b"] = np.array([0, 0, -1])
+    assert oracle_lib.simulate_loop(d, good)["status"] == 8

@@ -75,8 +75,8 @@ class InstanceBatch:
         d = {"p": p, "m": int(self.m[i]), "n_sub": int(self.n_sub[i]), "zero1": int(self.zero1[i])}
         for k in _STAGE_FIELDS:
             d[k] = getattr(self, k)[i, :p].copy()
-        for k in _BOUNDARY_FIELDS:
-            d[k] = getattr(self, k)[i, :max(p - 1, 0)].copy()
+        for k in _BOUNDARY_FIELDS:       # boundary s = link s -> s+1 (s < p-1); index p-1: Loop's wrap link
+            d[k] = getattr(self, k)[i, :p].copy()
         return d
 
     @staticmethod

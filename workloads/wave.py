@@ -1,4 +1,5 @@
-"""Wave-pattern plans (NEXT 1, reading Q32): random valid plans and the 4-bit packed layout.
+"""Multi-chunk plans (NEXT 1): Wave (reading Q32) and Loop (Q33) random valid plans and the 4-bit
+packed layout.
 
 Input generation only.  A plan gives every stage an ordered list of entries `type | chunk << 2`
 (type F=0, B=1, D=2, W=3 as in the UD layout; chunk 0 or 1).  The packed layout holds 8 entries
@@ -33,6 +34,52 @@ def random_wave_plan(p: int, m: int, n_sub: int = 1, rng=None, combined: bool = 
         if nD[1, s] < m and ((nF[1, s] > nD[1, s]) if s == 0 else (nD[1, s - 1] > nD[1, s])):
             r.append((B if combined else D, 1))
         if nD[0, s] < m and ((nD[1, s] > nD[0, s]) if s == p - 1 else (nD[0, s + 1] > nD[0, s])):
+            r.append((B if combined else D, 0))
+        if not combined:
+            for c in (0, 1):
+                if nW[c, s] < n_sub * nD[c, s]:
+                    r.append((W, c))
+        return r
+
+    while done < total:
+        cand = [(s, ready(s)) for s in range(p)]
+        cand = [(s, r) for s, r in cand if r]
+        s, r = cand[int(rng.integers(len(cand)))]
+        ws = [x for x in r if x[0] == W]
+        if ws and rng.random() < w_bias:
+            t, c = ws[int(rng.integers(len(ws)))]
+        else:
+            t, c = r[int(rng.integers(len(r)))]
+        rows[s].append(t | (c << 2))
+        if t == F:
+            nF[c, s] += 1
+        elif t == W:
+            nW[c, s] += 1
+        else:
+            nD[c, s] += 1
+        done += 1
+    return rows
+
+
+def random_loop_plan(p: int, m: int, n_sub: int = 1, rng=None, combined: bool = False, w_bias: float = 0.3):
+    """One random valid Loop plan (reading Q33, 2 chunks) -> list (per stage) of entry codes."""
+    rng = rng or np.random.default_rng()
+    nF = np.zeros((2, p), np.int64)
+    nD = np.zeros((2, p), np.int64)
+    nW = np.zeros((2, p), np.int64)
+    rows = [[] for _ in range(p)]
+    total = p * 2 * m * (2 if combined else 2 + n_sub)
+    done = 0
+
+    def ready(s):
+        r = []
+        if nF[0, s] < m and (s == 0 or nF[0, s - 1] > nF[0, s]):
+            r.append((F, 0))
+        if nF[1, s] < m and ((nF[0, p - 1] > nF[1, s]) if s == 0 else (nF[1, s - 1] > nF[1, s])):
+            r.append((F, 1))
+        if nD[1, s] < m and ((nF[1, s] > nD[1, s]) if s == p - 1 else (nD[1, s + 1] > nD[1, s])):
+            r.append((B if combined else D, 1))
+        if nD[0, s] < m and ((nD[1, 0] > nD[0, s]) if s == p - 1 else (nD[0, s + 1] > nD[0, s])):
             r.append((B if combined else D, 0))
         if not combined:
             for c in (0, 1):
