@@ -49,6 +49,11 @@ extern "C" {
 #define CP_OP_D 2u            /* input-gradient block (DGrad) */
 #define CP_OP_W 3u            /* ONE weight-gradient sub-block (n_sub per W block) */
 
+/* traversal patterns of cp_schedules.pattern */
+#define CP_PATTERN_UD 0
+#define CP_PATTERN_WAVE 1
+#define CP_PATTERN_LOOP 2
+
 /* static plan families (cp_build_static kind; equal to their sweep candidate ids) */
 #define CP_PLAN_GPIPE 0       /* F x m, then B x m (reading Q22) */
 #define CP_PLAN_1F1B 1        /* PipeDream-Flush, combined B, warm-up min(p-s-1, m) (Q23) */
@@ -102,10 +107,13 @@ typedef struct {
 typedef struct {
   int32_t n;                  /* number of schedules */
   int32_t stage_stride;       /* >= max_pp */
-  int32_t words;              /* words per stage row: capacity 16*words entries (8*words if entry_bits 4) */
-  int32_t entry_bits;         /* 0 or 2: UD plans, 2-bit entries (above).  4 (cp_simulate only): Wave plans
-                                 (reading Q32), 4-bit entries type | chunk << 2, 8 per word LSB-first, same
-                                 [n][words][stage_stride] order; needs max_pp <= 32 and max_mb <= 256 */
+  int32_t words;              /* words per stage row: capacity 16*words entries (8*words if pattern > 0) */
+  int32_t pattern;            /* traversal pattern (fig:pptravesal) of the plans, cp_simulate only:
+                                 CP_PATTERN_UD (0): 2-bit entries (above);
+                                 CP_PATTERN_WAVE (1, reading Q32) and CP_PATTERN_LOOP (2, Q33): two model
+                                 chunks per stage, 4-bit entries type | chunk << 2, 8 per word LSB-first,
+                                 same [n][words][stage_stride] order; need max_pp <= 32, max_mb <= 256.
+                                 Loop reads its wrap links at boundary index p-1 (Q33). */
   const int32_t* inst_of;     /* [n] instance of schedule i; NULL: instance i (or 0 if instances.n == 1) */
   uint32_t* ops;              /* [n][words][stage_stride]; input of cp_simulate, output of cp_greedy */
   uint16_t* len;              /* [n][stage_stride] entries per stage row */

@@ -41,7 +41,7 @@ class CpInstances(C.Structure):
 
 
 class CpSchedules(C.Structure):
-    _fields_ = [("n", C.c_int32), ("stage_stride", C.c_int32), ("words", C.c_int32), ("entry_bits", C.c_int32),
+    _fields_ = [("n", C.c_int32), ("stage_stride", C.c_int32), ("words", C.c_int32), ("pattern", C.c_int32),
                 ("inst_of", C.c_void_p), ("ops", C.c_void_p), ("len", C.c_void_p)]
 
 

@@ -108,19 +108,20 @@ def _results(n, stage_stride, stats, timeline, len_stride, device, best):
 # ---------------------------------------------------------------------------------------- calls
 def simulate(inst: Instances, ops: torch.Tensor, lens: torch.Tensor, inst_of: torch.Tensor = None, *,
              stats=False, timeline=False, len_stride=None, best=False, ring=None, stream=None, ws=None,
-             out=None, wave=False):
+             out=None, wave=False, loop=False):
     """cp_simulate: evaluate ops.shape[0] fixed plans.  ops uint32-as-int32 [n, words, stride], lens int16 [n, stride].
-    wave=True: Wave-pattern plans (reading Q32), 4-bit entries type | chunk << 2, 8 per word."""
+    wave=True / loop=True: two-chunk Wave (reading Q32) / Loop (Q33) plans, 4-bit entries type | chunk << 2,
+    8 per word."""
     _require_cuda(ops, lens, inst_of)
     n, words, stride = ops.shape
     dev = ops.device
     d = inst.desc(ring)
     if out is None:
-        out = _results(n, stride, stats, timeline, len_stride or (8 if wave else 16) * words, dev, best)
+        out = _results(n, stride, stats, timeline, len_stride or (8 if (wave or loop) else 16) * words, dev, best)
     r, cres = out
     if ws is None:
         ws = _workspace(0, d, n, dev)
-    sc = L.CpSchedules(n, stride, words, 4 if wave else 2, _ptr(inst_of), ops.data_ptr(), lens.data_ptr())
+    sc = L.CpSchedules(n, stride, words, 2 if loop else (1 if wave else 0), _ptr(inst_of), ops.data_ptr(), lens.data_ptr())
     if best:
         r["best_key"].fill_(KEY_NONE)
     rc = L.load().cp_simulate(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(ws.data_ptr()), ws.numel(),

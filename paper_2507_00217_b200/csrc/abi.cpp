@@ -280,7 +280,7 @@ size_t cp_workspace_bytes(int32_t which, const void* desc, int64_t n_items) {
   return ws_sim_greedy(in, n_items);
 }
 
-// Wave plans (reading Q32): k_wave32, one item per warp.  A first pass with small occupancy-gated
+// Two-chunk plans, Wave (reading Q32) or Loop (Q33): k_chunk32, one item per warp.  A first pass with small occupancy-gated
 // rings; items that stall on a full ring are re-run by a second pass with rings of n_mb slots.
 int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* res, void* ws, size_t ws_bytes,
              void* stream) {
@@ -289,6 +289,7 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
   if (ws_bytes < ws_sim_greedy(in, n) || !ws) return CP_EWORKSPACE;
   cpk::Args a;
   std::memset(&a, 0, sizeof(a));
+  a.chunk_pattern = sc->pattern;
   a.inst = in->inst;
   a.inst_of = sc->inst_of;
   a.n_inst = in->n;
@@ -335,9 +336,9 @@ int32_t cp_simulate(const cp_instances* in, const cp_schedules* sc, const cp_res
   if (!sc || !res || sc->n < 0 || !sc->ops || !sc->len || !res->makespan || !res->status) return CP_EINVAL;
   if (sc->stage_stride < in->max_pp || sc->words < 1 || (res->t_start && res->len_stride < 1)) return CP_EINVAL;
   if (!sc->inst_of && in->n != 1 && in->n < sc->n) return CP_EINVAL;
-  if (sc->entry_bits != 0 && sc->entry_bits != 2 && sc->entry_bits != 4) return CP_EINVAL;
+  if (sc->pattern < CP_PATTERN_UD || sc->pattern > CP_PATTERN_LOOP) return CP_EINVAL;
   if (sc->n == 0) return CP_OK;
-  if (sc->entry_bits == 4) return run_wave(in, sc, res, ws, ws_bytes, stream);
+  if (sc->pattern != CP_PATTERN_UD) return run_wave(in, sc, res, ws, ws_bytes, stream);
   return run_engine(cpk::MODE_SIM, in, sc, res, ws, ws_bytes, stream);
 }
 

@@ -53,6 +53,7 @@ struct Args {
   // blocks [pt_lo, pt_hi) of blk_inner points, slice [own_lo, own_hi) of each (cp_sweep_shard_rank)
   int64_t blk_inner;
   int32_t own_lo, own_hi;
+  int32_t chunk_pattern;               // two-chunk plans: CP_PATTERN_WAVE or CP_PATTERN_LOOP
   cp_grid grid;
 };
 

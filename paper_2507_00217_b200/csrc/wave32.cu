@@ -32,7 +32,8 @@ __device__ __forceinline__ int wmadd(int g, int d, int x) {   // x + g*d on the 
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const __grid_constant__ Args A) {
+template <bool kLoop>
+__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const __grid_constant__ Args A) {
   extern __shared__ __align__(16) int32_t smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -67,8 +68,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
       tf = I->t_f[s]; td = I->t_d[s]; tw = I->t_w[s];
       mf = I->m_f[s]; md = I->m_d[s]; mw = I->m_w[s]; mlim = I->m_lim[s];
       tdp = I->t_dp[s]; tag = (I->flags & 1) ? I->t_ag[s] : 0;
-      if (s < p - 1) { latR = I->lat_f[s]; bwR = I->bw_f[s]; lat_b_s = I->lat_b[s]; bw_b_s = I->bw_b[s]; }
+      // boundary s = link s -> s+1; Loop also uses index p-1, the wrap links p-1 -> 0 / 0 -> p-1 (Q33)
+      if (s < p - 1 || kLoop) { latR = I->lat_f[s]; bwR = I->bw_f[s]; lat_b_s = I->lat_b[s]; bw_b_s = I->bw_b[s]; }
       if (s > 0) { latL = I->lat_b[s - 1]; bwL = I->bw_b[s - 1]; }
+      else if (kLoop) { latL = I->lat_b[p - 1]; bwL = I->bw_b[p - 1]; }
       if (s < A.stage_stride) plen = A.len[item * A.stage_stride + s];
     }
     bool bad = p < 1 || p > CP_MAX_STAGES || p > A.stage_stride || m < 1 || ns < 1;
@@ -124,47 +127,86 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
       __syncwarp();
       continue;
     }
-    const bool sendR = s < p - 1, sendL = s > 0 && s < p;
     const int wq = tw / ns, wr = tw % ns;
+    const bool first_s = s == 0, last = s == p - 1;
+    // streams F0, F1, D0, D1 (counts cF = nF0 | nF1 << 16, cD = nD0 | nD1 << 16).  Per stream: whether
+    // it has a producer in another lane (else the zero row: stage 0's F0 and the own turn-arounds /
+    // loss, all already behind the lane's clock), the consumer column of its messages (0: none), and
+    // which link clock carries them (1: lkR, the right / forward link).
+    //   Wave (Q32): F0, D1 go right, F1, D0 go left.
+    //   Loop (Q33): F0, F1 go forward (right, the last stage's F0 over the wrap into stage 0's F1),
+    //               D1, D0 go backward (left, stage 0's D1 over the wrap into the last stage's D0).
+    const int inF0 = s > 0, inF1 = kLoop ? 1 : !last, inD1 = kLoop ? !last : s > 0, inD0 = kLoop ? 1 : !last;
+    int oF0, oF1, oD0, oD1;
+    if (kLoop) {
+      oF0 = last ? iF1 - s : iF0 + 1;
+      oF1 = last ? 0 : iF1 + 1;
+      oD1 = first_s ? iD0 + (p - 1) : iD1 - 1;
+      oD0 = first_s ? 0 : iD0 - 1;
+    } else {
+      oF0 = last ? 0 : iF0 + 1;
+      oF1 = first_s ? 0 : iF1 - 1;
+      oD1 = last ? 0 : iD1 + 1;
+      oD0 = first_s ? 0 : iD0 - 1;
+    }
+    if (s >= p) oF0 = oF1 = oD0 = oD1 = 0;
     // parameter tables, entry x = type | chunk << 2:
     //   tabA[x] = {duration, memory delta, link bw, latency} (W: first sub-block / whole W if n_sub 1)
-    //   tabB[x] = {input ring column (zero row without a producer), slot mask, output column at the
-    //             consumer (0: no message), 1 if the message goes right}
+    //   tabB[x] = {input ring column (zero row without a producer), slot mask, consumer column (0: no
+    //             message), 1 if the message uses the lkR clock}
     {
-      const int hasL = s > 0, hasR = s < p - 1;
       const int tW = ns == 1 ? tw : wq, mW = ns == 1 ? mw : 0;
+      const int dF1 = kLoop ? 1 : 0, dD1 = kLoop ? 0 : 1;       // clock of F1 / D1 (F0: lkR, D0: lkL)
       tabA[0 * 32] = make_int4(tf, mf, bwR, latR);
       tabA[1 * 32] = make_int4(td + tw, md + mw, bwL, latL);
       tabA[2 * 32] = make_int4(td, md, bwL, latL);
       tabA[3 * 32] = make_int4(tW, mW, 0, 0);
-      tabA[4 * 32] = make_int4(tf, mf, bwL, latL);
-      tabA[5 * 32] = make_int4(td + tw, md + mw, bwR, latR);
-      tabA[6 * 32] = make_int4(td, md, bwR, latR);
+      tabA[4 * 32] = make_int4(tf, mf, dF1 ? bwR : bwL, dF1 ? latR : latL);
+      tabA[5 * 32] = make_int4(td + tw, md + mw, dD1 ? bwR : bwL, dD1 ? latR : latL);
+      tabA[6 * 32] = make_int4(td, md, dD1 ? bwR : bwL, dD1 ? latR : latL);
       tabA[7 * 32] = make_int4(tW, mW, 0, 0);
-      tabB[0 * 32] = make_int4(hasL ? iF0 : iZ, hasL ? Rm : 0, sendR ? iF0 + 1 : 0, 1);
-      tabB[1 * 32] = make_int4(hasR ? iD0 : iZ, hasR ? Rm : 0, sendL ? iD0 - 1 : 0, 0);
+      tabB[0 * 32] = make_int4(inF0 ? iF0 : iZ, inF0 ? Rm : 0, oF0, 1);
+      tabB[1 * 32] = make_int4(inD0 ? iD0 : iZ, inD0 ? Rm : 0, oD0, 0);
       tabB[2 * 32] = tabB[1 * 32];
       tabB[3 * 32] = make_int4(iZ, 0, 0, 0);
-      tabB[4 * 32] = make_int4(hasR ? iF1 : iZ, hasR ? Rm : 0, sendL ? iF1 - 1 : 0, 0);
-      tabB[5 * 32] = make_int4(hasL ? iD1 : iZ, hasL ? Rm : 0, sendR ? iD1 + 1 : 0, 1);
+      tabB[4 * 32] = make_int4(inF1 ? iF1 : iZ, inF1 ? Rm : 0, oF1, dF1);
+      tabB[5 * 32] = make_int4(inD1 ? iD1 : iZ, inD1 ? Rm : 0, oD1, dD1);
       tabB[6 * 32] = tabB[5 * 32];
       tabB[7 * 32] = tabB[3 * 32];
     }
     int clk = tag, mem = 0, peak = 0, pos = 0, lkR = 0, lkL = 0;
-    // packed counts: aP = nF0 | nD1 << 16 (streams sent right), bP = nF1 | nD0 << 16 (sent left),
-    // wP = W sub-blocks of chunk 0 | chunk 1 << 16
-    int aP = 0, bP = 0, wP = 0;
-    int lm = s == 0 ? 0xffff : 0, rm = s == p - 1 ? 0xffff : 0;      // no producer / no consumer
+    int cF = 0, cD = 0, wP = 0;                        // wP: W sub-blocks of chunk 0 | chunk 1 << 16
+    int lm = first_s ? 0xffff : 0, rm = last ? 0xffff : 0;      // no producer / no consumer
     asm("mov.b32 %0, %0;" : "+r"(lm));
     asm("mov.b32 %0, %0;" : "+r"(rm));
-    const bool last = s == p - 1, first_s = s == 0;
+    const int wsrc = first_s ? p - 1 : 0;              // Loop: the wrap partner lane
+    // producer count X and consumer count Y of every stream, from the neighbours' packed counts
+    struct XY { int xF0, yF0, xF1, yF1, xD0, yD0, xD1, yD1; };
+    auto neighbours = [&]() -> XY {
+      const int lF = __shfl_up_sync(WFULL, cF, 1), lD = __shfl_up_sync(WFULL, cD, 1);
+      const int rF = __shfl_down_sync(WFULL, cF, 1), rD = __shfl_down_sync(WFULL, cD, 1);
+      const int nF0 = cF & 0xffff, nF1 = cF >> 16, nD1 = cD >> 16;
+      XY q;
+      if (kLoop) {
+        const int wF = __shfl_sync(WFULL, cF, wsrc), wD = __shfl_sync(WFULL, cD, wsrc);
+        q.xF0 = (lF & 0xffff) | lm;               q.yF0 = last ? (wF >> 16) : (rF & 0xffff);
+        q.xF1 = first_s ? (wF & 0xffff) : (lF >> 16); q.yF1 = (rF >> 16) | rm;
+        q.xD1 = last ? nF1 : (rD >> 16);          q.yD1 = first_s ? (wD & 0xffff) : (lD >> 16);
+        q.xD0 = last ? (wD >> 16) : (rD & 0xffff); q.yD0 = (lD & 0xffff) | lm;
+      } else {
+        q.xF0 = (lF & 0xffff) | lm;               q.yF0 = (rF & 0xffff) | rm;
+        q.xF1 = last ? nF0 : (rF >> 16);          q.yF1 = (lF >> 16) | lm;
+        q.xD1 = first_s ? nF1 : (lD >> 16);       q.yD1 = (rD >> 16) | rm;
+        q.xD0 = last ? nD1 : (rD & 0xffff);       q.yD0 = (lD & 0xffff) | lm;
+      }
+      return q;
+    };
     __syncwarp();
     auto rounds = [&](auto n1) {
       constexpr bool kN1 = decltype(n1)::value;       // n_sub == 1: a W entry is a whole W block
       for (;;) {
-        const int la = __shfl_up_sync(WFULL, aP, 1), lb = __shfl_up_sync(WFULL, bP, 1);
-        const int ra = __shfl_down_sync(WFULL, aP, 1), rb = __shfl_down_sync(WFULL, bP, 1);
-        const int nF0 = aP & 0xffff, nD1 = aP >> 16, nF1 = bP & 0xffff, nD0 = bP >> 16;
+        const XY q = neighbours();
+        const int nF0 = cF & 0xffff, nF1 = cF >> 16, nD0 = cD & 0xffff, nD1 = cD >> 16;
         const uint32_t wv = (uint32_t)smem[iP + ((pos >> 3) << 5)];
         const uint32_t x = (wv >> ((pos & 7) << 2)) & 7u;
         const int4 ta = tabA[x << 5];
@@ -172,17 +214,17 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
         const int ch = (int)(x >> 2);
         const bool isF = (x & 3u) == CP_OP_F, isW = (x & 3u) == CP_OP_W;
         // readiness: input produced (or the own turn-around / loss), room in the consumer's ring
-        const bool rF0 = (((la & 0xffff) | lm) > nF0) & (nF0 - ((ra & 0xffff) | rm) < R);
-        const bool rD1 = ((first_s ? nF1 : (la >> 16)) > nD1) & (nD1 - ((ra >> 16) | rm) < R);
-        const bool rF1 = ((last ? nF0 : (rb & 0xffff)) > nF1) & (nF1 - ((lb & 0xffff) | lm) < R);
-        const bool rD0 = ((last ? nD1 : (rb >> 16)) > nD0) & (nD0 - ((lb >> 16) | lm) < R);
+        const bool rF0 = (q.xF0 > nF0) & (nF0 - q.yF0 < R);
+        const bool rF1 = (q.xF1 > nF1) & (nF1 - q.yF1 < R);
+        const bool rD1 = (q.xD1 > nD1) & (nD1 - q.yD1 < R);
+        const bool rD0 = (q.xD0 > nD0) & (nD0 - q.yD0 < R);
         const int wc = ch ? (wP >> 16) : (wP & 0xffff), ndc = ch ? nD1 : nD0;
         const bool rW = kN1 ? wc < ndc : wc < ns * ndc;
         const bool rdy = isF ? (ch ? rF1 : rF0) : (isW ? rW : (ch ? rD1 : rD0));
         const bool go = (pos < plen) & rdy;
-        const bool right = tb.w != 0;                   // F0, D1 go right; F1, D0 go left
+        const bool right = tb.w != 0;
         // the entry's own count of its stream addresses both its input slot and its message slot
-        const int cnt = ((right ? aP : bP) >> (isF ? 0 : 16)) & 0xffff;
+        const int cnt = ((isF ? cF : cD) >> (ch ? 16 : 0)) & 0xffff;
         const int start = wmx(clk, smem[tb.x + ((cnt & tb.y) << 5)]);
         int dur = ta.x, dm = ta.y;
         if (!kN1) {                                     // W sub-block k of its W block (Q12)
@@ -192,21 +234,23 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
         }
         const int end = start + dur;
         const int nl = wmx(end, right ? lkR : lkL) + ta.z;   // FIFO link clock (App. X1)
-        if (go & (tb.z != 0)) smem[tb.z + ((cnt & Rm) << 5)] = nl + ta.w;
+        if (go & (tb.z != 0)) smem[tb.z + ((cnt & Rm) << 5)] = nl + ta.w;   // (tb.z: consumer column, 0 = none)
         if (A.t_start && go && pos < A.len_stride)
           A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
         const int gi = go ? 1 : 0;
         clk = wmadd(gi, end - clk, clk);
         mem = wmadd(gi, dm, mem);
         peak = wmx(peak, mem);
-        const int gR = (go & !isW & right) ? 1 : 0, gL = (go & !isW & !right) ? 1 : 0;
+        // a link clock advances only with a message on it (Loop: stage 0's D0 and the last stage's F1
+        // send nothing, while the same clocks carry their wrap-around D1 / F0 messages)
+        const bool sent = go & (tb.z != 0);
+        const int gR = (sent & right) ? 1 : 0, gL = (sent & !right) ? 1 : 0;
         lkR = wmadd(gR, nl - lkR, lkR);
         lkL = wmadd(gL, nl - lkL, lkL);
-        // count increments: F0 +1 / D1 +65536 into aP, F1 +1 / D0 +65536 into bP, W into wP
-        const int inc = isF ? 1 : 65536;
-        aP = wmadd(gR, inc, aP);
-        bP = wmadd(gL, inc, bP);
-        wP = wmadd((go & isW) ? 1 : 0, ch ? 65536 : 1, wP);
+        const int inc = ch ? 65536 : 1;
+        cF = wmadd((go & isF) ? 1 : 0, inc, cF);
+        cD = wmadd((go & !isF & !isW) ? 1 : 0, inc, cD);
+        wP = wmadd((go & isW) ? 1 : 0, inc, wP);
         pos = wmadd(gi, 1, pos);
         __syncwarp();
         if (!__any_sync(WFULL, go)) break;
@@ -214,11 +258,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
     };
     if (ns == 1) rounds(std::true_type{});
     else rounds(std::false_type{});
-    const int nF0 = aP & 0xffff, nD1 = aP >> 16, nF1 = bP & 0xffff, nD0 = bP >> 16;
+    const int nF0 = cF & 0xffff, nF1 = cF >> 16, nD0 = cD & 0xffff, nD1 = cD >> 16;
     // no lane progressed: complete, a cyclic wait on full rings (-> second pass), or deadlock
-    const int lb = __shfl_up_sync(WFULL, bP, 1), ra = __shfl_down_sync(WFULL, aP, 1);
-    const bool ring_full = (sendR && (nF0 - (ra & 0xffff) >= R || nD1 - (ra >> 16) >= R)) ||
-                           (sendL && (nF1 - (lb & 0xffff) >= R || nD0 - (lb >> 16) >= R));
+    const XY q = neighbours();
+    const bool ring_full = (oF0 && nF0 - q.yF0 >= R) || (oF1 && nF1 - q.yF1 >= R) ||
+                           (oD1 && nD1 - q.yD1 >= R) || (oD0 && nD0 - q.yD0 >= R);
     const bool complete = !__any_sync(WFULL, s < p && pos < plen);
     // cannot continue: a W ahead of its D (prefix rule) reports BAD_PLAN -> scan the rest of the row
     bool badc = false;
@@ -274,7 +318,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_wave32(const _
 }
 
 int launch_wave32(const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  const void* fn = (const void*)k_wave32;
+  const void* fn = a.chunk_pattern == CP_PATTERN_LOOP ? (const void*)k_chunk32<true> : (const void*)k_chunk32<false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
@@ -284,7 +328,7 @@ int launch_wave32(const Args& a, int blocks, int threads, size_t smem, void* str
 }
 
 int wave32_blocks_per_sm(int threads, size_t smem) {
-  const void* fn = (const void*)k_wave32;
+  const void* fn = (const void*)k_chunk32<false>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;

@@ -613,3 +613,58 @@ def test_wave_bench_size_sampled(O):
     ok = r["status"] == 0
     best = int(r["best_key"][0])
     assert best >> 32 == int(r["makespan"][ok].min())
+
+
+# ------------------------------------------------------------------------------------- Loop pattern (NEXT 1)
+def _loop_batch(n, seed, max_p, max_m, combined_frac=0.25):
+    from workloads.wave import pack_wave_plans, random_loop_plan
+    rng = np.random.default_rng(seed)
+    batch = K.random_instances(n, seed=seed, max_p=max_p, max_m=max_m, intra_delay=True)
+    for i in range(n):                                   # wrap links p-1 -> 0 / 0 -> p-1 (boundary p-1)
+        p = int(batch.p[i])
+        for fld in ("lat_f", "bw_f", "lat_b", "bw_b"):
+            getattr(batch, fld)[i, p - 1] = int(rng.integers(0, 300)) if rng.random() < 0.7 else 0
+    plans = [random_loop_plan(int(batch.p[i]), int(batch.m[i]), int(batch.n_sub[i]), rng,
+                              combined=bool(rng.random() < combined_frac)) for i in range(n)]
+    ops, ln = pack_wave_plans(plans, stage_stride=32)
+    return batch, plans, ops, ln
+
+
+def check_loop(O, batch, plans, r, timeline):
+    for i, pl in enumerate(plans):
+        d = batch.item(i)
+        w = O.simulate_loop(d, pl, timeline=timeline)
+        p = d["p"]
+        assert int(r["status"][i]) == w["status"], (i, int(r["status"][i]), w["status"])
+        assert int(r["makespan"][i]) == w["makespan"], (i, int(r["makespan"][i]), w["makespan"])
+        assert int(r["peak_mem"][i]) == w["peak_mem"], i
+        if w["makespan"] >= 0:
+            ss = r["stage_stats"][i]
+            assert np.array_equal(ss[:p, 0], w["first_start"]) and np.array_equal(ss[:p, 1], w["last_end"]), i
+            assert np.array_equal(ss[:p, 2], w["busy"]) and np.array_equal(ss[:p, 3], w["peak"]), i
+            if timeline:
+                for s in range(p):
+                    L = len(pl[s])
+                    assert np.array_equal(r["t_start"][i][s, :L], w["t_start"][s, :L]), (i, s)
+
+
+@pytest.mark.parametrize("max_p,seed", [(32, 60), (8, 61), (2, 62)])
+def test_simulate_loop_random_plans(O, max_p, seed):
+    """Loop plans (reading Q33: wrap-around links at boundary p-1) through cp_simulate == the oracle's
+    Loop DAG: status, makespan, peak, per-stage stats and every start tick."""
+    batch, plans, ops, ln = _loop_batch(120, seed, max_p, 10)
+    o, l_ = plans_to_device(ops, ln)
+    r = to_host(cp.simulate(cp.Instances(batch), o, l_, stats=True, timeline=True, loop=True))
+    check_loop(O, batch, plans, r, timeline=True)
+
+
+def test_simulate_loop_ring_fixup(O):
+    """1-slot first-pass rings force the second pass for Loop plans without changing any result."""
+    batch, plans, ops, ln = _loop_batch(80, 63, 16, 12, combined_frac=0.0)
+    inst = cp.Instances(batch)
+    o, l_ = plans_to_device(ops, ln)
+    ref = to_host(cp.simulate(inst, o, l_, stats=True, loop=True))
+    small = to_host(cp.simulate(inst, o, l_, stats=True, loop=True, ring=1))
+    for k in ("status", "makespan", "peak_mem", "stage_stats"):
+        assert np.array_equal(ref[k], small[k]), k
+    check_loop(O, batch, plans, ref, timeline=False)
