@@ -312,30 +312,37 @@ def run_ours(args):
                   "workload": "config3: 1e5 instances/GPU, p=16, 2 DCs, m=32, n_sub 1/2/4, memory x DP x ZeRO-1 grid",
                   "ms_per_launch": gms / gsteps, "status_ok": bool((g["status"] == 0).all().item())}
 
-    # ---------------- secondary: Wave-pattern evaluation (NEXT 1, reading Q32): 2e5 random valid Wave
-    # plans per GPU of one p=32 / 4-DC / m=32 instance (two chunks: 192 entries per stage, as config 4)
-    wave = None
+    # ---------------- secondary: two-chunk patterns (NEXT 1): Wave (reading Q32) and Loop (Q33), 2e5
+    # random valid plans per GPU of one p=32 / 4-DC / m=32 instance (192 entries per stage, as config 4)
+    wave = loop = None
     if not args.no_wave:
-        wb = K.wave_instance()
-        winst = cp.Instances(wb)
-        nw = args.n_wave or 200_000
-        wops, wln = PL.wave_plans_device(32, 32, 1, nw, seed=K.PERTURB_SEED ^ 0x3A, id0=rank * nw, q=1, stride=32)
-        for _ in range(3):
-            wr = cp.simulate(winst, wops, wln, best=True, wave=True)
-        wsteps = max(1, min(args.steps, 5))
-        barrier(ws)
-        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        v0.record(stream)
-        for _ in range(wsteps):
-            wr = cp.simulate(winst, wops, wln, best=True, wave=True)
-        v1.record(stream)
-        torch.cuda.synchronize()
-        wms = max_over_ranks(v0.elapsed_time(v1), ws)
-        wave = {"value": ws * nw * wsteps / (wms / 1e3), "unit": "evals/s",
-                "workload": "Wave (2 chunks, V): 2e5 random valid plans/GPU of one p=32, 4-DC, m=32 instance "
-                            "(L=T_F, T_bw=T_F/2), makespan + peak memory + argmin",
-                "ms_per_launch": wms / wsteps, "status_ok": bool((wr["status"] == 0).all().item())}
-        del wops, wln
+        for name, b_, is_loop in (("wave", K.wave_instance(), False), ("loop", K.loop_instance(), True)):
+            winst = cp.Instances(b_)
+            nw = args.n_wave or 200_000
+            wops, wln = PL.wave_plans_device(32, 32, 1, nw, seed=K.PERTURB_SEED ^ 0x3A, id0=rank * nw, q=1, stride=32,
+                                             loop=is_loop)
+            kw = {"loop": True} if is_loop else {"wave": True}
+            for _ in range(3):
+                wr = cp.simulate(winst, wops, wln, best=True, **kw)
+            wsteps = max(1, min(args.steps, 5))
+            barrier(ws)
+            v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            v0.record(stream)
+            for _ in range(wsteps):
+                wr = cp.simulate(winst, wops, wln, best=True, **kw)
+            v1.record(stream)
+            torch.cuda.synchronize()
+            wms = max_over_ranks(v0.elapsed_time(v1), ws)
+            line_w = {"value": ws * nw * wsteps / (wms / 1e3), "unit": "evals/s",
+                      "workload": ("Loop (2 chunks, wrap-around links)" if is_loop else "Wave (2 chunks, V)") +
+                                  ": 2e5 random valid plans/GPU of one p=32, 4-DC, m=32 instance (L=T_F, T_bw=T_F/2), "
+                                  "makespan + peak memory + argmin",
+                      "ms_per_launch": wms / wsteps, "status_ok": bool((wr["status"] == 0).all().item())}
+            if is_loop:
+                loop = line_w
+            else:
+                wave = line_w
+            del wops, wln
 
     # ---------------- secondary: sweeps (config 2 on one GPU's shard, config 5 sharded over all
     # ranks with one all_reduce(MIN) of the packed keys inside the timed region)
@@ -391,6 +398,7 @@ def run_ours(args):
             "clocks": clk,
             "greedy": greedy,
             "wave": wave,
+            "loop": loop,
             "sweep": sweeps,
             "best_schedule": {"makespan_ticks": best >> 32, "index": best & 0xFFFFFFFF, "all_status_ok": status_ok},
         }

@@ -668,3 +668,23 @@ def test_simulate_loop_ring_fixup(O):
     for k in ("status", "makespan", "peak_mem", "stage_stats"):
         assert np.array_equal(ref[k], small[k]), k
     check_loop(O, batch, plans, ref, timeline=False)
+
+
+def test_loop_bench_size_sampled(O):
+    """The bench's Loop workload (p=32, 4 DCs, m=32, cross-DC wrap links; device plans == host
+    plans) in the bench launch configuration; 30 sampled plans checked against the oracle."""
+    from workloads.wave import unpack_wave_plans
+    b = K.loop_instance()
+    n = 20_000
+    ops, ln = PL.wave_plans_device(32, 32, 1, n, seed=K.PERTURB_SEED ^ 0x3A, q=1, stride=32, loop=True)
+    r = to_host(cp.simulate(cp.Instances(b), ops, ln, stats=True, best=True, loop=True))
+    hops, hln = PL.wave_plans_host(32, 32, 1, n, seed=K.PERTURB_SEED ^ 0x3A, q=1, stride=32, loop=True)
+    assert np.array_equal(hops.view(np.int32), ops.cpu().numpy()) and np.array_equal(hln.view(np.int16), ln.cpu().numpy())
+    codes, lens = unpack_wave_plans(hops, hln)
+    d = b.item(0)
+    for i in np.random.default_rng(20).choice(n, 30, replace=False):
+        w = O.simulate_loop(d, [list(codes[i, s, :lens[i, s]]) for s in range(32)])
+        assert int(r["status"][i]) == w["status"] and int(r["makespan"][i]) == w["makespan"], i
+        assert int(r["peak_mem"][i]) == w["peak_mem"], i
+    ok = r["status"] == 0
+    assert int(r["best_key"][0]) >> 32 == int(r["makespan"][ok].min())

@@ -125,6 +125,15 @@ def perturbed_instance() -> InstanceBatch:
 PERTURB_SEED = SEED ^ 0x4
 
 
+def loop_instance() -> InstanceBatch:
+    """Loop bench instance (NEXT 1, reading Q33): config 4's setup with m = 32 and the wrap-around links
+    p-1 -> 0 / 0 -> p-1 (boundary index p-1) crossing from the last DC back to the first with the same
+    (L = T_F, T_bw = T_F/2); memory budget 3x the 1F1B device peak."""
+    b = uniform_instance(32, 32, 4, T_F, T_F, T_F, lat=T_F, bw=T_F // 2, mlim_x1000=3000)
+    b.lat_f[0, 31], b.bw_f[0, 31], b.lat_b[0, 31], b.bw_b[0, 31] = T_F, T_F // 2, T_F, T_F // 2
+    return b
+
+
 def wave_instance() -> InstanceBatch:
     """Wave bench instance (NEXT 1): config 4's setup (p=32, 4 DCs, L = T_F, T_bw = T_F/2) with m = 32, so
     each stage runs 2 chunks x 3 x 32 = 192 entries as in config 4; memory budget 3x the 1F1B device

@@ -74,8 +74,11 @@ __host__ __device__ static int gen_plan(int p, int m, int nsub, const int32_t* m
 // need a D of chunk c).  No memory gating, so the game cannot get stuck.  Preference: D (chunk 1
 // first) > F (chunk 0 first) > W, or with probability q/4 a uniformly random executable entry.
 // Output: 4-bit entries type | chunk << 2, 8 per word, word-major / stage-minor.
+// loop = 1: the Loop pattern (reading Q33) instead: F1 on stage 0 needs F0 of the last stage (wrap),
+// F1 elsewhere F1 of s-1; D1 needs D1 of s+1, or the own F1 on the last stage; D0 needs D0 of s+1,
+// or D1 of stage 0 on the last stage (wrap).
 __host__ __device__ static int gen_wave_plan(int p, int m, int nsub, uint64_t seed, uint64_t id, int q, uint32_t* ops,
-                                             uint16_t* len, int words, int stride) {
+                                             uint16_t* len, int words, int stride, int loop = 0) {
   const int total = 2 * (2 + nsub) * m;
   if (p < 1 || p > GEN_MAXP || m < 1 || nsub < 1 || total > 8 * words) return 2;
   int nF[2][GEN_MAXP], nD[2][GEN_MAXP], nW[2][GEN_MAXP], pF[2][GEN_MAXP], pD[2][GEN_MAXP];
@@ -93,10 +96,17 @@ __host__ __device__ static int gen_wave_plan(int p, int m, int nsub, uint64_t se
       if (k == total) continue;
       done = false;
       int cand[6], nx = 0;                       // entry codes, in preference order
-      if (nD[1][s] < m && (s == 0 ? nF[1][s] > nD[1][s] : pD[1][s - 1] > nD[1][s])) cand[nx++] = 2 | 4;
-      if (nD[0][s] < m && (s == p - 1 ? nD[1][s] > nD[0][s] : pD[0][s + 1] > nD[0][s])) cand[nx++] = 2;
-      if (nF[0][s] < m && (s == 0 || pF[0][s - 1] > nF[0][s])) cand[nx++] = 0;
-      if (nF[1][s] < m && (s == p - 1 ? nF[0][s] > nF[1][s] : pF[1][s + 1] > nF[1][s])) cand[nx++] = 4;
+      if (!loop) {
+        if (nD[1][s] < m && (s == 0 ? nF[1][s] > nD[1][s] : pD[1][s - 1] > nD[1][s])) cand[nx++] = 2 | 4;
+        if (nD[0][s] < m && (s == p - 1 ? nD[1][s] > nD[0][s] : pD[0][s + 1] > nD[0][s])) cand[nx++] = 2;
+        if (nF[0][s] < m && (s == 0 || pF[0][s - 1] > nF[0][s])) cand[nx++] = 0;
+        if (nF[1][s] < m && (s == p - 1 ? nF[0][s] > nF[1][s] : pF[1][s + 1] > nF[1][s])) cand[nx++] = 4;
+      } else {
+        if (nD[1][s] < m && (s == p - 1 ? nF[1][s] > nD[1][s] : pD[1][s + 1] > nD[1][s])) cand[nx++] = 2 | 4;
+        if (nD[0][s] < m && (s == p - 1 ? pD[1][0] > nD[0][s] : pD[0][s + 1] > nD[0][s])) cand[nx++] = 2;
+        if (nF[0][s] < m && (s == 0 || pF[0][s - 1] > nF[0][s])) cand[nx++] = 0;
+        if (nF[1][s] < m && (s == 0 ? pF[0][p - 1] > nF[1][s] : pF[1][s - 1] > nF[1][s])) cand[nx++] = 4;
+      }
       if (nW[1][s] < nsub * nD[1][s]) cand[nx++] = 3 | 4;
       if (nW[0][s] < nsub * nD[0][s]) cand[nx++] = 3;
       if (nx == 0) continue;
@@ -118,11 +128,11 @@ __host__ __device__ static int gen_wave_plan(int p, int m, int nsub, uint64_t se
 }
 
 __global__ void k_gen_wave(int p, int m, int nsub, uint64_t seed, uint64_t id0, int q, long long n, int words,
-                           int stride, uint32_t* ops, uint16_t* len, int32_t* err) {
+                           int stride, uint32_t* ops, uint16_t* len, int32_t* err, int loop) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (gen_wave_plan(p, m, nsub, seed, id0 + (uint64_t)i, q, ops + i * (long long)words * stride,
-                    len + i * (long long)stride, words, stride))
+                    len + i * (long long)stride, words, stride, loop))
     atomicAdd(err, 1);
 }
 
@@ -156,19 +166,19 @@ int cpgen_plans_host(int p, int m, int nsub, const int32_t* mf, const int32_t* m
 
 // Wave plans (host / device, identical for the same ids)
 int cpgen_wave_plans_host(int p, int m, int nsub, uint64_t seed, uint64_t id0, int q, long long n, uint32_t* ops,
-                          uint16_t* len, int words, int stride) {
+                          uint16_t* len, int words, int stride, int loop) {
   int err = 0;
   for (long long i = 0; i < n; ++i)
     err += gen_wave_plan(p, m, nsub, seed, id0 + (uint64_t)i, q, ops + i * (long long)words * stride,
-                         len + i * (long long)stride, words, stride) != 0;
+                         len + i * (long long)stride, words, stride, loop) != 0;
   return err;
 }
 int cpgen_wave_plans_device(int p, int m, int nsub, uint64_t seed, uint64_t id0, int q, long long n, uint32_t* ops,
-                            uint16_t* len, int words, int stride, int32_t* err, void* stream) {
+                            uint16_t* len, int words, int stride, int32_t* err, void* stream, int loop) {
   const int threads = 128;
   const long long blocks = (n + threads - 1) / threads;
   k_gen_wave<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(p, m, nsub, seed, id0, q, n, words, stride, ops,
-                                                                      len, err);
+                                                                      len, err, loop);
   return (int)cudaGetLastError();
 }
 

@@ -38,11 +38,11 @@ def lib():
                                          C.c_void_p, C.c_void_p]
         L.cpgen_wave_plans_host.restype = C.c_int
         L.cpgen_wave_plans_host.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int, C.c_longlong,
-                                            C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+                                            C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
         L.cpgen_wave_plans_device.restype = C.c_int
         L.cpgen_wave_plans_device.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
                                               C.c_longlong, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p,
-                                              C.c_void_p]
+                                              C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -95,21 +95,22 @@ def wave_words(p, m, n_sub=1):
     return (2 * (2 + n_sub) * m + 7) // 8
 
 
-def wave_plans_host(p, m, n_sub, n, seed, id0=0, q=1, stride=None):
-    """n random valid Wave plans (reading Q32), 4-bit entries (host).  Returns (ops uint32 [n, words, stride],
-    len uint16 [n, stride])."""
+def wave_plans_host(p, m, n_sub, n, seed, id0=0, q=1, stride=None, loop=False):
+    """n random valid Wave (reading Q32) or, loop=True, Loop (Q33) plans, 4-bit entries (host).  Returns
+    (ops uint32 [n, words, stride], len uint16 [n, stride])."""
     stride = stride or p
     words = wave_words(p, m, n_sub)
     ops = np.zeros((n, words, stride), dtype=np.uint32)
     ln = np.zeros((n, stride), dtype=np.uint16)
-    err = lib().cpgen_wave_plans_host(p, m, n_sub, seed, id0, q, n, ops.ctypes.data, ln.ctypes.data, words, stride)
+    err = lib().cpgen_wave_plans_host(p, m, n_sub, seed, id0, q, n, ops.ctypes.data, ln.ctypes.data, words, stride,
+                                      int(loop))
     if err:
         raise RuntimeError(f"wave plan generator failed on {err} plans")
     return ops, ln
 
 
-def wave_plans_device(p, m, n_sub, n, seed, id0=0, q=1, stride=None, device="cuda"):
-    """Same Wave plans generated on the GPU.  Returns torch tensors."""
+def wave_plans_device(p, m, n_sub, n, seed, id0=0, q=1, stride=None, device="cuda", loop=False):
+    """Same Wave / Loop plans generated on the GPU.  Returns torch tensors."""
     import torch
     stride = stride or p
     words = wave_words(p, m, n_sub)
@@ -117,7 +118,7 @@ def wave_plans_device(p, m, n_sub, n, seed, id0=0, q=1, stride=None, device="cud
     ln = torch.zeros((n, stride), dtype=torch.int16, device=device)
     err = torch.zeros(1, dtype=torch.int32, device=device)
     rc = lib().cpgen_wave_plans_device(p, m, n_sub, seed, id0, q, n, ops.data_ptr(), ln.data_ptr(), words, stride,
-                                       err.data_ptr(), torch.cuda.current_stream().cuda_stream)
+                                       err.data_ptr(), torch.cuda.current_stream().cuda_stream, int(loop))
     if rc:
         raise RuntimeError(f"cpgen launch failed: {rc}")
     if int(err.item()):
