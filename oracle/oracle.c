@@ -773,6 +773,29 @@ void or_build_zbh1(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t ma
   }
 }
 
+/* Interleaved 1F1B (IV1F1B, Table tab:ppschedules :471, cited not restated; Megatron's interleaved
+ * schedule), reading Q34, for the Loop pattern with 2 chunks and combined B.  Forward unit k
+ * (k = 0 .. 2m-1) is chunk (k / p) % 2 of microbatch (k / 2p) p + k % p; backward unit k takes the
+ * chunks in reverse, 1 - (k / p) % 2.  Stage s runs the first w = min(2 (p - s - 1) + p, 2m)
+ * forward units, then (next forward, next backward) pairs, then the remaining backward units. */
+int32_t or_build_iv1f1b(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen) {
+  if (p < 1 || m < 1 || m % p != 0 || maxlen < 4 * m) return -1;
+  for (int s = 0; s < p; ++s) {
+    int8_t* row = codes + (int64_t)s * maxlen;
+    int w = 2 * (p - s - 1) + p; if (w > 2 * m) w = 2 * m;
+    int k = 0;
+#define FWD(u) ((int8_t)(OR_F | ((((u) / p) % 2) << 2)))
+#define BWD(u) ((int8_t)(OR_B | ((1 - ((u) / p) % 2) << 2)))
+    for (int u = 0; u < w; ++u) row[k++] = FWD(u);
+    for (int i = 0; i < 2 * m - w; ++i) { row[k++] = FWD(w + i); row[k++] = BWD(i); }
+    for (int u = 2 * m - w; u < 2 * m; ++u) row[k++] = BWD(u);
+#undef FWD
+#undef BWD
+    len[s] = k;
+  }
+  return 0;
+}
+
 void or_build_gpipe(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen) {
   for (int s = 0; s < p; ++s) {
     int k = 0;

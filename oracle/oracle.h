@@ -108,6 +108,9 @@ int32_t or_greedy(const or_inst* I, int8_t* codes, int32_t* len, int32_t maxlen,
 /* Static builders (combined backward B). Return number of entries per stage written. */
 void or_build_1f1b(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
 void or_build_gpipe(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
+/* Interleaved 1F1B for the Loop pattern with 2 chunks (reading Q34), combined B, entries type |
+ * chunk << 2; needs m % p == 0 (returns 0) else writes nothing (returns -1); maxlen >= 4m. */
+int32_t or_build_iv1f1b(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
 /* ZB-H1 (split D/W), reading Q31: maxlen >= 3m. */
 void or_build_zbh1(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
 

@@ -87,6 +87,8 @@ def lib():
         L.or_check_plan_wave.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32]
         for fn in ("or_build_1f1b", "or_build_gpipe", "or_build_zbh1"):
             getattr(L, fn).argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
+        L.or_build_iv1f1b.restype = C.c_int32
+        L.or_build_iv1f1b.argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
         L.or_enumerate_opt.restype = C.c_int64
         L.or_enumerate_opt.argtypes = [P(OrInst), C.c_int64, P(C.c_int8), P(C.c_int32), C.c_int32, P(OrResult)]
         L.or_quantize.restype = C.c_int32
@@ -211,6 +213,16 @@ def check_plan(d, codes, lens=None) -> int:
 
 
 def build_static(kind: str, p: int, m: int):
+    """gpipe / 1f1b / zbh1 (UD plans) or iv1f1b (Loop plans, 2 chunks, needs m % p == 0)."""
+    if kind == "iv1f1b":
+        maxlen = 4 * m
+        c = np.zeros((p, maxlen), dtype=np.int8)
+        ln = np.zeros(p, dtype=np.int32)
+        rc = lib().or_build_iv1f1b(p, m, c.ctypes.data_as(C.POINTER(C.c_int8)), ln.ctypes.data_as(C.POINTER(C.c_int32)),
+                                   maxlen)
+        if rc:
+            raise ValueError("iv1f1b needs m % p == 0")
+        return c, ln
     maxlen = 3 * m if kind == "zbh1" else 2 * m
     c = np.zeros((p, maxlen), dtype=np.int8)
     ln = np.zeros(p, dtype=np.int32)

@@ -569,3 +569,26 @@ def test_loop_deadlock_and_wrap_validation(oracle_lib):
     assert oracle_lib.simulate_loop(d, cyc)["status"] == 1
     d["lat_b"] = np.array([0, 0, -1])
     assert oracle_lib.simulate_loop(d, good)["status"] == 8
+
+
+def test_iv1f1b_closed_form_and_memory(oracle_lib):
+    """Reading Q34 (interleaved 1F1B on the Loop pattern, 2 chunks, combined B): at zero delay with
+    uniform costs and m % p == 0 the makespan is 2m(f+b) + (p-1)(f+b) with b = t_d + t_w -- 1F1B's
+    pipeline fill (p-1)(f+b) per chunk, halved relative to running the two chunks as one block (the
+    interleaving's purpose, :471 "Bubble Ratio: Medium"); stage s holds w_s + 1 microbatch-chunks,
+    w_s = min(2(p-s-1) + p, 2m), so its peak is (w_s + 1) m_f."""
+    rng = np.random.default_rng(34)
+    for _ in range(80):
+        p = int(rng.integers(1, 9))
+        m = p * int(rng.integers(1, 4))
+        f, dd_, w = (int(x) for x in rng.integers(1, 80, size=3))
+        mf = int(rng.integers(1, 5))
+        md = -int(rng.integers(0, mf + 1))
+        d = inst(p, m, int(rng.integers(1, 5)), f, dd_, w, m_f=mf, m_d=md, m_w=-mf - md, mlim_x1000=10**6)
+        c, l_ = oracle_lib.build_static("iv1f1b", p, m)
+        assert oracle_lib.check_plan_wave(d, c, l_) == 0
+        r = oracle_lib.simulate_loop(d, c, l_)
+        b = dd_ + w
+        assert r["status"] == 0 and r["makespan"] == 2 * m * (f + b) + (p - 1) * (f + b), (p, m, f, dd_, w)
+        assert list(r["peak"]) == [(min(2 * (p - s - 1) + p, 2 * m) + 1) * mf if min(2 * (p - s - 1) + p, 2 * m) < 2 * m
+                                   else 2 * m * mf for s in range(p)]
