@@ -220,7 +220,7 @@ def build_static(kind: str, inst: Instances, n=None, inst_of=None, *, stage_stri
     n = inst.n if n is None else int(n)
     stride = stage_stride or inst.max_pp
     if words is None:
-        words = ((3 if kind == "zbh1" else 2) * inst.max_mb + 15) // 16
+        words = (4 * inst.max_mb + 7) // 8 if kind == "iv1f1b" else ((3 if kind == "zbh1" else 2) * inst.max_mb + 15) // 16
     ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
     ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
     d = inst.desc(None)

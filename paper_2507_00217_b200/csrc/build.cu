@@ -24,16 +24,17 @@ __global__ void __launch_bounds__(256) k_build_static(int kind, const cp_inst_v1
     const int r = (int)(t - item * stride);
     const long long ii = inst_of ? (long long)inst_of[item] : (n_inst == 1 ? 0 : item);
     const int p = inst[ii].n_pp, m = inst[ii].n_mb;
+    const int eb = plan_entry_bits(kind), per = 32 / eb;          // 16 or 8 entries per word
     int L = (r < p && m >= 1 && p <= stride) ? plan_row_len(kind, m) : 0;
-    if (L > 16 * words) L = 0;                       // does not fit: all-zero rows
+    if (L > per * words || (kind == CP_PLAN_IV1F1B && m % p != 0)) L = 0;   // does not fit: all-zero rows
     uint32_t* row = ops + item * (long long)words * stride + r;
     uint32_t wv = 0;
     int k = 0;
     for (int pos = 0; pos < L; ++pos) {
-      wv |= (uint32_t)plan_code(kind, r, p, m, pos) << ((pos & 15) << 1);
-      if ((pos & 15) == 15) { row[(long long)k * stride] = wv; wv = 0; ++k; }
+      wv |= (uint32_t)plan_code(kind, r, p, m, pos) << ((pos % per) * eb);
+      if (pos % per == per - 1) { row[(long long)k * stride] = wv; wv = 0; ++k; }
     }
-    if (L & 15) { row[(long long)k * stride] = wv; ++k; }
+    if (L % per) { row[(long long)k * stride] = wv; ++k; }
     for (; k < words; ++k) row[(long long)k * stride] = 0u;
     len[item * stride + r] = (uint16_t)L;
   }

@@ -10,10 +10,27 @@
 
 namespace cpk {
 
-__host__ __device__ __forceinline__ int plan_row_len(int kind, int m) { return kind == CP_PLAN_ZBH1 ? 3 * m : 2 * m; }
+__host__ __device__ __forceinline__ int plan_row_len(int kind, int m) {
+  return kind == CP_PLAN_ZBH1 ? 3 * m : (kind == CP_PLAN_IV1F1B ? 4 * m : 2 * m);
+}
+__host__ __device__ __forceinline__ int plan_entry_bits(int kind) { return kind == CP_PLAN_IV1F1B ? 4 : 2; }
 
 __host__ __device__ __forceinline__ int plan_code(int kind, int s, int p, int m, int pos) {
   if (kind == CP_PLAN_GPIPE) return pos < m ? (int)CP_OP_F : (int)CP_OP_B;
+  if (kind == CP_PLAN_IV1F1B) {
+    // 4-bit entries type | chunk << 2 (Q34): w forward units, (forward, backward) pairs, backward units;
+    // forward unit u is chunk (u / p) % 2, backward unit u chunk 1 - (u / p) % 2
+    const int w = (2 * (p - s - 1) + p) < 2 * m ? (2 * (p - s - 1) + p) : 2 * m;
+    int u, fw;
+    if (pos < w) { u = pos; fw = 1; }
+    else {
+      const int q = pos - w;
+      if (q < 2 * (2 * m - w)) { fw = !(q & 1); u = fw ? w + (q >> 1) : (q >> 1); }
+      else { fw = 0; u = (2 * m - w) + (q - 2 * (2 * m - w)); }
+    }
+    const int c = (u / p) % 2;
+    return fw ? ((int)CP_OP_F | (c << 2)) : ((int)CP_OP_B | ((1 - c) << 2));
+  }
   if (kind == CP_PLAN_1F1B) {
     const int w = (p - s - 1) < m ? (p - s - 1) : m;
     const int q = pos - w;

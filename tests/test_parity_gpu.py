@@ -688,3 +688,36 @@ def test_loop_bench_size_sampled(O):
         assert int(r["peak_mem"][i]) == w["peak_mem"], i
     ok = r["status"] == 0
     assert int(r["best_key"][0]) >> 32 == int(r["makespan"][ok].min())
+
+
+def test_build_iv1f1b_and_simulate_loop(O):
+    """cp_build_static(IV1F1B) (reading Q34) == the oracle's builder entry by entry (items with
+    m % p != 0 get all-zero rows), and the built plans through cp_simulate(loop) == the oracle's
+    Loop simulation of its own IV1F1B plans, with delays on every link including the wraps."""
+    from workloads.wave import unpack_wave_plans
+    rng = np.random.default_rng(44)
+    batch = K.random_instances(150, seed=45, max_p=16, max_m=4, intra_delay=True)
+    for i in range(150):
+        p = int(batch.p[i])
+        batch.m[i] = p * int(rng.integers(1, 4)) if i % 10 else p + 1 if p > 1 else 1    # a few m % p != 0
+        batch.n_sub[i] = 1
+        for fld in ("lat_f", "bw_f", "lat_b", "bw_b"):
+            getattr(batch, fld)[i, p - 1] = int(rng.integers(0, 200))
+    inst = cp.Instances(batch)
+    ops, ln = cp.build_static("iv1f1b", inst, stage_stride=32)
+    r = to_host(cp.simulate(inst, ops, ln, stats=True, timeline=True, loop=True))
+    codes, lens = unpack_wave_plans(ops.cpu().numpy().view(np.uint32), ln.cpu().numpy().view(np.uint16))
+    for i in range(150):
+        d = batch.item(i)
+        p, m = d["p"], d["m"]
+        if m % p:
+            assert not lens[i].any() and not codes[i].any(), i
+            continue
+        c, l_ = O.build_static("iv1f1b", p, m)
+        assert np.array_equal(lens[i, :p], l_), i
+        for s in range(p):
+            assert np.array_equal(codes[i, s, :l_[s]], c[s, :l_[s]]), (i, s)
+        w = O.simulate_loop(d, c, l_, timeline=True)
+        assert int(r["status"][i]) == w["status"] and int(r["makespan"][i]) == w["makespan"], i
+        for s in range(p):
+            assert np.array_equal(r["t_start"][i][s, :l_[s]], w["t_start"][s, :l_[s]]), (i, s)
