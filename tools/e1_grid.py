@@ -33,9 +33,43 @@ summary = {
     "slowdown bandwidth only (lat=0, bw=4 T_F)": {n: round(float(cm[0, -1, c]) / ref, 4) if cm[0, -1, c] >= 0 else None
                                                   for c, n in enumerate(names)},
 }
-# oracle spot check of 24 points
+# IV1F1B (Loop pattern, reading Q33/Q34) on the same points.  Interleaving splits each stage's layers
+# into two chunks, so a chunk block costs T_F/2 (the same model and the same activation messages);
+# the wrap link (stage 3 in the second DC back to stage 0) crosses DCs and carries the point's
+# (latency, T_bw) like the inner boundary
+from workloads.core import InstanceBatch
+parts = []
+for li in grid.lat:
+    for bi in grid.bw:
+        b = K.uniform_instance(4, 8, 2, K.T_F // 2, K.T_F // 2, K.T_F // 2, m_f=1, m_d=-1, m_w=0,
+                               lat=int(li), bw=int(bi))
+        b.lat_f[0, 3], b.bw_f[0, 3], b.lat_b[0, 3], b.bw_b[0, 3] = int(li), int(bi), int(li), int(bi)
+        parts.append(b)
+ib = InstanceBatch.concat(parts)
+iinst = cp.Instances(ib)
+io = torch.arange(len(ib), dtype=torch.int32, device="cuda")
+iops, iln = cp.build_static("iv1f1b", iinst, stage_stride=4)
+ir = cp.simulate(iinst, iops, iln, loop=True)
+torch.cuda.synchronize()
+iv = ir["makespan"].cpu().numpy().reshape(len(grid.lat), len(grid.bw))
+ivst = ir["status"].cpu().numpy()
+table["IV1F1B (Loop)"] = (iv / ref).round(4).tolist()
+g["IV1F1B (Loop)"] = iv
+summary["IV1F1B (Loop) status"] = ("memory above the 1F1B budget at every point: reported regardless, as the paper "
+                                   "evaluates static schedules" if (ivst == 2).all() else str(sorted(set(ivst.tolist()))))
+for key, (a, b_) in {"slowdown at max delay (lat=bw=4 T_F)": (-1, -1), "slowdown latency only (lat=4 T_F, bw=0)": (-1, 0),
+                     "slowdown bandwidth only (lat=0, bw=4 T_F)": (0, -1)}.items():
+    summary[key]["IV1F1B (Loop)"] = round(float(iv[a, b_]) / ref, 4)
+summary["IV1F1B at zero delay vs ZB-H1"] = round(float(iv[0, 0]) / ref, 4)
+summary["Loop most delay-sensitive (PAPER.md:496 'Loop schedules show the highest sensitivity')"] = bool(
+    iv[-1, -1] / iv[0, 0] > max(g[n][-1, -1] / g[n][0, 0] for n in ("1F1B", "ZB-H1")))
+# oracle spot check of 24 points (and of IV1F1B at 6 points)
 from oracle import oracle as O
 O.build()
+ci, li_ = O.build_static("iv1f1b", 4, 8)
+for k in np.random.default_rng(8).choice(len(ib), 6, replace=False):
+    w = O.simulate_loop(ib.item(int(k)), ci, li_)
+    assert int(ir["makespan"][int(k)]) == w["makespan"], (k, int(ir["makespan"][int(k)]), w["makespan"])
 G, keep = O.to_or_grid(grid)
 rng = np.random.default_rng(7)
 flat = cm.reshape(-1, 6)
@@ -45,7 +79,7 @@ for k in rng.choice(grid.n_points, 24, replace=False):
     assert list(flat[k]) == cms, (k, list(flat[k]), cms)
     checked += 1
 doc = {"workload": "E1: p=4, 2 DCs (2+2), m=8, F=D=W=T_F=38000 ticks, M_L = 1F1B budget, zero DP",
-       "axes": {"T_lat/T_F": ratios, "T_bw/T_F": ratios}, "candidates": names,
+       "axes": {"T_lat/T_F": ratios, "T_bw/T_F": ratios}, "candidates": names + ["IV1F1B (Loop)"],
        "slowdown_vs_zbh1_zero_delay": table, "summary": summary, "oracle_spot_checked_points": checked}
 os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
 with open(out, "w") as f:
