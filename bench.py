@@ -34,9 +34,10 @@ INT_PEAK_FILE = os.path.join(ROOT, "profiles", "int_peak_r01.jsonl")
 # algorithmic bytes per config-4 evaluation: plan 32 stages x 12 words x 4 B + len 32 x 2 B
 # + results (makespan 8 + peak 4 + status 4); the instance record (1792 B) is read once per launch
 BYTES_PER_EVAL = 32 * 12 * 4 + 32 * 2 + 16
-# algorithmic integer ops per evaluation: 5 per block x 6144 blocks + 3 per
-# message x 3968 messages
-OPS_PER_EVAL = 5 * 6144 + 3 * 3968
+# algorithmic integer ops per evaluation, SURVEY.md §8(d)'s per-unit figure: ~8 per block
+# (start max, end add, memory add, peak max, and the dependency bookkeeping: input/order checks and
+# counter updates) x 6144 blocks + ~4 per message (window max, bw add, lat add, link update) x 3968
+OPS_PER_EVAL = 8 * 6144 + 4 * 3968
 
 
 def peaks():
