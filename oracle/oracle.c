@@ -796,6 +796,53 @@ int32_t or_build_iv1f1b(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32
   return 0;
 }
 
+/* ZB-V (Table tab:ppschedules :473, cited not restated; the V-shaped Wave layout with split W),
+ * reading Q35: the per-stage order of a unit-time list schedule of the Wave data flow (reading
+ * Q32, 2 chunks) with every block one tick long and no delays.  At tick t every stage takes at
+ * most one block whose inputs were produced at ticks < t:
+ *   F0: from stage s-1 (stage 0: none)     F1: from stage s+1 (stage p-1: its own F0)
+ *   D1: from stage s-1 (stage 0: its own F1)   D0: from stage s+1 (stage p-1: its own D1)
+ *   W_c: after the stage's own D_c;  F only while the stage holds fewer than 2p chunk activations
+ *   (F in, W out; 2p chunks = the p full-stage activations 1F1B holds on stage 0, Table :473
+ *   "Medium").
+ * Choice: a W (W0 before W1) when no other block is ready or the stage is at 2p, else the first
+ * ready of F1, F0, D0, D1.  Rows have 6m entries.  Returns 0, or -1 (nothing defined) for p < 1,
+ * m < 1 or maxlen < 6m.                                                                       */
+int32_t or_build_zbv(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen) {
+  if (p < 1 || m < 1 || maxlen < 6 * m) return -1;
+  /* n[s][0..5] = blocks done at stage s: F0, F1, D0, D1, W0, W1; prev = the same at tick start */
+  int32_t (*n)[6] = (int32_t(*)[6])calloc((size_t)p, sizeof *n);
+  int32_t (*prev)[6] = (int32_t(*)[6])calloc((size_t)p, sizeof *prev);
+  for (int s = 0; s < p; ++s) len[s] = 0;
+  int64_t left = (int64_t)p * 6 * m;
+  while (left > 0) {
+    memcpy(prev, n, (size_t)p * sizeof *n);
+    for (int s = 0; s < p; ++s) {
+      const int32_t* c = prev[s];
+      const int f0 = c[0] < m && (s == 0 || prev[s - 1][0] > c[0]);
+      const int f1 = c[1] < m && (s == p - 1 ? c[0] > c[1] : prev[s + 1][1] > c[1]);
+      const int d1 = c[3] < m && (s == 0 ? c[1] > c[3] : prev[s - 1][3] > c[3]);
+      const int d0 = c[2] < m && (s == p - 1 ? c[3] > c[2] : prev[s + 1][2] > c[2]);
+      const int w0 = c[4] < c[2], w1 = c[5] < c[3];
+      const int full = c[0] + c[1] - c[4] - c[5] >= 2 * p;
+      const int fa = !full && f1, fb = !full && f0;
+      int8_t e;
+      if ((w0 || w1) && (full || !(fa || fb || d0 || d1))) e = w0 ? (int8_t)(OR_W | 0 << 2) : (int8_t)(OR_W | 1 << 2);
+      else if (fa) e = (int8_t)(OR_F | 1 << 2);
+      else if (fb) e = (int8_t)(OR_F | 0 << 2);
+      else if (d0) e = (int8_t)(OR_D | 0 << 2);
+      else if (d1) e = (int8_t)(OR_D | 1 << 2);
+      else continue;                                      /* idle this tick */
+      codes[(int64_t)s * maxlen + len[s]++] = e;
+      const int ch = e >> 2, ty = e & 3;
+      ++n[s][ty == OR_F ? ch : (ty == OR_D ? 2 + ch : 4 + ch)];
+      --left;
+    }
+  }
+  free(n); free(prev);
+  return 0;
+}
+
 void or_build_gpipe(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen) {
   for (int s = 0; s < p; ++s) {
     int k = 0;

@@ -111,6 +111,9 @@ void or_build_gpipe(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t m
 /* Interleaved 1F1B for the Loop pattern with 2 chunks (reading Q34), combined B, entries type |
  * chunk << 2; needs m % p == 0 (returns 0) else writes nothing (returns -1); maxlen >= 4m. */
 int32_t or_build_iv1f1b(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
+/* ZB-V for the Wave pattern with 2 chunks and split W (reading Q35): unit-time list schedule;
+ * rows of 6m entries type | chunk << 2; returns 0, or -1 for p < 1, m < 1, maxlen < 6m. */
+int32_t or_build_zbv(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
 /* ZB-H1 (split D/W), reading Q31: maxlen >= 3m. */
 void or_build_zbh1(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t maxlen);
 

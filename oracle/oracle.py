@@ -87,6 +87,8 @@ def lib():
         L.or_check_plan_wave.argtypes = [P(OrInst), P(C.c_int8), P(C.c_int32), C.c_int32]
         for fn in ("or_build_1f1b", "or_build_gpipe", "or_build_zbh1"):
             getattr(L, fn).argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
+        L.or_build_zbv.restype = C.c_int32
+        L.or_build_zbv.argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
         L.or_build_iv1f1b.restype = C.c_int32
         L.or_build_iv1f1b.argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
         L.or_enumerate_opt.restype = C.c_int64
@@ -213,7 +215,17 @@ def check_plan(d, codes, lens=None) -> int:
 
 
 def build_static(kind: str, p: int, m: int):
-    """gpipe / 1f1b / zbh1 (UD plans) or iv1f1b (Loop plans, 2 chunks, needs m % p == 0)."""
+    """gpipe / 1f1b / zbh1 (UD plans), iv1f1b (Loop plans, 2 chunks, needs m % p == 0) or zbv (Wave
+    plans, 2 chunks, split W)."""
+    if kind == "zbv":
+        maxlen = 6 * m
+        c = np.zeros((p, maxlen), dtype=np.int8)
+        ln = np.zeros(p, dtype=np.int32)
+        rc = lib().or_build_zbv(p, m, c.ctypes.data_as(C.POINTER(C.c_int8)), ln.ctypes.data_as(C.POINTER(C.c_int32)),
+                                maxlen)
+        if rc:
+            raise ValueError("zbv needs p >= 1, m >= 1")
+        return c, ln
     if kind == "iv1f1b":
         maxlen = 4 * m
         c = np.zeros((p, maxlen), dtype=np.int8)

@@ -592,3 +592,47 @@ def test_iv1f1b_closed_form_and_memory(oracle_lib):
         assert r["status"] == 0 and r["makespan"] == 2 * m * (f + b) + (p - 1) * (f + b), (p, m, f, dd_, w)
         assert list(r["peak"]) == [(min(2 * (p - s - 1) + p, 2 * m) + 1) * mf if min(2 * (p - s - 1) + p, 2 * m) < 2 * m
                                    else 2 * m * mf for s in range(p)]
+
+
+# --------------------------------------------------------------------------- ZB-V (reading Q35)
+def test_zbv_zero_bubble_at_the_lower_bound(oracle_lib):
+    """Reading Q35 (ZB-V, Wave pattern, split W), SPEC.md:545 acceptance 2 ("bubble ratio <= 0.02 on
+    every stage" for uniform t_f = t_d = t_w, zero delay, m >= 2p): here every stage's bubble ratio
+    over its active window is exactly 0 and the makespan is the lower bound
+    (6m + p - 1) t -- the last stage cannot start before (p - 1) t (chunk 0 crosses p - 1 stages)
+    and then runs 6m blocks of t.  Peak memory stays within 2p chunk activations, the 1F1B stage-0
+    peak of p full-stage activations (Table :473, "Memory: Medium")."""
+    rng = np.random.default_rng(35)
+    for p in range(1, 9):
+        for m in sorted({2 * p, 2 * p + 1, 3 * p, 4 * p + 3}):
+            t = int(rng.integers(1, 50))
+            d = inst(p, m, int(rng.integers(1, 5)), t, t, t, m_f=1, m_d=0, m_w=-1, mlim_x1000=10**6)
+            c, l_ = oracle_lib.build_static("zbv", p, m)
+            assert list(l_) == [6 * m] * p and oracle_lib.check_plan_wave(d, c, l_) == 0
+            r = oracle_lib.simulate_wave(d, c, l_, timeline=True)
+            assert r["status"] == 0 and r["makespan"] == (6 * m + p - 1) * t, (p, m)
+            for s in range(p):
+                st = r["t_start"][s][:6 * m]
+                assert st.max() + t - st.min() == 6 * m * t, (p, m, s)        # busy window: no idle tick
+            assert max(r["peak"]) <= 2 * p
+
+
+def test_zbv_small_m_and_dominance(oracle_lib):
+    """m < 2p: the plan is valid and completes within the 2p budget (no zero-bubble claim).  Zero-delay
+    dominance (Fig. 6's left edge): with the stage cost split over two half-cost
+    chunks, makespan(ZBV) <= makespan(ZBH1) <= makespan(1F1B) at t_d = t_w."""
+    for p in range(1, 9):
+        for m in range(1, 2 * p):
+            d = inst(p, m, 2, 10, 10, 10, m_f=1, m_d=0, m_w=-1, mlim_x1000=10**6)
+            c, l_ = oracle_lib.build_static("zbv", p, m)
+            r = oracle_lib.simulate_wave(d, c, l_)
+            assert oracle_lib.check_plan_wave(d, c, l_) == 0 and r["status"] == 0 and max(r["peak"]) <= 2 * p
+    for p in (4, 8):
+        for m in (2 * p, 3 * p):
+            for f, b in ((100, 100), (60, 100), (100, 40)):
+                ud = inst(p, m, 2, f, b, b, mlim_x1000=10**6)
+                half = inst(p, m, 2, f // 2, b // 2, b // 2, m_f=1, m_d=0, m_w=-1, mlim_x1000=10**6)
+                zv = oracle_lib.simulate_wave(half, *oracle_lib.build_static("zbv", p, m))["makespan"]
+                zh = oracle_lib.simulate(ud, *oracle_lib.build_static("zbh1", p, m))["makespan"]
+                one = oracle_lib.simulate(ud, *oracle_lib.build_static("1f1b", p, m))["makespan"]
+                assert zv <= zh <= one, (p, m, f, b, zv, zh, one)
