@@ -60,6 +60,8 @@ extern "C" {
 #define CP_PLAN_ZBH1 5        /* ZB-H1, split D/W, W deferred by s microbatches on stage s (Q31) */
 #define CP_PLAN_IV1F1B 6      /* interleaved 1F1B, Loop pattern plans (pattern CP_PATTERN_LOOP, 4-bit entries,
                                  2 chunks, combined B), needs n_mb % n_pp == 0 (Q34) */
+#define CP_PLAN_ZBV 7         /* ZB-V, Wave pattern plans (pattern CP_PATTERN_WAVE, 4-bit entries, 2 chunks,
+                                 split W): unit-time list schedule, 2p chunk-activation budget (Q35) */
 #define CP_N_CAND 6           /* sweep candidates: 0 GPipe, 1 1F1B, 2/3/4 greedy n_sub 1/2/4, 5 ZB-H1 */
 
 typedef enum { CP_OK = 0, CP_EINVAL = -1, CP_EUNSUPPORTED = -2, CP_ECUDA = -3, CP_EWORKSPACE = -4 } cp_rc;
@@ -191,12 +193,13 @@ int32_t cp_sweep_shard(const cp_grid* grid, int64_t point_lo, int64_t point_hi,
 /* Build static plans (PAPER.md Table tab:ppschedules :468-473; readings Q22, Q23, Q31) for the
  * out->n items of `out`: item i uses instance inst_of[i] (NULL: instance i, or 0 if inst->n == 1)
  * and gets its (p, m) plan in the packed layout cp_simulate reads.  kind: CP_PLAN_GPIPE,
- * CP_PLAN_1F1B, CP_PLAN_ZBH1 (2-bit UD entries) or CP_PLAN_IV1F1B (4-bit Loop entries, 8 per word;
- * an item with n_mb % n_pp != 0 gets all-zero rows).  Every word of out->ops and every row of out->len is written
+ * CP_PLAN_1F1B, CP_PLAN_ZBH1 (2-bit UD entries), CP_PLAN_IV1F1B (4-bit Loop entries, 8 per word;
+ * an item with n_mb % n_pp != 0 gets all-zero rows) or CP_PLAN_ZBV (4-bit Wave entries, 6*n_mb per
+ * row; Table :473, reading Q35; an item with n_pp > 32 gets all-zero rows).  Every word of out->ops and every row of out->len is written
  * (entries past a row's length and rows >= p are 0), so the result is fully defined.
  * Errors: CP_EINVAL for an unknown kind, NULL / inconsistent descriptors, stage_stride < max_pp,
- * or the row capacity (16*words entries, 8*words for IV1F1B) < entries per row at max_mb (2*max_mb;
- * 3*max_mb for ZB-H1; 4*max_mb for IV1F1B).  An item whose own
+ * or the row capacity (16*words entries, 8*words for IV1F1B / ZB-V) < entries per row at max_mb
+ * (2*max_mb; 3*max_mb for ZB-H1; 4*max_mb for IV1F1B; 6*max_mb for ZB-V).  An item whose own
  * (p, m) exceeds (stage_stride, words) gets all-zero rows.  Enqueued on `stream`, no sync. */
 int32_t cp_build_static(int32_t kind, const cp_instances* inst, const cp_schedules* out, void* stream);
 

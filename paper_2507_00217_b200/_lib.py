@@ -78,7 +78,7 @@ EXPORTS = ("cp_abi_version", "cp_status_string", "cp_workspace_bytes", "cp_simul
            "cp_validate_instance")
 ABI_VERSION = 2
 N_CAND = 6                    # sweep candidates: 0 GPipe, 1 1F1B, 2/3/4 greedy n_sub 1/2/4, 5 ZB-H1
-PLAN_KINDS = {"gpipe": 0, "1f1b": 1, "zbh1": 5, "iv1f1b": 6}   # iv1f1b: Loop plans (4-bit entries)
+PLAN_KINDS = {"gpipe": 0, "1f1b": 1, "zbh1": 5, "iv1f1b": 6, "zbv": 7}   # iv1f1b: Loop, zbv: Wave plans (4-bit)
 
 _lib = None
 

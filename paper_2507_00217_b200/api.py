@@ -211,7 +211,8 @@ def greedy(inst: Instances, *, stats=False, timeline=False, stage_stride=None, w
 
 
 def build_static(kind: str, inst: Instances, n=None, inst_of=None, *, stage_stride=None, words=None, stream=None):
-    """cp_build_static: static plans ("gpipe", "1f1b" or "zbh1") for n items (item i uses instance
+    """cp_build_static: static plans ("gpipe", "1f1b", "zbh1"; "iv1f1b" for loop=True and "zbv" for
+    wave=True simulation) for n items (item i uses instance
     inst_of[i], or i / 0 as in cp_simulate) -> (ops int32 [n, words, stride], len int16 [n, stride]),
     ready for simulate()."""
     _require_cuda(inst.dev)
@@ -220,7 +221,8 @@ def build_static(kind: str, inst: Instances, n=None, inst_of=None, *, stage_stri
     n = inst.n if n is None else int(n)
     stride = stage_stride or inst.max_pp
     if words is None:
-        words = (4 * inst.max_mb + 7) // 8 if kind == "iv1f1b" else ((3 if kind == "zbh1" else 2) * inst.max_mb + 15) // 16
+        per_mb = {"zbh1": 3, "iv1f1b": 4, "zbv": 6}.get(kind, 2)
+        words = (per_mb * inst.max_mb + 7) // 8 if kind in ("iv1f1b", "zbv") else (per_mb * inst.max_mb + 15) // 16
     ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
     ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
     d = inst.desc(None)

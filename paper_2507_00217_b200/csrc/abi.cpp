@@ -343,14 +343,17 @@ int32_t cp_simulate(const cp_instances* in, const cp_schedules* sc, const cp_res
 }
 
 int32_t cp_build_static(int32_t kind, const cp_instances* in, const cp_schedules* out, void* stream) {
-  if (kind != CP_PLAN_GPIPE && kind != CP_PLAN_1F1B && kind != CP_PLAN_ZBH1 && kind != CP_PLAN_IV1F1B) return CP_EINVAL;
+  if (kind != CP_PLAN_GPIPE && kind != CP_PLAN_1F1B && kind != CP_PLAN_ZBH1 && kind != CP_PLAN_IV1F1B &&
+      kind != CP_PLAN_ZBV)
+    return CP_EINVAL;
   int rc = check_instances(in);
   if (rc) return rc;
   if (!out || out->n < 0 || !out->ops || !out->len || out->words < 1) return CP_EINVAL;
   if (out->stage_stride < in->max_pp) return CP_EINVAL;
   if (!out->inst_of && in->n != 1 && in->n < out->n) return CP_EINVAL;
-  const long long need = kind == CP_PLAN_ZBH1 ? 3LL * in->max_mb : (kind == CP_PLAN_IV1F1B ? 4LL : 2LL) * in->max_mb;
-  if ((kind == CP_PLAN_IV1F1B ? 8LL : 16LL) * out->words < need) return CP_EINVAL;
+  const long long per_mb = kind == CP_PLAN_ZBH1 ? 3 : (kind == CP_PLAN_IV1F1B ? 4 : (kind == CP_PLAN_ZBV ? 6 : 2));
+  const bool nibbles = kind == CP_PLAN_IV1F1B || kind == CP_PLAN_ZBV;
+  if ((nibbles ? 8LL : 16LL) * out->words < per_mb * in->max_mb) return CP_EINVAL;
   if (out->n == 0) return CP_OK;
   return cpk::launch_build_static(kind, in->inst, in->n, out->inst_of, out->n, out->stage_stride, out->words, out->ops,
                                   out->len, stream) == cudaSuccess ? CP_OK : CP_ECUDA;

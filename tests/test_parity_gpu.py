@@ -721,3 +721,36 @@ def test_build_iv1f1b_and_simulate_loop(O):
         assert int(r["status"][i]) == w["status"] and int(r["makespan"][i]) == w["makespan"], i
         for s in range(p):
             assert np.array_equal(r["t_start"][i][s, :l_[s]], w["t_start"][s, :l_[s]]), (i, s)
+
+
+def test_build_zbv_and_simulate_wave(O):
+    """cp_build_static(ZBV) (reading Q35; one warp per item, a round per unit tick) == the oracle's
+    builder entry by entry, for p up to 32 and m on both sides of 2p (row capacity exactly 6 max_mb),
+    and the built plans through cp_simulate(wave) == the oracle's Wave simulation of its own ZB-V
+    plans, start tick by start tick, with delays on every link."""
+    from workloads.wave import unpack_wave_plans
+    rng = np.random.default_rng(47)
+    n = 120
+    batch = K.random_instances(n, seed=48, max_p=32, max_m=4, intra_delay=True)
+    for i in range(n):
+        p = int(batch.p[i])
+        batch.m[i] = int(rng.integers(1, 2 * p)) if i % 3 == 0 else int(rng.integers(2 * p, 4 * p + 3))
+        batch.n_sub[i] = 1
+    batch.m[int(np.argmax(batch.p[:n]))] = 64                         # the widest item at m = 64
+    inst = cp.Instances(batch)
+    ops, ln = cp.build_static("zbv", inst, stage_stride=32)
+    assert ops.shape[1] == (6 * int(batch.m[:n].max()) + 7) // 8
+    r = to_host(cp.simulate(inst, ops, ln, stats=True, timeline=True, wave=True))
+    codes, lens = unpack_wave_plans(ops.cpu().numpy().view(np.uint32), ln.cpu().numpy().view(np.uint16))
+    for i in range(n):
+        d = batch.item(i)
+        p, m = d["p"], d["m"]
+        c, l_ = O.build_static("zbv", p, m)
+        assert np.array_equal(lens[i, :p], l_) and not lens[i, p:].any(), i
+        assert not codes[i, p:].any() and not codes[i, :, 6 * m:].any(), i
+        for s in range(p):
+            assert np.array_equal(codes[i, s, :l_[s]], c[s, :l_[s]]), (i, s)
+        w = O.simulate_wave(d, c, l_, timeline=True)
+        assert int(r["status"][i]) == w["status"] and int(r["makespan"][i]) == w["makespan"], i
+        for s in range(p):
+            assert np.array_equal(r["t_start"][i][s, :l_[s]], w["t_start"][s, :l_[s]]), (i, s)
