@@ -1,0 +1,82 @@
+"""E2: cross-DC PP vs cross-DC DP for Llama-3-405B (§5.2 :503-516, App. E :855-858,
+Fig. cross_dc_dp_or_pp; reading Q36; scenario inputs in workloads/ppdp.py) on the GPU kernels.
+
+Per (latency, bandwidth) point:
+  t_PP  = best greedy CrossUDSub (n_sub 1/2/4, 1F1B memory budget; cp_greedy), as SPEC.md:500
+          prescribes at n_PP = 16 (the paper's exact CrossUD/CrossWave is out of reach there);
+          t_PP_static = best of 1F1B, ZB-H1 (cp_build_static + cp_simulate) and ZBV (Wave, Q35) under the
+          same delays, reported beside it;
+  t_DP  = ZBV at zero delay (single DC) + 2 alpha + 2 N beta (Q36);
+  speedup = t_DP / t_PP, slowdown = t_PP / ideal (ZBV at zero delay).
+Spot-checks greedy points against the oracle.  usage: python tools/e2_ppdp.py [out.json]"""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2507_00217_b200 as cp
+from workloads import ppdp as E
+from workloads.core import InstanceBatch
+
+out = sys.argv[1] if len(sys.argv) > 1 else "profiles/e2_pp_vs_dp_r01.json"
+lats, bws = E.LATENCIES_MS, E.BANDWIDTHS_GBS
+pts = [(l, g) for l in lats for g in bws]
+p, m = E.LLAMA3_405B["n_pp"], E.n_microbatches()
+
+# greedy CrossUDSub, n_sub 1/2/4
+gb = InstanceBatch.concat([E.pp_instance(l * 1e-3, g * 1e9, n_sub=ns) for ns in (1, 2, 4) for (l, g) in pts])
+gr = cp.greedy(cp.Instances(gb))
+gms = gr["makespan"].cpu().numpy().reshape(3, len(pts))
+assert (gr["status"].cpu().numpy() == 0).all()
+t_greedy = gms.min(axis=0) * E.TICK_S
+# static UD schedules and ZBV under the same delays
+ub = InstanceBatch.concat([E.pp_instance(l * 1e-3, g * 1e9) for (l, g) in pts])
+uinst = cp.Instances(ub)
+stat = {}
+for kind in ("1f1b", "zbh1"):
+    o, ln = cp.build_static(kind, uinst)
+    stat[kind] = cp.simulate(uinst, o, ln)["makespan"].cpu().numpy() * E.TICK_S
+vb = InstanceBatch.concat([E.wave_instance(l * 1e-3, g * 1e9) for (l, g) in pts] + [E.wave_instance(0.0, float("inf"))])
+vinst = cp.Instances(vb)
+vo, vl = cp.build_static("zbv", vinst)
+vms = cp.simulate(vinst, vo, vl, wave=True)["makespan"].cpu().numpy() * E.TICK_S
+stat["zbv"], ideal = vms[:-1], float(vms[-1])
+torch.cuda.synchronize()
+t_static = np.minimum(np.minimum(stat["1f1b"], stat["zbh1"]), stat["zbv"])
+fam = np.array(["1F1B", "ZB-H1", "ZBV"])[np.argmin(np.stack([stat["1f1b"], stat["zbh1"], stat["zbv"]]), axis=0)]
+t_dp = np.array([ideal + E.dp_cost_s(l * 1e-3, g * 1e9) for (l, g) in pts])
+speed, slow = t_dp / t_greedy, t_greedy / ideal
+S = lambda a: a.reshape(len(lats), len(bws))
+
+# oracle spot check (greedy, ZBV)
+from oracle import oracle as O
+O.build()
+rng = np.random.default_rng(36)
+for k in rng.choice(len(pts), 6, replace=False):
+    ns_i = int(rng.integers(3))
+    d = gb.item(ns_i * len(pts) + int(k))
+    assert O.greedy(d)["makespan"] == int(gms[ns_i, k]), (k, ns_i)
+    w = O.simulate_wave(vb.item(int(k)), *O.build_static("zbv", p, m))["makespan"]
+    assert abs(w * E.TICK_S - stat["zbv"][k]) < 1e-9, k
+sp, sl = S(speed), S(slow)
+i4, i128, g4, g64 = lats.index(4), lats.index(128), bws.index(4), bws.index(64)
+summary = {
+    "T_F (s)": round(E.stage_forward_s(), 5), "m": m, "PP message (GB)": E.pp_message_bytes() / 1e9,
+    "ideal single-DC ZBV (s)": round(ideal, 3),
+    "speedup PP over DP at 4 GB/s (paper: up to 3.05x)": round(float(sp[:, g4].max()), 3),
+    "PP slowdown vs single DC at 64 GB/s (paper: 1.3x)": [round(float(x), 3) for x in sl[:, g64]],
+    "speedup at 1024 / 4096 GB/s (paper: negligible beyond 1024)": [round(float(sp[i4, bws.index(1024)]), 3),
+                                                                    round(float(sp[i4, bws.index(4096)]), 3)],
+    "max t_PP change over latency 4-128 ms (paper: little impact)": round(float((S(t_greedy)[i128] / S(t_greedy)[i4] - 1).max()), 4),
+    "speedup non-increasing in bandwidth (1% slack)": bool(all((sp[i, 1:] <= sp[i, :-1] * 1.01).all() for i in range(len(lats)))),
+    "points where a static schedule beats the greedy": int((t_static < t_greedy).sum()),
+}
+doc = {"workload": "E2: Llama-3-405B, n_TP 8, n_PP 16, n_DP 64, s 8192, b 1, m 32, 2 DCs (8+8 stages), "
+                   "tick 0.1 ms; readings Q35/Q36",
+       "axes": {"latency_ms": lats, "bandwidth_GBps": bws},
+       "t_pp_greedy_s": S(t_greedy).round(4).tolist(), "t_pp_static_best_s": S(t_static).round(4).tolist(),
+       "static_best_family": fam.reshape(len(lats), len(bws)).tolist(), "t_dp_s": S(t_dp).round(4).tolist(),
+       "speedup_pp_over_dp": sp.round(4).tolist(), "slowdown_pp_vs_single_dc": sl.round(4).tolist(),
+       "summary": summary, "oracle_spot_checked_points": 6}
+os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
+with open(out, "w") as f:
+    json.dump(doc, f)
+print(json.dumps(summary, indent=1))
