@@ -636,3 +636,35 @@ def test_zbv_small_m_and_dominance(oracle_lib):
                 zh = oracle_lib.simulate(ud, *oracle_lib.build_static("zbh1", p, m))["makespan"]
                 one = oracle_lib.simulate(ud, *oracle_lib.build_static("1f1b", p, m))["makespan"]
                 assert zv <= zh <= one, (p, m, f, b, zv, zh, one)
+
+
+def test_e1_orderings_spec_acceptance_5(oracle_lib):
+    """SPEC.md:548 acceptance 5 on the §5.1 setup (4 stages, 2 DCs x 2, 8 microbatches, F = D = W = T_F,
+    UD memory budget = 1F1B's) over (T_lat/T_F, T_bw/T_F) in {0, 0.5, 1, 2}^2, slowdowns relative to
+    ZBV at zero delay (PAPER.md :486): (a) at zero delay Wave <= every UD schedule; (b) at (2, 2) every
+    UD schedule <= Wave; (c) Loop (IV1F1B) >= Wave and >= the WGrad-split UD schedules (ZB-H1, greedy)
+    at every nonzero point (:496).  Two-chunk schedules run half-cost chunks; the Loop wrap link
+    crosses DCs.  (The unified-backward 1F1B stays above IV1F1B at small delays: DESIGN.md §12.)"""
+    O = oracle_lib
+    f, h = 200, 100
+    cz, lz = O.build_static("zbv", 4, 8)
+    ci, li_ = O.build_static("iv1f1b", 4, 8)
+    res = {}
+    for a in (0, 0.5, 1, 2):
+        for b in (0, 0.5, 1, 2):
+            lat, bw = int(a * f), int(b * f)
+            ud = inst(4, 8, 2, f, f, f, lat=lat, bw=bw)
+            r = {k: O.simulate(ud, *O.build_static(k, 4, 8))["makespan"] for k in ("1f1b", "zbh1")}
+            r["greedy"] = min(O.greedy(inst(4, 8, 2, f, f, f, lat=lat, bw=bw, n_sub=ns))["makespan"] for ns in (1, 2, 4))
+            r["zbv"] = O.simulate_wave(inst(4, 8, 2, h, h, h, m_f=1, m_d=0, m_w=-1, mlim_x1000=2000, lat=lat, bw=bw),
+                                       cz, lz)["makespan"]
+            lb = K.uniform_instance(4, 8, 2, h, h, h, m_f=1, m_d=-1, m_w=0, lat=lat, bw=bw, mlim_x1000=10**6)
+            lb.lat_f[0, 3], lb.bw_f[0, 3], lb.lat_b[0, 3], lb.bw_b[0, 3] = lat, bw, lat, bw
+            r["iv1f1b"] = O.simulate_loop(lb.item(0), ci, li_)["makespan"]
+            res[a, b] = r
+    ud_all = ("1f1b", "zbh1", "greedy")
+    assert all(res[0, 0]["zbv"] <= res[0, 0][k] for k in ud_all), res[0, 0]
+    assert all(res[2, 2][k] <= res[2, 2]["zbv"] for k in ud_all), res[2, 2]
+    for (a, b), r in res.items():
+        if (a, b) != (0, 0):
+            assert r["iv1f1b"] >= max(r["zbv"], r["zbh1"], r["greedy"]), ((a, b), r)
