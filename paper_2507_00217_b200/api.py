@@ -232,6 +232,28 @@ def build_static(kind: str, inst: Instances, n=None, inst_of=None, *, stage_stri
     return ops, ln
 
 
+def exact(inst: Instances, *, cap=65536, max_plans=1 << 32, stage_stride=None, stream=None):
+    """cp_exact: the makespan-optimal split plan (n_sub = 1) of every (tiny) instance by exhaustive
+    search on the GPU -> dict(ops int32 [n, words, stride], len int16 [n, stride], makespan, status).
+    Plans are in simulate()'s layout; status CPI_OVERFLOW (16) marks instances beyond the limits."""
+    _require_cuda(inst.dev)
+    dev = inst.dev.device
+    n = inst.n
+    stride = stage_stride or inst.max_pp
+    words = max(1, (3 * min(inst.max_mb, 8) + 15) // 16)
+    ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
+    ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
+    ms = torch.empty(n, dtype=torch.int32, device=dev)
+    st = torch.empty(n, dtype=torch.int32, device=dev)
+    nb = int(L.load().cp_exact_workspace_bytes(n, cap))
+    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+    d = inst.desc(None)
+    sc = L.CpSchedules(n, stride, words, 0, None, ops.data_ptr(), ln.data_ptr())
+    L.check(L.load().cp_exact(C.byref(d), C.byref(sc), C.c_void_p(ms.data_ptr()), C.c_void_p(st.data_ptr()), cap,
+                              int(max_plans), C.c_void_p(ws.data_ptr()), nb, _stream(stream)), "cp_exact")
+    return {"ops": ops, "len": ln, "makespan": ms, "status": st}
+
+
 def to_cp_grid(grid) -> L.CpGrid:
     """workloads.Grid -> cp_grid (host struct, passed to the kernel by value)."""
     g = L.CpGrid()

@@ -754,3 +754,64 @@ def test_build_zbv_and_simulate_wave(O):
         assert int(r["status"][i]) == w["status"] and int(r["makespan"][i]) == w["makespan"], i
         for s in range(p):
             assert np.array_equal(r["t_start"][i][s, :l_[s]], w["t_start"][s, :l_[s]]), (i, s)
+
+
+def test_exact_search_matches_oracle_enumeration(O):
+    """cp_exact (NEXT 3) == the oracle's exhaustive optimum (or_enumerate_opt) on random tiny
+    instances with delays, memory budgets, DP tails and ZeRO-1: same makespan and the same plan,
+    entry by entry (both return the first optimum in product order).  Limits: n_sub != 1, m > 8 or a
+    too-small max_plans give CPI_OVERFLOW; the plan through cp_simulate reproduces the makespan."""
+    from workloads.core import unpack_plans
+    rng = np.random.default_rng(51)
+    n = 24
+    batch = K.random_instances(n, seed=52, max_p=3, max_m=3, intra_delay=True)
+    batch.n_sub[:n] = 1
+    for i in range(n):
+        p = int(batch.p[i])
+        batch.m_lim[i, :p] = batch.m_f[i, :p] * int(rng.integers(1, 4))       # 1-3 activations in flight
+    batch.n_sub[n - 1] = 2                                                  # unsupported -> overflow
+    inst = cp.Instances(batch)
+    r = cp.exact(inst)
+    ms, st = r["makespan"].cpu().numpy(), r["status"].cpu().numpy()
+    codes, lens = unpack_plans(r["ops"].cpu().numpy().view(np.uint32), r["len"].cpu().numpy().view(np.uint16))
+    for i in range(n - 1):
+        d = batch.item(i)
+        e = O.enumerate_opt(d)
+        assert e["evaluated"] >= 0, i
+        if e["makespan"] < 0:
+            assert st[i] == 1 and ms[i] == -1, i                           # every plan deadlocks
+            continue
+        assert st[i] == 0 and ms[i] == e["makespan"], (i, ms[i], e["makespan"])
+        p = d["p"]
+        for s in range(p):
+            assert np.array_equal(codes[i, s, :lens[i, s]], e["codes"][s, :e["len"][s]]), (i, s)
+    assert st[n - 1] == 16 and ms[n - 1] == -1
+    sim = cp.simulate(inst, r["ops"][: n - 1], r["len"][: n - 1], inst_of=torch.arange(n - 1, dtype=torch.int32,
+                                                                                     device="cuda"))
+    ok = st[: n - 1] == 0
+    assert np.array_equal(sim["makespan"].cpu().numpy()[ok], ms[: n - 1][ok])
+    small = cp.exact(inst, max_plans=2)
+    assert (small["status"].cpu().numpy()[:n - 1][ok] == 16).any()
+
+
+def test_exact_search_bounds_greedy(O):
+    """Beyond the oracle's reach (p = 3, m = 4 and p = 4, m = 3: up to ~10^7 plans): the optimum is a
+    valid plan (oracle re-simulation gives the same makespan), and it is <= the greedy's and the
+    static 1F1B's makespan (the optimality sandwich of SPEC.md:547)."""
+    from workloads.core import unpack_plans
+    parts = []
+    for (p, m, lat, bw) in ((3, 4, 0, 0), (3, 4, 120, 60), (4, 3, 0, 0), (4, 3, 150, 40)):
+        parts.append(K.uniform_instance(p, m, 2, 100, 100, 100, lat=lat, bw=bw, mlim_x1000=1000))
+    from workloads.core import InstanceBatch
+    batch = InstanceBatch.concat(parts)
+    inst = cp.Instances(batch)
+    r = cp.exact(inst)
+    g = cp.greedy(inst)
+    ms, st = r["makespan"].cpu().numpy(), r["status"].cpu().numpy()
+    codes, lens = unpack_plans(r["ops"].cpu().numpy().view(np.uint32), r["len"].cpu().numpy().view(np.uint16))
+    for i in range(len(parts)):
+        d = batch.item(i)
+        assert st[i] == 0
+        assert O.simulate(d, codes[i, :d["p"]], lens[i, :d["p"]])["makespan"] == ms[i]
+        assert ms[i] <= int(g["makespan"][i])
+        assert ms[i] <= O.simulate(d, *O.build_static("1f1b", d["p"], d["m"]))["makespan"]
