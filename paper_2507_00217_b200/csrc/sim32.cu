@@ -232,49 +232,71 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         tabA[1 * 32] = make_int4(tB, mB, bwB, latB);
         tabA[2 * 32] = make_int4(td, md, bwB, latB);
         tabA[3 * 32] = make_int4(tw, mw, 0, 0);
-        tabB[0 * 32] = make_int4(iF, Rm, sendF ? 1 : 0, 0);
-        tabB[1 * 32] = make_int4(iD, Rm, sendD ? -1 : 0, 0);
-        tabB[2 * 32] = make_int4(iD, Rm, sendD ? -1 : 0, 0);
-        tabB[3 * 32] = make_int4(wbase + zero_row + lane, 0, 0, 0);
+        // shared-window byte addresses, masks on counts * 32
+        const unsigned sb = (unsigned)__cvta_generic_to_shared(smem);
+        tabB[0 * 32] = make_int4((int)(sb + 4u * iF), Rm << 5, sendF ? 4 : 0, 0);
+        tabB[1 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, 0);
+        tabB[2 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, 0);
+        tabB[3 * 32] = make_int4((int)(sb + 4u * (wbase + zero_row + lane)), 0, 0, 0);
       }
       __syncwarp();
       clk = tag;
+      // Counters are kept scaled by 32 (one ring slot = 32 words) and the plan position doubled,
+      // so that every address is one LEA off a shared-window base: the entry code comes from one
+      // funnel shift of the staged word, the table row is tab + code * 512 B, the ring slot is
+      // column + ((count & mask) << 2).  (A row holds at most 1024 >= 2m entries, so 32 * m <= 16384
+      // fits the 16-bit halves of the neighbour shuffle.)
+      const unsigned sb = (unsigned)__cvta_generic_to_shared(smem);
+      const unsigned tab0 = sb + 4u * (unsigned)(wbase + 4 * lane);        // tabA[0][lane]; tabB at +2048 B
+      const unsigned iPb = sb + 4u * (unsigned)iP;
+      const int R32 = R << 5, plen2 = 2 * plen;
+      int pos2 = 0;
       for (;;) {
         const int me = madd(nD, 65536, nF);
         const int cu = __shfl_up_sync(FULLM, me, 1);
         const int cd = __shfl_down_sync(FULLM, me, 1);
         const int leftF = (cu & 0xffff) | lmF;
-        const int leftD = cu >> 16;                 // stage 0 reads itself: nD - nD < R
+        const int leftD = cu >> 16;
         const int rightF = (cd & 0xffff) | rmF;
-        const int rightD = last ? nF : (cd >> 16);  // the last stage's D follows its own F
-        const unsigned code = (wv >> ((pos & 15) << 1)) & 3u;
-        const int4 ta = tabA[code << 5];            // {duration, memory delta, link bw, latency}
-        const int4 tb = tabB[code << 5];            // {ring column, slot mask, send offset, -}
+        const int rightD = last ? nF : (cd >> 16);
+        unsigned code;
+        asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(code) : "r"(wv), "r"(pos2));
+        code &= 3u;
+        asm("mov.b32 %0, %0;" : "+r"(code));        // materialized once: LEA for the table row
+        const unsigned ta_addr = tab0 + (code << 9);
+        int4 ta, tb;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(ta.x), "=r"(ta.y), "=r"(ta.z), "=r"(ta.w) : "r"(ta_addr));
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+2048];"
+                     : "=r"(tb.x), "=r"(tb.y), "=r"(tb.z), "=r"(tb.w) : "r"(ta_addr));
         const bool isF = code == CP_OP_F, isW = code == CP_OP_W;
-        const bool rF = (leftF > nF) & (nF - rightF < R);
-        const bool rD = (rightD > nD) & (nD - leftD < R);
+        const bool rF = (leftF > nF) & (nF - rightF < R32);
+        const bool rD = (rightD > nD) & (nD - leftD < R32);
         const bool isDB = !isF & !isW;
-        const bool go = (pos < plen) & ((isF & rF) | (isW & (went < nD)) | (isDB & rD));
-        const int raddr = tb.x + (((isF ? nF : nD) & tb.y) << 5);
-        const int start = mx(clk, smem[raddr]);
+        const bool go = (pos2 < plen2) & ((isF & rF) | (isW & (went < nD)) | (isDB & rD));
+        const unsigned raddr = (unsigned)tb.x + ((unsigned)((isF ? nF : nD) & tb.y) << 2);
+        int arr;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"(raddr));
+        const int start = mx(clk, arr);
         const int end = start + ta.x;
         const int nl = mx(end, isF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
-        if (go && tb.z != 0) smem[raddr + tb.z] = nl + ta.w;
+        if (go && tb.z != 0) asm volatile("st.shared.b32 [%0], %1;" :: "r"(raddr + tb.z), "r"(nl + ta.w) : "memory");
         const int gi = go ? 1 : 0, gFi = (go & isF) ? 1 : 0, gWi = (go & isW) ? 1 : 0;
         const int gDi = gi - gFi - gWi;
         clk = madd(gi, end - clk, clk);
         mem = madd(gi, ta.y, mem);
         peak = mx(peak, mem);
-        pos = madd(gi, 1, pos);
+        pos2 = madd(gi, 2, pos2);
         linkF = madd(gFi, nl - linkF, linkF);
         linkB = madd(gDi, nl - linkB, linkB);
-        nF = madd(gFi, 1, nF);
-        nD = madd(gDi, 1, nD);
-        went = madd(gWi, 1, went);
-        wv = (uint32_t)smem[iP + ((pos >> 4) << 5)];
+        nF = madd(gFi, 32, nF);
+        nD = madd(gDi, 32, nD);
+        went = madd(gWi, 32, went);
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(iPb + (((unsigned)pos2 & ~31u) << 2)));
         __syncwarp();                               // ring stores visible to the neighbours' next reads
         if (!__any_sync(FULLM, go)) break;
       }
+      nF >>= 5; nD >>= 5; went >>= 5; pos = pos2 >> 1;
     } else {
       rounds(std::false_type{});
     }
