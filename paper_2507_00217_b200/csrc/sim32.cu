@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         const int nl = mx(end, isF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
         if (go && tb.z != 0) asm volatile("st.shared.b32 [%0], %1;" :: "r"(raddr + tb.z), "r"(nl + ta.w) : "memory");
         const int gi = go ? 1 : 0, gFi = (go & isF) ? 1 : 0, gWi = (go & isW) ? 1 : 0;
-        const int gDi = gi - gFi - gWi;
+        const int gDi = (go & isDB) ? 1 : 0;
         clk = madd(gi, end - clk, clk);
         mem = madd(gi, ta.y, mem);
         peak = mx(peak, mem);
@@ -292,7 +292,9 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         nF = madd(gFi, 32, nF);
         nD = madd(gDi, 32, nD);
         went = madd(gWi, 32, went);
-        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(iPb + (((unsigned)pos2 & ~31u) << 2)));
+        unsigned wa;                                // iPb + 4 * (pos2 & ~31): one LOP3 + one IMAD
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(wa) : "r"((unsigned)pos2 & ~31u), "r"(iPb));
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(wa));
         __syncwarp();                               // ring stores visible to the neighbours' next reads
         if (!__any_sync(FULLM, go)) break;
       }
