@@ -9,5 +9,5 @@ python bench.py > gpurun_out/bench_n1_$tag.json 2> gpurun_out/bench_n1_$tag.err;
 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref_$tag.json 2>&1; tail -1 gpurun_out/bench_ref_$tag.json | cut -c1-200
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch_$tag.log 2>&1; echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:k_sim32 -s 3 -c 1 -f -o gpurun_out/sim32_$tag \
+ncu --set full --clock-control none --import-source on -k regex:k_sim32 -s 2 -c 1 -f -o gpurun_out/sim32_$tag \
     python tools/prof_sim.py sim 1000000 > gpurun_out/ncu_full_$tag.log 2>&1; echo "ncu full rc=$?"
