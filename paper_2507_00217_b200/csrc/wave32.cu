@@ -32,7 +32,7 @@ __device__ __forceinline__ int wmadd(int g, int d, int x) {   // x + g*d on the 
 }
 }  // namespace
 
-template <bool kLoop>
+template <bool kLoop, bool kTL>   // kTL: per-entry start ticks requested (A.t_start)
 __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const __grid_constant__ Args A) {
   extern __shared__ __align__(16) int32_t smem[];
   const int lane = threadIdx.x & 31;
@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
       oD0 = first_s ? 0 : iD0 - 1;
     }
     if (s >= p) oF0 = oF1 = oD0 = oD1 = 0;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(smem);
     // parameter tables, entry x = type | chunk << 2:
     //   tabA[x] = {duration, memory delta, link bw, latency} (W: first sub-block / whole W if n_sub 1)
     //   tabB[x] = {input ring column (zero row without a producer), slot mask, consumer column (0: no
@@ -165,12 +166,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
       tabA[5 * 32] = make_int4(td + tw, md + mw, dD1 ? bwR : bwL, dD1 ? latR : latL);
       tabA[6 * 32] = make_int4(td, md, dD1 ? bwR : bwL, dD1 ? latR : latL);
       tabA[7 * 32] = make_int4(tW, mW, 0, 0);
-      tabB[0 * 32] = make_int4(inF0 ? iF0 : iZ, inF0 ? Rm : 0, oF0, 1);
-      tabB[1 * 32] = make_int4(inD0 ? iD0 : iZ, inD0 ? Rm : 0, oD0, 0);
+      // columns as shared-window byte addresses (0: no consumer), masks on counts scaled by 32
+      const auto B = [&](int col) { return col ? (int)(sb + 4u * (unsigned)col) : 0; };
+      const int Rm32 = Rm << 5;
+      tabB[0 * 32] = make_int4(B(inF0 ? iF0 : iZ), inF0 ? Rm32 : 0, B(oF0), 1);
+      tabB[1 * 32] = make_int4(B(inD0 ? iD0 : iZ), inD0 ? Rm32 : 0, B(oD0), 0);
       tabB[2 * 32] = tabB[1 * 32];
-      tabB[3 * 32] = make_int4(iZ, 0, 0, 0);
-      tabB[4 * 32] = make_int4(inF1 ? iF1 : iZ, inF1 ? Rm : 0, oF1, dF1);
-      tabB[5 * 32] = make_int4(inD1 ? iD1 : iZ, inD1 ? Rm : 0, oD1, dD1);
+      tabB[3 * 32] = make_int4(B(iZ), 0, 0, 0);
+      tabB[4 * 32] = make_int4(B(inF1 ? iF1 : iZ), inF1 ? Rm32 : 0, B(oF1), dF1);
+      tabB[5 * 32] = make_int4(B(inD1 ? iD1 : iZ), inD1 ? Rm32 : 0, B(oD1), dD1);
       tabB[6 * 32] = tabB[5 * 32];
       tabB[7 * 32] = tabB[3 * 32];
     }
@@ -204,39 +208,57 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
     __syncwarp();
     auto rounds = [&](auto n1) {
       constexpr bool kN1 = decltype(n1)::value;       // n_sub == 1: a W entry is a whole W block
+      // counts (and wP) are kept scaled by 32, one ring slot, and the plan position by 4 (one entry
+      // nibble): the entry code is one funnel shift, the table row tab + x * 512 B and the ring slot
+      // column + ((count & mask) << 2) are single LEAs off shared-window byte addresses
+      const unsigned tab0 = sb + 4u * (unsigned)(wbase + 4 * lane), iPb = sb + 4u * (unsigned)iP;
+      const int R32 = R << 5, Rm32 = Rm << 5, plen4 = 4 * plen;
+      int pos4 = 0;
       for (;;) {
         const XY q = neighbours();
         const int nF0 = cF & 0xffff, nF1 = cF >> 16, nD0 = cD & 0xffff, nD1 = cD >> 16;
-        const uint32_t wv = (uint32_t)smem[iP + ((pos >> 3) << 5)];
-        const uint32_t x = (wv >> ((pos & 7) << 2)) & 7u;
-        const int4 ta = tabA[x << 5];
-        const int4 tb = tabB[x << 5];
+        unsigned wa, wv, x;
+        asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(wa) : "r"((unsigned)pos4 & ~31u), "r"(iPb));
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(wa));
+        asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(x) : "r"(wv), "r"(pos4));
+        x &= 7u;
+        asm("mov.b32 %0, %0;" : "+r"(x));
+        const unsigned ta_addr = tab0 + (x << 9);
+        int4 ta, tb;
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(ta.x), "=r"(ta.y), "=r"(ta.z), "=r"(ta.w) : "r"(ta_addr));
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+4096];"
+                     : "=r"(tb.x), "=r"(tb.y), "=r"(tb.z), "=r"(tb.w) : "r"(ta_addr));
         const int ch = (int)(x >> 2);
         const bool isF = (x & 3u) == CP_OP_F, isW = (x & 3u) == CP_OP_W;
         // readiness: input produced (or the own turn-around / loss), room in the consumer's ring
-        const bool rF0 = (q.xF0 > nF0) & (nF0 - q.yF0 < R);
-        const bool rF1 = (q.xF1 > nF1) & (nF1 - q.yF1 < R);
-        const bool rD1 = (q.xD1 > nD1) & (nD1 - q.yD1 < R);
-        const bool rD0 = (q.xD0 > nD0) & (nD0 - q.yD0 < R);
+        const bool rF0 = (q.xF0 > nF0) & (nF0 - q.yF0 < R32);
+        const bool rF1 = (q.xF1 > nF1) & (nF1 - q.yF1 < R32);
+        const bool rD1 = (q.xD1 > nD1) & (nD1 - q.yD1 < R32);
+        const bool rD0 = (q.xD0 > nD0) & (nD0 - q.yD0 < R32);
         const int wc = ch ? (wP >> 16) : (wP & 0xffff), ndc = ch ? nD1 : nD0;
         const bool rW = kN1 ? wc < ndc : wc < ns * ndc;
         const bool rdy = isF ? (ch ? rF1 : rF0) : (isW ? rW : (ch ? rD1 : rD0));
-        const bool go = (pos < plen) & rdy;
+        const bool go = (pos4 < plen4) & rdy;
         const bool right = tb.w != 0;
         // the entry's own count of its stream addresses both its input slot and its message slot
         const int cnt = ((isF ? cF : cD) >> (ch ? 16 : 0)) & 0xffff;
-        const int start = wmx(clk, smem[tb.x + ((cnt & tb.y) << 5)]);
+        int arr;
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"((unsigned)tb.x + ((unsigned)(cnt & tb.y) << 2)));
+        const int start = wmx(clk, arr);
         int dur = ta.x, dm = ta.y;
         if (!kN1) {                                     // W sub-block k of its W block (Q12)
-          const int k = wc % ns;
+          const int k = (wc >> 5) % ns;
           dur = isW ? wq + (k < wr ? 1 : 0) : dur;
           dm = isW ? (k == ns - 1 ? mw : 0) : dm;
         }
         const int end = start + dur;
         const int nl = wmx(end, right ? lkR : lkL) + ta.z;   // FIFO link clock (App. X1)
-        if (go & (tb.z != 0)) smem[tb.z + ((cnt & Rm) << 5)] = nl + ta.w;   // (tb.z: consumer column, 0 = none)
-        if (A.t_start && go && pos < A.len_stride)
-          A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + pos] = start;
+        if (go & (tb.z != 0))                           // (tb.z: consumer column, 0 = none)
+          asm volatile("st.shared.b32 [%0], %1;" :: "r"((unsigned)tb.z + ((unsigned)(cnt & Rm32) << 2)), "r"(nl + ta.w)
+                       : "memory");
+        if (kTL && go && (pos4 >> 2) < A.len_stride)
+          A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + (pos4 >> 2)] = start;
         const int gi = go ? 1 : 0;
         clk = wmadd(gi, end - clk, clk);
         mem = wmadd(gi, dm, mem);
@@ -247,14 +269,16 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
         const int gR = (sent & right) ? 1 : 0, gL = (sent & !right) ? 1 : 0;
         lkR = wmadd(gR, nl - lkR, lkR);
         lkL = wmadd(gL, nl - lkL, lkL);
-        const int inc = ch ? 65536 : 1;
+        const int inc = ch ? (32 << 16) : 32;
         cF = wmadd((go & isF) ? 1 : 0, inc, cF);
         cD = wmadd((go & !isF & !isW) ? 1 : 0, inc, cD);
         wP = wmadd((go & isW) ? 1 : 0, inc, wP);
-        pos = wmadd(gi, 1, pos);
+        pos4 = wmadd(gi, 4, pos4);
         __syncwarp();
         if (!__any_sync(WFULL, go)) break;
       }
+      const auto unscale = [](int c) { return ((c & 0xffff) >> 5) | ((c >> 21) << 16); };
+      cF = unscale(cF); cD = unscale(cD); wP = unscale(wP); pos = pos4 >> 2;
     };
     if (ns == 1) rounds(std::true_type{});
     else rounds(std::false_type{});
@@ -318,7 +342,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
 }
 
 int launch_wave32(const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  const void* fn = a.chunk_pattern == CP_PATTERN_LOOP ? (const void*)k_chunk32<true> : (const void*)k_chunk32<false>;
+  const bool tl = a.t_start != nullptr;
+  const void* fn = a.chunk_pattern == CP_PATTERN_LOOP ? (tl ? (const void*)k_chunk32<true, true> : (const void*)k_chunk32<true, false>)
+                                                      : (tl ? (const void*)k_chunk32<false, true> : (const void*)k_chunk32<false, false>);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
@@ -328,7 +354,7 @@ int launch_wave32(const Args& a, int blocks, int threads, size_t smem, void* str
 }
 
 int wave32_blocks_per_sm(int threads, size_t smem) {
-  const void* fn = (const void*)k_chunk32<false>;
+  const void* fn = (const void*)k_chunk32<false, false>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;
