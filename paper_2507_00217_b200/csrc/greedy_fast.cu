@@ -263,13 +263,14 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(co
       const int end = tstar + ta.x;
       const int nl = gmax(end, pF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
       if (go & (pF ? sendF : (pD & sendD))) smem[pF ? adF + 1 : adD - 1] = nl + ta.w;
-      // emit the 2-bit entry; a full word goes straight to global memory
+      // emit the 2-bit entry into a shift register (the newest entry enters at bits 30-31, so after
+      // 16 entries entry k sits at bits 2k); a full word goes straight to global memory
       const uint32_t code = pF ? CP_OP_F : (pD ? CP_OP_D : CP_OP_W);
-      const uint32_t w1 = emitw | (code << ((pos & 15) << 1));
       if (!kGrid) {
+        const uint32_t w1 = (emitw >> 2) | (code << 30);
         const bool flush = go & ((pos & 15) == 15);
         if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
-        emitw = go ? (flush ? 0u : w1) : emitw;
+        emitw = go ? w1 : emitw;
       }
       const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
       const bool gW = go & pW;
@@ -335,7 +336,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(co
               const int4 v = (complete && on) ? make_int4(Pf + xf, clk, m * (tf + td + tw), peak) : make_int4(0, 0, 0, 0);
               *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + s) * 4) = v;
             }
-            if (on && (pos & 15) && s < A.stage_stride) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw;
+            if (on && (pos & 15) && s < A.stage_stride)         // the partial word, aligned to bit 0
+              A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = emitw >> (32 - 2 * (pos & 15));
             finish_rows(item, on ? pos : 0, false);
           }
           need = true;
