@@ -126,9 +126,35 @@ def dist_setup(args):
     if ws > 1:
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        bind_gpu_local_cpus(local)
     else:
         torch.cuda.set_device(0)
     return rank, ws, local
+
+
+NUMA_BOUND = False
+
+
+def bind_gpu_local_cpus(dev):
+    """N > 1: pin this rank to the CPUs NVML reports as local to its GPU, so the pinned host buffers
+    of the e2e leg (first touch by this process) land on the GPU's NUMA node.  Best effort."""
+    global NUMA_BOUND
+    try:
+        import pynvml
+        import torch
+        pr = torch.cuda.get_device_properties(dev)
+        bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        n = os.cpu_count() or 64
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (w >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            NUMA_BOUND = True
+    except Exception:
+        pass
 
 
 def barrier(ws):
@@ -394,7 +420,8 @@ def run_ours(args):
                              "peak_source": peak_src, "bytes_per_eval": BYTES_PER_EVAL},
             "cpu_baseline": None,
             "e2e": {"value": e2e_val, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": f"cp.HostPipeline ({args.chunks} chunks, copy/compute overlap)", "matches_device_run": e2e_ok},
+                    "api": f"cp.HostPipeline ({args.chunks} chunks, copy/compute overlap)", "matches_device_run": e2e_ok,
+                    "host_cpus_bound_to_gpu_numa_node": NUMA_BOUND},
             "gpu_launches": 2 * args.steps,
             "clocks": clk,
             "greedy": greedy,
