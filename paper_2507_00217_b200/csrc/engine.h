@@ -89,7 +89,10 @@ constexpr int kThreads = 128;          // 4 warps per block
 constexpr int kFastThreads = 64;
 constexpr int kFastMinBlocks = 9;
 constexpr int kFixWarps = 148 * 4;     // warps of a global-ring (fix-up) launch
-constexpr int kGreedyTableWords = 768;   // k_greedy_fast per-warp parameter table: [6 entries][32 lanes] int4
+constexpr int kGreedyTableWords = 256;   // k_greedy_fast per-warp parameter table: [F, D][32 lanes] int4
+// k_greedy_fast: 12 two-warp blocks per SM (6 warps per scheduler) fit its 9 KB per warp; the bound
+// caps registers at 85 (78 used)
+constexpr int kGreedyMinBlocks = 12;
 constexpr int kSim32TableWords = 1024;  // k_sim32 per-warp parameter tables: 2 x [4 codes][32 lanes] int4
 
 }  // namespace cpk

@@ -49,7 +49,7 @@ __device__ __noinline__ void greedy_finish_rows(const Args& A, long long it, int
 }
 
 template <int W, bool kGrid>
-__global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(const __grid_constant__ Args A) {
+__global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(const __grid_constant__ Args A) {
   extern __shared__ __align__(128) int32_t smem[];
   constexpr int NSEG = 32 / W;
   const int lane = threadIdx.x & 31;
@@ -152,14 +152,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(co
           // the last stage's D ring may hold a larger instance's arrivals: it must read 0
           if (lastS && s < W - 1)
             for (int k = 0; k < R; ++k) smem[iD + (k << 5)] = 0;
-          // parameter table: 0 = F, 1 = D, 2 + e + 2f = W sub-block with duration wq + e, memory
-          // delta f ? m_w : 0 (f: last sub-block of its W block)
+          // parameter table: 0 = F, 1 = D (W sub-blocks are computed from wq, wr, m_w in the round)
           tab[0 * 32] = make_int4(tf, mf, bwF, latF);
           tab[1 * 32] = make_int4(td, md, bwB, latB);
-          tab[2 * 32] = make_int4(wq, 0, 0, 0);
-          tab[3 * 32] = make_int4(wq + 1, 0, 0, 0);
-          tab[4 * 32] = make_int4(wq, mw, 0, 0);
-          tab[5 * 32] = make_int4(wq + 1, mw, 0, 0);
         }
       }
       // warp-wide: lookahead prefix sums (segment scans), horizon bound, status ballots
@@ -257,10 +252,11 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(co
       const bool go = (tstar < GINF) & (tstar < gmin(Lh, Rh)) & !(pF & (nF - nD >= R));
       const bool pW = !pD & !pF;
       const bool wfin = wsub + 1 == nsub;
-      const int tiW = 2 + (wsub < wr ? 1 : 0) + (wfin ? 2 : 0);
-      const int ti = pF ? 0 : (pD ? 1 : tiW);
-      const int4 ta = tab[ti << 5];                        // {duration, memory delta, link bw, latency}
-      const int end = tstar + ta.x;
+      const int4 ta = tab[pF ? 0 : 32];                    // F or D row: {duration, memory delta, link bw, latency}
+      // a W sub-block (Q12): duration wq + (sub-block index < t_w mod n_sub), memory delta m_w at the last
+      const int dur = pW ? wq + (wsub < wr ? 1 : 0) : ta.x;
+      const int dmv = pW ? (wfin ? mw : 0) : ta.y;
+      const int end = tstar + dur;
       const int nl = gmax(end, pF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
       if (go & (pF ? sendF : (pD & sendD))) smem[pF ? adF + 1 : adD - 1] = nl + ta.w;
       // emit the 2-bit entry into a shift register (the newest entry enters at bits 30-31, so after
@@ -275,7 +271,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_greedy_fast(co
       const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
       const bool gW = go & pW;
       clk = gmadd(gi, end - clk, clk);
-      mem = gmadd(gi, ta.y, mem);
+      mem = gmadd(gi, dmv, mem);
       peak = gmax(peak, mem);
       linkF = gmadd(gFi, nl - linkF, linkF);
       linkB = gmadd(gDi, nl - linkB, linkB);
