@@ -138,7 +138,7 @@ class HostPipeline:
     chunk is one cp_simulate call on device views with index_base = chunk start, so best_key
     carries global schedule ids.  Device buffers and streams are allocated once and reused."""
 
-    def __init__(self, inst: Instances, n: int, words: int, stride: int, chunks: int = 8, device="cuda"):
+    def __init__(self, inst: Instances, n: int, words: int, stride: int, chunks: int = 32, device="cuda"):
         self.inst, self.n, self.chunks = inst, n, max(1, chunks)
         self.ops_d = torch.empty((n, words, stride), dtype=torch.int32, device=device)
         self.len_d = torch.empty((n, stride), dtype=torch.int16, device=device)
