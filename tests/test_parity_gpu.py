@@ -815,3 +815,36 @@ def test_exact_search_bounds_greedy(O):
         assert O.simulate(d, codes[i, :d["p"]], lens[i, :d["p"]])["makespan"] == ms[i]
         assert ms[i] <= int(g["makespan"][i])
         assert ms[i] <= O.simulate(d, *O.build_static("1f1b", d["p"], d["m"]))["makespan"]
+
+
+def test_two_chunk_plans_at_the_size_limit(O):
+    """Wave / Loop plans at the GPU limit n_mb = 256 (p = 32, 1536 entries per row: the first pass's
+    8-slot rings and the second pass's 256-slot rings in shared memory), ZB-V built at that size, all
+    against the oracle; n_mb = 257 is refused with CP_EUNSUPPORTED (include/crosspipe.h)."""
+    from workloads.wave import unpack_wave_plans
+    for loop in (False, True):
+        b = K.uniform_instance(32, 256, 4, 100, 100, 100, lat=100, bw=50, mlim_x1000=10**6)
+        if loop:
+            b.lat_f[0, 31], b.bw_f[0, 31], b.lat_b[0, 31], b.bw_b[0, 31] = 100, 50, 100, 50
+        inst = cp.Instances(b)
+        ops, ln = PL.wave_plans_device(32, 256, 1, 3, seed=61, stride=32, loop=loop)
+        r = to_host(cp.simulate(inst, ops, ln, stats=True, wave=not loop, loop=loop))
+        codes, lens = unpack_wave_plans(ops.cpu().numpy().view(np.uint32), ln.cpu().numpy().view(np.uint16))
+        sim = O.simulate_loop if loop else O.simulate_wave
+        for i in range(3):
+            rows = [list(codes[i, s, :lens[i, s]]) for s in range(32)]
+            w = sim(b.item(0), rows)
+            assert int(r["status"][i]) == w["status"] and int(r["makespan"][i]) == w["makespan"], (loop, i)
+    vb = K.uniform_instance(32, 256, 4, 100, 100, 100, m_f=1, m_d=0, m_w=-1, lat=100, bw=50, mlim_x1000=10**6)
+    vinst = cp.Instances(vb)
+    vo, vl = cp.build_static("zbv", vinst, stage_stride=32)
+    rv = cp.simulate(vinst, vo, vl, wave=True)
+    cz, lz = O.build_static("zbv", 32, 256)
+    codes, lens = unpack_wave_plans(vo.cpu().numpy().view(np.uint32), vl.cpu().numpy().view(np.uint16))
+    for s in range(32):
+        assert np.array_equal(codes[0, s, :lens[0, s]], cz[s, :lz[s]]), s
+    assert int(rv["makespan"][0]) == O.simulate_wave(vb.item(0), cz, lz)["makespan"]
+    big = K.uniform_instance(32, 257, 4, 100, 100, 100, mlim_x1000=10**6)
+    bo, bl = PL.wave_plans_device(32, 257, 1, 1, seed=62, stride=32)
+    with pytest.raises(RuntimeError):
+        cp.simulate(cp.Instances(big), bo, bl, wave=True)
