@@ -114,8 +114,8 @@ def load():
     L.cp_exact_workspace_bytes.restype = C.c_size_t
     L.cp_exact_workspace_bytes.argtypes = [C.c_int32, C.c_int32]
     L.cp_exact.restype = C.c_int32
-    L.cp_exact.argtypes = [P(CpInstances), P(CpSchedules), C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p,
-                           C.c_size_t, C.c_void_p]
+    L.cp_exact.argtypes = [P(CpInstances), P(CpSchedules), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
+                           C.c_void_p, C.c_size_t, C.c_void_p]
     L.cp_quantize.restype = C.c_int32
     L.cp_quantize.argtypes = [P(CpSpecSI), C.c_void_p]
     L.cp_validate_instance.restype = C.c_int32

@@ -232,10 +232,12 @@ def build_static(kind: str, inst: Instances, n=None, inst_of=None, *, stage_stri
     return ops, ln
 
 
-def exact(inst: Instances, *, cap=65536, max_plans=1 << 32, stage_stride=None, stream=None):
+def exact(inst: Instances, *, cap=65536, max_plans=1 << 32, upper=None, stage_stride=None, stream=None):
     """cp_exact: the makespan-optimal split plan (n_sub = 1) of every (tiny) instance by exhaustive
     search on the GPU -> dict(ops int32 [n, words, stride], len int16 [n, stride], makespan, status).
-    Plans are in simulate()'s layout; status CPI_OVERFLOW (16) marks instances beyond the limits."""
+    Plans are in simulate()'s layout; status CPI_OVERFLOW (16) marks instances beyond the limits.
+    upper: optional int32 [n] device tensor of feasible makespans (e.g. greedy(inst)["makespan"] for
+    n_sub = 1 instances) seeding the search's cut; the result does not change."""
     _require_cuda(inst.dev)
     dev = inst.dev.device
     n = inst.n
@@ -249,7 +251,8 @@ def exact(inst: Instances, *, cap=65536, max_plans=1 << 32, stage_stride=None, s
     ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
     d = inst.desc(None)
     sc = L.CpSchedules(n, stride, words, 0, None, ops.data_ptr(), ln.data_ptr())
-    L.check(L.load().cp_exact(C.byref(d), C.byref(sc), C.c_void_p(ms.data_ptr()), C.c_void_p(st.data_ptr()), cap,
+    up = None if upper is None else upper.to(device=dev, dtype=torch.int32).contiguous()
+    L.check(L.load().cp_exact(C.byref(d), C.byref(sc), _ptr(up), C.c_void_p(ms.data_ptr()), C.c_void_p(st.data_ptr()), cap,
                               int(max_plans), C.c_void_p(ws.data_ptr()), nb, _stream(stream)), "cp_exact")
     return {"ops": ops, "len": ln, "makespan": ms, "status": st}
 

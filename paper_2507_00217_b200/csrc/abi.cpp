@@ -375,18 +375,18 @@ size_t cp_exact_workspace_bytes(int32_t n, int32_t cap) {
   return n < 1 || cap < 1 ? 0 : cpk::exact_ws_bytes(n, cap);
 }
 
-int32_t cp_exact(const cp_instances* in, const cp_schedules* out, int32_t* makespan, int32_t* status, int32_t cap,
-                 int64_t max_plans, void* ws, size_t ws_bytes, void* stream) {
+int32_t cp_exact(const cp_instances* in, const cp_schedules* out, const int32_t* upper, int32_t* makespan,
+                 int32_t* status, int32_t cap, int64_t max_plans, void* ws, size_t ws_bytes, void* stream) {
   int rc = check_instances(in);
   if (rc) return rc;
   if (!out || out->n != in->n || out->inst_of || !out->ops || !out->len || !makespan || !status) return CP_EINVAL;
   if (out->stage_stride < in->max_pp || out->words < 1 || 16LL * out->words < 3LL * std::min(in->max_mb, 8))
     return CP_EINVAL;
-  if (cap < 1 || max_plans < 1 || max_plans > (1LL << 36)) return CP_EINVAL;
+  if (cap < 1 || max_plans < 1 || max_plans >= (1LL << 36)) return CP_EINVAL;
   if (in->n == 0) return CP_OK;
   if (!ws || ws_bytes < cpk::exact_ws_bytes(in->n, cap)) return CP_EWORKSPACE;
-  return cpk::launch_exact(in->inst, in->n, cap, max_plans, ws, out->stage_stride, out->words, out->ops, out->len,
-                           makespan, status, stream) == cudaSuccess ? CP_OK : CP_ECUDA;
+  return cpk::launch_exact(in->inst, in->n, cap, max_plans, upper, ws, out->stage_stride, out->words, out->ops,
+                           out->len, makespan, status, stream) == cudaSuccess ? CP_OK : CP_ECUDA;
 }
 
 int32_t cp_greedy(const cp_instances* in, const cp_schedules* out, const cp_results* res, void* ws, size_t ws_bytes,

@@ -75,8 +75,9 @@ int launch_build_static(int kind, const cp_inst_v1* inst, int n_inst, const int3
 // cp_exact (exact.cu): batched exhaustive search for tiny instances
 constexpr int kExactMaxP = 8;          // stages
 constexpr int kExactMaxM = 8;          // microbatches (3m <= 24 entries: one uint64 per stage sequence)
-int launch_exact(const cp_inst_v1* inst, int n, int cap, long long max_plans, void* ws, int stride, int words,
-                 uint32_t* ops, uint16_t* len, int32_t* makespan, int32_t* status, void* stream);
+int launch_exact(const cp_inst_v1* inst, int n, int cap, long long max_plans, const int32_t* upper, void* ws,
+                 int stride, int words, uint32_t* ops, uint16_t* len, int32_t* makespan, int32_t* status,
+                 void* stream);
 size_t exact_ws_seq_bytes(int n, int cap);
 size_t exact_ws_bytes(int n, int cap);
 int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, long long inner, int own_lo,

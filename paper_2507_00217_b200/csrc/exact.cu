@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(128) k_exact_sets(const cp_inst_v1* __restrict
 }
 
 __global__ void k_exact_prep(const cp_inst_v1* __restrict__ inst, int n, int cap, long long max_plans,
-                             const int32_t* __restrict__ cnt, long long* __restrict__ total,
+                             const int32_t* __restrict__ upper, const int32_t* __restrict__ cnt,
+                             long long* __restrict__ total,
                              long long* __restrict__ chunks, int32_t* __restrict__ status,
                              unsigned long long* __restrict__ keys) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
@@ -103,7 +104,10 @@ __global__ void k_exact_prep(const cp_inst_v1* __restrict__ inst, int n, int cap
   total[item] = tot;
   chunks[item] = (tot + kExactChunk - 1) / kExactChunk;
   status[item] = st;
-  keys[item] = kExactNone;
+  // a known feasible makespan U (e.g. the greedy's) seeds the incumbent as (U << 36 | max index): plans
+  // longer than U are cut from the start, and any plan of makespan <= U replaces it
+  const int ub = upper ? upper[item] : -1;
+  keys[item] = ub >= 0 && ub < (1 << 28) ? (((unsigned long long)ub << 36) | ((1ull << 36) - 1)) : kExactNone;
 }
 
 // exclusive prefix over the chunk counts (one thread; n is at most a few thousand tiny searches)
@@ -219,7 +223,7 @@ __global__ void k_exact_finish(const cp_inst_v1* __restrict__ inst, int n, int c
   const int item = (int)(t / stride), s = (int)(t % stride);
   const int p = inst[item].n_pp, m = inst[item].n_mb;
   const unsigned long long key = keys[item];
-  const bool found = status[item] == 0 && key != kExactNone;
+  const bool found = status[item] == 0 && key != kExactNone && (key & ((1ull << 36) - 1)) != (1ull << 36) - 1;
   unsigned long long sq = 0;
   int L = 0;
   if (found && s < p) {
@@ -238,8 +242,9 @@ __global__ void k_exact_finish(const cp_inst_v1* __restrict__ inst, int n, int c
   }
 }
 
-int launch_exact(const cp_inst_v1* inst, int n, int cap, long long max_plans, void* ws, int stride, int words,
-                 uint32_t* ops, uint16_t* len, int32_t* makespan, int32_t* status, void* stream) {
+int launch_exact(const cp_inst_v1* inst, int n, int cap, long long max_plans, const int32_t* upper, void* ws,
+                 int stride, int words, uint32_t* ops, uint16_t* len, int32_t* makespan, int32_t* status,
+                 void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   char* b = (char*)ws;
   unsigned long long* seqs = (unsigned long long*)b;   b += exact_ws_seq_bytes(n, cap);
@@ -249,7 +254,7 @@ int launch_exact(const cp_inst_v1* inst, int n, int cap, long long max_plans, vo
   unsigned long long* keys = (unsigned long long*)b;
   const long long nt = (long long)n * kExactMaxP;
   k_exact_sets<<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(inst, n, cap, seqs, cnt);
-  k_exact_prep<<<(n + 127) / 128, 128, 0, st>>>(inst, n, cap, max_plans, cnt, total, chunks, status, keys);
+  k_exact_prep<<<(n + 127) / 128, 128, 0, st>>>(inst, n, cap, max_plans, upper, cnt, total, chunks, status, keys);
   k_exact_scan<<<1, 1, 0, st>>>(n, chunks);
   k_exact_eval<<<device_sm_count() * 8, 128, 0, st>>>(inst, n, cap, seqs, cnt, total, chunks, keys);
   const long long nr = (long long)n * stride;

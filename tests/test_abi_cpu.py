@@ -143,11 +143,11 @@ def test_argument_errors_before_any_device_work():
     assert lib.cp_build_static(4, C.byref(inst), C.byref(good), None) == L.CP_EINVAL          # kind 4: no static family
     assert lib.cp_build_static(7, C.byref(inst), C.byref(L.CpSchedules(4, 4, 1, 0, None, fake.value, fake.value)),
                                None) == L.CP_EINVAL                                           # ZB-V: 8 entries < 6 * max_mb
-    assert lib.cp_exact(None, C.byref(good), ms, st, 16, 100, None, 0, None) == L.CP_EINVAL
-    assert lib.cp_exact(C.byref(inst), C.byref(good), ms, st, 0, 100, None, 0, None) == L.CP_EINVAL     # cap < 1
-    assert lib.cp_exact(C.byref(inst), C.byref(good), ms, st, 16, 1 << 37, None, 0, None) == L.CP_EINVAL
-    assert lib.cp_exact(C.byref(inst), C.byref(L.CpSchedules(3, 4, 2, 0, None, fake.value, fake.value)), ms, st, 16,
-                        100, None, 0, None) == L.CP_EINVAL                                    # n mismatch
-    assert lib.cp_exact(C.byref(inst), C.byref(good), ms, st, 16, 100, None, 0, None) == L.CP_EWORKSPACE
+    assert lib.cp_exact(None, C.byref(good), None, ms, st, 16, 100, None, 0, None) == L.CP_EINVAL
+    assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 0, 100, None, 0, None) == L.CP_EINVAL   # cap < 1
+    assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 16, 1 << 37, None, 0, None) == L.CP_EINVAL
+    assert lib.cp_exact(C.byref(inst), C.byref(L.CpSchedules(3, 4, 2, 0, None, fake.value, fake.value)), None, ms, st,
+                        16, 100, None, 0, None) == L.CP_EINVAL                                # n mismatch
+    assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 16, 100, None, 0, None) == L.CP_EWORKSPACE
     assert lib.cp_exact_workspace_bytes(0, 16) == 0
     assert lib.cp_exact_workspace_bytes(4, 16) >= 4 * 8 * 16 * 8

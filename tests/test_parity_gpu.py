@@ -815,6 +815,13 @@ def test_exact_search_bounds_greedy(O):
         assert O.simulate(d, codes[i, :d["p"]], lens[i, :d["p"]])["makespan"] == ms[i]
         assert ms[i] <= int(g["makespan"][i])
         assert ms[i] <= O.simulate(d, *O.build_static("1f1b", d["p"], d["m"]))["makespan"]
+    # a warm start from the greedy's makespan (n_sub = 1: one of the enumerated plans) changes nothing
+    w = cp.exact(inst, upper=g["makespan"])
+    assert torch.equal(w["makespan"], r["makespan"]) and torch.equal(w["ops"], r["ops"])
+    assert torch.equal(w["status"], r["status"])
+    # an upper bound no plan reaches reports DEADLOCK (include/crosspipe.h)
+    lo = cp.exact(inst, upper=r["makespan"] - 1)
+    assert (lo["status"].cpu().numpy() == 1).all()
 
 
 def test_two_chunk_plans_at_the_size_limit(O):

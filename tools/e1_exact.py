@@ -19,8 +19,11 @@ mk = lambda ns: InstanceBatch.concat([K.uniform_instance(4, m, 2, f, f, f, lat=i
                                       for (a, b) in pts])
 ex_inst = cp.Instances(mk(1))
 torch.cuda.synchronize()
+# warm start: the greedy's n_sub = 1 makespan (a plan of the enumerated set) seeds the cut
+g1 = cp.greedy(ex_inst)["makespan"]
+torch.cuda.synchronize()
 t0 = time.perf_counter()
-ex = cp.exact(ex_inst, max_plans=1 << 36)
+ex = cp.exact(ex_inst, max_plans=(1 << 36) - 1, upper=g1)
 torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 ems, est = ex["makespan"].cpu().numpy(), ex["status"].cpu().numpy()
