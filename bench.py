@@ -63,12 +63,23 @@ def int_peak(sm_max_mhz):
         return 148 * 4 * 32 * sm_max_mhz * 1e6 / 1e12, "fallback (unit counts x clock)"
 
 
-def traffic_per_launch():
+def traffic_per_launch(key="simulate_config4_bytes_per_launch"):
     try:
         with open(TRAFFIC_FILE) as f:
-            return json.load(f).get("simulate_config4_bytes_per_launch")
+            return json.load(f).get(key)
     except Exception:
         return None
+
+
+def issue_roofline(evals_per_s, sm_hz):
+    ipe = traffic_per_launch("simulate_config4_warp_instructions_per_eval")
+    if not ipe or not sm_hz:
+        return None
+    peak = 148 * 4 * sm_hz                       # warp-instructions/s: 148 SMs x 4 schedulers x SM clock
+    ach = ipe * evals_per_s
+    return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-instr/s", "frac": ach / peak,
+            "instructions_per_eval": ipe, "source": "ncu smsp__inst_executed.sum (profiles/ncu_sim32_v13_r01.txt)",
+            "sm_clock_hz": sm_hz}
 
 
 class Clocks:
@@ -283,6 +294,8 @@ def run_ours(args):
     ms_local = e0.elapsed_time(e1)
     kern_ms = statistics.mean(a.elapsed_time(b_) for a, b_ in ks)
     clk = clocks.stop() if clocks else None
+    sm_clk_hz = (clk or {}).get("sm_mhz")
+    sm_clk_hz = sm_clk_hz * 1e6 if sm_clk_hz else None
     ms_tot = max_over_ranks(ms_local, ws)
     kern_ms = max_over_ranks(kern_ms, ws)
     value = ws * n * args.steps / (ms_tot / 1e3)
@@ -428,6 +441,9 @@ def run_ours(args):
                          "frac": alu_ach / alu_peak, "traffic": traffic_per_launch(),
                          "peak_source": alu_src, "kernel": "k_sim32 (cp_simulate fast path)",
                          "kernel_ms": kern_ms, "ops_per_eval": OPS_PER_EVAL, "evals_per_launch": n},
+            # the integer-issue ceiling SURVEY.md §8(d) names: 4 warp-instructions per clock per SM; the
+            # instructions per evaluation come from the committed ncu capture (profiles/traffic.json)
+            "roofline_issue": issue_roofline(value / ws, sm_clk_hz),       # per GPU
             "roofline_hbm": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved / hbm_peak, "traffic": traffic_per_launch(),
                              "peak_source": peak_src, "bytes_per_eval": BYTES_PER_EVAL},
