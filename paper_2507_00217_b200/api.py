@@ -257,6 +257,23 @@ def exact(inst: Instances, *, cap=65536, max_plans=1 << 32, upper=None, stage_st
     return {"ops": ops, "len": ln, "makespan": ms, "status": st}
 
 
+def bubble_ratios(result: dict, n_pp):
+    """Per-stage bubble ratios from simulate(..., stats=True) (reading Q7): local =
+    1 - busy / (last_end - first_start) over the stage's active window, global = 1 - busy / makespan.
+    n_pp: int or int tensor [n]; stages >= n_pp and items without a completed timeline give NaN.
+    Returns (local, global), float64 tensors [n, stride] on the result's device."""
+    st = result["stage_stats"].to(torch.float64)            # [n, stride, 4]: first, last, busy, peak
+    ms = result["makespan"].to(torch.float64)[:, None]
+    n, stride = st.shape[0], st.shape[1]
+    pp = torch.as_tensor(n_pp, device=st.device).reshape(-1, 1)
+    on = (torch.arange(stride, device=st.device)[None, :] < pp) & (result["status"][:, None] & ~2 == 0) & (ms > 0)
+    win = st[..., 1] - st[..., 0]
+    nan = torch.full_like(win, float("nan"))
+    loc = torch.where(on & (win > 0), 1 - st[..., 2] / win.clamp(min=1), nan)
+    glo = torch.where(on, 1 - st[..., 2] / ms.clamp(min=1), nan)
+    return loc, glo
+
+
 def to_cp_grid(grid) -> L.CpGrid:
     """workloads.Grid -> cp_grid (host struct, passed to the kernel by value)."""
     g = L.CpGrid()

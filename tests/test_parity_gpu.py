@@ -855,3 +855,29 @@ def test_two_chunk_plans_at_the_size_limit(O):
     bo, bl = PL.wave_plans_device(32, 257, 1, 1, seed=62, stride=32)
     with pytest.raises(RuntimeError):
         cp.simulate(cp.Instances(big), bo, bl, wave=True)
+
+
+def test_bubble_ratios(O):
+    """cp.bubble_ratios (reading Q7) from the GPU stage stats == the ratios formed
+    from the oracle's per-stage first / last / busy / makespan; SPEC.md:544 acceptance 1: 1F1B p = 4,
+    m = 8, t_f = 1, t_d + t_w = 2, zero delay -> stage-0 ratio 9/33."""
+    from tests.helpers_independent import bubble
+    batch = K.random_instances(60, seed=71, max_p=32, max_m=6, intra_delay=True)
+    inst = cp.Instances(batch)
+    g = cp.greedy(inst, stats=True)
+    loc, glo = cp.bubble_ratios(g, torch.from_numpy(batch.p[:60].astype(np.int64)).cuda())
+    loc, glo = loc.cpu().numpy(), glo.cpu().numpy()
+    for i in range(60):
+        d = batch.item(i)
+        r = O.greedy(d)
+        if r["status"] & ~2:
+            assert np.isnan(glo[i]).all(); continue
+        for s in range(d["p"]):
+            el, eg = bubble(r["first_start"][s], r["last_end"][s], r["busy"][s], r["makespan"])
+            assert abs(glo[i, s] - eg) < 1e-12 and (abs(loc[i, s] - el) < 1e-12 or (np.isnan(loc[i, s]) and el != el)), (i, s)
+    d = K.uniform_instance(4, 8, 1, 1, 1, 1, mlim_x1000=10**6)
+    c, l_ = O.build_static("1f1b", 4, 8)
+    o, l2 = plans_to_device(*codes_list_to_packed([[list(c[s, :l_[s]]) for s in range(4)]], stride=4))
+    r = cp.simulate(cp.Instances(d), o, l2, stats=True)
+    loc, glo = cp.bubble_ratios(r, 4)
+    assert int(r["makespan"][0]) == 33 and abs(float(glo[0, 0]) - 9 / 33) < 1e-9
