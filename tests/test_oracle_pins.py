@@ -214,6 +214,10 @@ def test_appendix_c_bubble_strides(oracle_lib):
     r1 = oracle_lib.simulate(inst(p, m, 2, TF, TF, TF, lat=g["lat"], mlim_x1000=1000), c, ln)
     assert r0["makespan"] == (m + p - 1) * 3 * TF
     assert r1["makespan"] - r0["makespan"] > 1.5 * TF
+    # SPEC.md:550 "critical-path crossing count >= 2": the makespan is piecewise linear in the boundary
+    # latency with slope = the number of DC-boundary crossings on the critical path (one tick apart)
+    r2 = oracle_lib.simulate(inst(p, m, 2, TF, TF, TF, lat=g["lat"] + 1, mlim_x1000=1000), c, ln)
+    assert r2["makespan"] - r1["makespan"] >= 2
     gr0 = oracle_lib.greedy(inst(p, m, 2, TF, TF, TF))
     gr1 = oracle_lib.greedy(inst(p, m, 2, TF, TF, TF, lat=g["lat"]))
     assert gr0["makespan"] == (3 * m + p - 1) * TF                  # Z6
