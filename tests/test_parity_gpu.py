@@ -881,3 +881,13 @@ def test_bubble_ratios(O):
     r = cp.simulate(cp.Instances(d), o, l2, stats=True)
     loc, glo = cp.bubble_ratios(r, 4)
     assert int(r["makespan"][0]) == 33 and abs(float(glo[0, 0]) - 9 / 33) < 1e-9
+
+
+def test_e1_grid_every_point(O):
+    """The E1 delay-sensitivity grid of PAPER.md §5.1 (4 stages / 2 DCs / 8 microbatches, T_lat/T_F x
+    T_bw/T_F on 33 x 33 values in [0, 4], six candidates) -- every point and every candidate against
+    the oracle (the table `tools/e1_grid.py` reports)."""
+    grid = K.e1_grid()
+    keys, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
