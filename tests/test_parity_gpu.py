@@ -266,25 +266,24 @@ def test_sweep_tiny_grid(O):
     check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
 
 
-def test_sweep_config2_sample(O):
-    """Config 2 (16 stages / 2 DCs / 32 mb, 64 x 64 latency x bandwidth): 300 sampled points,
-    each checked candidate by candidate."""
+def test_sweep_config2_every_point(O):
+    """Config 2 (16 stages / 2 DCs / 32 mb, 64 x 64 latency x bandwidth): every point, each checked
+    candidate by candidate."""
     grid = K.gpt16_grid()
     keys, cm = cp.sweep_shard(grid, cand=True)
     torch.cuda.synchronize()
-    pts = np.random.default_rng(16).choice(grid.n_points, 300, replace=False)
-    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), pts)
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
 
 
 def test_sweep_config5_sample_and_shards(O):
-    """Config 5 (4 DCs, p 8-32, m 8-128, memory grid): sampled points; shards over 1/2/4/8
+    """Config 5 (4 DCs, p 8-32, m 8-128, memory grid): 400 sampled points; shards over 1/2/4/8
     cost-balanced ranges assembled with MIN give byte-identical keys."""
     grid = K.full_sweep_grid()
     full, cm = cp.sweep_shard(grid, cand=True)
     torch.cuda.synchronize()
     full_h = full.cpu().numpy()
     rng = np.random.default_rng(17)
-    pts = np.concatenate([rng.choice(grid.n_points, 120, replace=False)])
+    pts = np.concatenate([rng.choice(grid.n_points, 400, replace=False)])
     check_sweep(O, grid, full_h, cm.cpu().numpy(), pts)
     for world in (2, 4, 8):
         b = cp.sweep_partition(grid, world)
