@@ -209,8 +209,9 @@ int32_t cp_build_static(int32_t kind, const cp_instances* inst, const cp_schedul
  * D_j and the memory capacity m_lim along the sequence is enumerated and simulated (cp_simulate's
  * model), and the makespan-optimal plan is returned -- the first optimum in the order "stage sequences
  * in lexicographic order F < D < W, the last stage varying fastest".  Deadlocking plans are skipped.
- * Limits: n_pp <= 8, n_mb <= 8, at most `cap` valid sequences per stage and `max_plans` (< 2^36)
- * plans per instance, horizon < 2^28 ticks; an instance beyond them gets status CPI_OVERFLOW and
+ * Limits: n_pp <= 8, n_mb <= 8, at most `cap` valid sequences per stage and `max_plans` (< 2^52)
+ * plans per instance, horizon < 2^30 ticks and < 2^(63 - ceil(log2 plans)) (the packed key);
+ * an instance beyond them gets status CPI_OVERFLOW and
  * makespan -1; one without any completing plan CPI_DEADLOCK.
  * upper (nullable, device) [n] int32: a known feasible makespan per instance (e.g. cp_greedy's with
  * n_sub = 1), -1 for none; it only seeds the search's cut (plans longer than it are skipped early),
@@ -219,7 +220,7 @@ int32_t cp_build_static(int32_t kind, const cp_instances* inst, const cp_schedul
  * out: n == inst->n, inst_of NULL, stage_stride >= max_pp, 16*words >= 3*max_mb; every word and
  * row is written (2-bit entries, zero past 3m and for rows >= n_pp).  makespan, status: [n] int32.
  * ws: cp_exact_workspace_bytes(n, cap) bytes (n * 8 * cap * 8 B of sequences).  Errors: CP_EINVAL
- * for NULL / inconsistent arguments, cap < 1, max_plans outside [1, 2^36); CP_EWORKSPACE.
+ * for NULL / inconsistent arguments, cap < 1, max_plans outside [1, 2^52); CP_EWORKSPACE.
  * Enqueued on `stream`, no sync. */
 size_t cp_exact_workspace_bytes(int32_t n, int32_t cap);
 int32_t cp_exact(const cp_instances* inst, const cp_schedules* out, const int32_t* upper, int32_t* makespan,

@@ -382,7 +382,7 @@ int32_t cp_exact(const cp_instances* in, const cp_schedules* out, const int32_t*
   if (!out || out->n != in->n || out->inst_of || !out->ops || !out->len || !makespan || !status) return CP_EINVAL;
   if (out->stage_stride < in->max_pp || out->words < 1 || 16LL * out->words < 3LL * std::min(in->max_mb, 8))
     return CP_EINVAL;
-  if (cap < 1 || max_plans < 1 || max_plans >= (1LL << 36)) return CP_EINVAL;
+  if (cap < 1 || max_plans < 1 || max_plans >= (1LL << 52)) return CP_EINVAL;
   if (in->n == 0) return CP_OK;
   if (!ws || ws_bytes < cpk::exact_ws_bytes(in->n, cap)) return CP_EWORKSPACE;
   return cpk::launch_exact(in->inst, in->n, cap, max_plans, upper, ws, out->stage_stride, out->words, out->ops,

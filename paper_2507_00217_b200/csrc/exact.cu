@@ -14,8 +14,9 @@
 //    sequentially (§3.5 start-time rule, FIFO link windows = first fit under UD, App. X1; ZeRO-1
 //    gate; DP tail).  A plan is abandoned once a stage's clock + its remaining work + its DP tail
 //    exceeds the instance's best makespan so far (strictly, so equal-makespan plans survive), and
-//    the finished ones race on a 64-bit atomicMin of (makespan << 36 | product index): the result
-//    is the smallest-index optimum, independent of thread timing.
+//    the finished ones race on a 64-bit atomicMin of (makespan << b | product index), b = the bits of
+//    the instance's product size: the result is the smallest-index optimum, independent of thread
+//    timing.
 // 4. k_exact_finish: decodes each instance's key into its plan (packed rows) and makespan.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(128) k_exact_sets(const cp_inst_v1* __restrict
 
 __global__ void k_exact_prep(const cp_inst_v1* __restrict__ inst, int n, int cap, long long max_plans,
                              const int32_t* __restrict__ upper, const int32_t* __restrict__ cnt,
-                             long long* __restrict__ total,
+                             int32_t* __restrict__ ibits, long long* __restrict__ total,
                              long long* __restrict__ chunks, int32_t* __restrict__ status,
                              unsigned long long* __restrict__ keys) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
@@ -93,21 +94,28 @@ __global__ void k_exact_prep(const cp_inst_v1* __restrict__ inst, int n, int cap
   }
   long long tot = 1;
   if (bad) st = CPI_BAD_INSTANCE;
-  else if (ns != 1 || p > kExactMaxP || m > kExactMaxM || u >= (1LL << 28)) st = CPI_OVERFLOW;
+  else if (ns != 1 || p > kExactMaxP || m > kExactMaxM || u >= (1LL << 30)) st = CPI_OVERFLOW;
   else
     for (int s = 0; s < p; ++s) {
       const long long c = cnt[(long long)item * kExactMaxP + s];
       if (c > cap || c < 1 || tot > max_plans / c) { st = CPI_OVERFLOW; break; }
       tot *= c;
     }
+  // key = makespan << b | index: b bits hold every index and the sentinel 2^b - 1 (> the last index),
+  // the remaining 64 - b bits must hold the horizon
+  int b = 1;
+  while (b < 62 && (1LL << b) <= tot) ++b;
+  if (!st && (64 - b >= 31 ? false : u >= (1LL << (64 - b)) - 1)) st = CPI_OVERFLOW;
   if (st) tot = 0;
+  ibits[item] = b;
   total[item] = tot;
   chunks[item] = (tot + kExactChunk - 1) / kExactChunk;
   status[item] = st;
   // a known feasible makespan U (e.g. the greedy's) seeds the incumbent as (U << 36 | max index): plans
   // longer than U are cut from the start, and any plan of makespan <= U replaces it
   const int ub = upper ? upper[item] : -1;
-  keys[item] = ub >= 0 && ub < (1 << 28) ? (((unsigned long long)ub << 36) | ((1ull << 36) - 1)) : kExactNone;
+  const bool seed = ub >= 0 && !st && (64 - b >= 31 || ub < (1LL << (64 - b)) - 1);
+  keys[item] = seed ? (((unsigned long long)ub << b) | ((1ull << b) - 1)) : kExactNone;
 }
 
 // exclusive prefix over the chunk counts (one thread; n is at most a few thousand tiny searches)
@@ -120,6 +128,7 @@ __global__ void k_exact_scan(int n, long long* __restrict__ chunks) {
 __global__ void __launch_bounds__(128) k_exact_eval(const cp_inst_v1* __restrict__ inst, int n, int cap,
                                                     const unsigned long long* __restrict__ seqs,
                                                     const int32_t* __restrict__ cnt,
+                                                    const int32_t* __restrict__ ibits,
                                                     const long long* __restrict__ total,
                                                     const long long* __restrict__ chunk_off,
                                                     unsigned long long* __restrict__ keys) {
@@ -130,7 +139,7 @@ __global__ void __launch_bounds__(128) k_exact_eval(const cp_inst_v1* __restrict
     while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (chunk_off[mid] <= c) lo = mid; else hi = mid - 1; }
     const int item = lo;
     const cp_inst_v1* I = inst + item;
-    const int p = I->n_pp, m = I->n_mb, L = 3 * m;
+    const int p = I->n_pp, m = I->n_mb, L = 3 * m, ib = ibits[item];
     const long long i0 = (c - chunk_off[item]) * kExactChunk;
     const long long i1 = min(i0 + kExactChunk, total[item]);
     const bool zero1 = I->flags & 1;
@@ -223,7 +232,8 @@ __global__ void __launch_bounds__(128) k_exact_eval(const cp_inst_v1* __restrict
     // the stage digits that changed since the last prefix test (all at the chunk start)
     int chg = 0;
     for (long long idx = i0; idx < i1;) {
-      const int best = (int)(*(volatile unsigned long long*)&keys[item] >> 36);   // racy incumbent: a bound only
+      const unsigned long long bk = *(volatile unsigned long long*)&keys[item] >> ib;   // racy incumbent: a bound only
+      const int best = bk > 0x7fffffffull ? 0x7fffffff : (int)bk;
       // Test the deepest prefix (stages 0..p-2, the last stage relaxed) whenever it changed.  A chunk
       // covers 64 plans, so a cut at a shallower level could skip no further than the chunk's end:
       // testing those levels too measured slower (m = 4 E1 replicas 4.1 s against 2.8 s).
@@ -247,7 +257,7 @@ __global__ void __launch_bounds__(128) k_exact_eval(const cp_inst_v1* __restrict
       chg = p - 1;                                               // (no prefix left to test at this plan)
       const int ms = simulate(p, best);
       if (ms >= 0) {
-        const unsigned long long key = ((unsigned long long)ms << 36) | (unsigned long long)idx;
+        const unsigned long long key = ((unsigned long long)ms << ib) | (unsigned long long)idx;
         if (key < *(volatile unsigned long long*)&keys[item]) atomicMin(&keys[item], key);
       }
       for (int s = p - 1; s >= 0; --s) {                         // odometer, last stage fastest
@@ -263,6 +273,7 @@ __global__ void __launch_bounds__(128) k_exact_eval(const cp_inst_v1* __restrict
 
 __global__ void k_exact_finish(const cp_inst_v1* __restrict__ inst, int n, int cap,
                                const unsigned long long* __restrict__ seqs, const int32_t* __restrict__ cnt,
+                               const int32_t* __restrict__ ibits,
                                const unsigned long long* __restrict__ keys, int stride, int words,
                                uint32_t* __restrict__ ops, uint16_t* __restrict__ len, int32_t* __restrict__ makespan,
                                int32_t* __restrict__ status) {
@@ -271,11 +282,13 @@ __global__ void k_exact_finish(const cp_inst_v1* __restrict__ inst, int n, int c
   const int item = (int)(t / stride), s = (int)(t % stride);
   const int p = inst[item].n_pp, m = inst[item].n_mb;
   const unsigned long long key = keys[item];
-  const bool found = status[item] == 0 && key != kExactNone && (key & ((1ull << 36) - 1)) != (1ull << 36) - 1;
+  const int ib = ibits[item];
+  const unsigned long long imask = (1ull << ib) - 1;
+  const bool found = status[item] == 0 && key != kExactNone && (key & imask) != imask;
   unsigned long long sq = 0;
   int L = 0;
   if (found && s < p) {
-    long long r = (long long)(key & ((1ull << 36) - 1));
+    long long r = (long long)(key & imask);
     int d = 0;
     for (int q = p - 1; q >= s; --q) { const int c = cnt[(long long)item * kExactMaxP + q]; d = (int)(r % c); r /= c; }
     sq = seqs[((long long)item * kExactMaxP + s) * cap + d];
@@ -285,7 +298,7 @@ __global__ void k_exact_finish(const cp_inst_v1* __restrict__ inst, int n, int c
   for (int k = 0; k < words; ++k) row[(long long)k * stride] = k < 2 ? (uint32_t)(sq >> (32 * k)) : 0u;
   len[t] = (uint16_t)L;
   if (s == 0) {
-    makespan[item] = found ? (int32_t)(key >> 36) : -1;
+    makespan[item] = found ? (int32_t)(key >> ib) : -1;
     if (status[item] == 0 && !found) status[item] = CPI_DEADLOCK;
   }
 }
@@ -299,14 +312,16 @@ int launch_exact(const cp_inst_v1* inst, int n, int cap, long long max_plans, co
   int32_t* cnt = (int32_t*)b;                          b += ((size_t)n * kExactMaxP * 4 + 255) & ~(size_t)255;
   long long* total = (long long*)b;                    b += ((size_t)n * 8 + 255) & ~(size_t)255;
   long long* chunks = (long long*)b;                   b += ((size_t)(n + 1) * 8 + 255) & ~(size_t)255;
-  unsigned long long* keys = (unsigned long long*)b;
+  unsigned long long* keys = (unsigned long long*)b;   b += ((size_t)n * 8 + 255) & ~(size_t)255;
+  int32_t* ibits = (int32_t*)b;
   const long long nt = (long long)n * kExactMaxP;
   k_exact_sets<<<(unsigned)((nt + 127) / 128), 128, 0, st>>>(inst, n, cap, seqs, cnt);
-  k_exact_prep<<<(n + 127) / 128, 128, 0, st>>>(inst, n, cap, max_plans, upper, cnt, total, chunks, status, keys);
+  k_exact_prep<<<(n + 127) / 128, 128, 0, st>>>(inst, n, cap, max_plans, upper, cnt, ibits, total, chunks, status,
+                                                 keys);
   k_exact_scan<<<1, 1, 0, st>>>(n, chunks);
-  k_exact_eval<<<device_sm_count() * 8, 128, 0, st>>>(inst, n, cap, seqs, cnt, total, chunks, keys);
+  k_exact_eval<<<device_sm_count() * 8, 128, 0, st>>>(inst, n, cap, seqs, cnt, ibits, total, chunks, keys);
   const long long nr = (long long)n * stride;
-  k_exact_finish<<<(unsigned)((nr + 127) / 128), 128, 0, st>>>(inst, n, cap, seqs, cnt, keys, stride, words, ops, len,
+  k_exact_finish<<<(unsigned)((nr + 127) / 128), 128, 0, st>>>(inst, n, cap, seqs, cnt, ibits, keys, stride, words, ops, len,
                                                                 makespan, status);
   return (int)cudaGetLastError();
 }
@@ -316,7 +331,7 @@ size_t exact_ws_seq_bytes(int n, int cap) { return ((size_t)n * kExactMaxP * cap
 size_t exact_ws_bytes(int n, int cap) {
   return exact_ws_seq_bytes(n, cap) + (((size_t)n * kExactMaxP * 4 + 255) & ~(size_t)255) +
          (((size_t)n * 8 + 255) & ~(size_t)255) + (((size_t)(n + 1) * 8 + 255) & ~(size_t)255) +
-         (((size_t)n * 8 + 255) & ~(size_t)255);
+         (((size_t)n * 8 + 255) & ~(size_t)255) + (((size_t)n * 4 + 255) & ~(size_t)255);
 }
 
 }  // namespace cpk

@@ -145,7 +145,7 @@ def test_argument_errors_before_any_device_work():
                                None) == L.CP_EINVAL                                           # ZB-V: 8 entries < 6 * max_mb
     assert lib.cp_exact(None, C.byref(good), None, ms, st, 16, 100, None, 0, None) == L.CP_EINVAL
     assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 0, 100, None, 0, None) == L.CP_EINVAL   # cap < 1
-    assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 16, 1 << 37, None, 0, None) == L.CP_EINVAL
+    assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 16, 1 << 53, None, 0, None) == L.CP_EINVAL
     assert lib.cp_exact(C.byref(inst), C.byref(L.CpSchedules(3, 4, 2, 0, None, fake.value, fake.value)), None, ms, st,
                         16, 100, None, 0, None) == L.CP_EINVAL                                # n mismatch
     assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 16, 100, None, 0, None) == L.CP_EWORKSPACE

@@ -23,7 +23,7 @@ torch.cuda.synchronize()
 g1 = cp.greedy(ex_inst)["makespan"]
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-ex = cp.exact(ex_inst, max_plans=(1 << 36) - 1, upper=g1)
+ex = cp.exact(ex_inst, max_plans=(1 << 51), upper=g1)
 torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 ems, est = ex["makespan"].cpu().numpy(), ex["status"].cpu().numpy()

@@ -19,7 +19,7 @@ inst = cp.Instances(b)
 g1 = cp.greedy(inst)
 torch.cuda.synchronize()
 t0 = time.perf_counter()
-ex = cp.exact(inst, upper=g1["makespan"], max_plans=(1 << 36) - 1)
+ex = cp.exact(inst, upper=g1["makespan"], max_plans=(1 << 51))
 torch.cuda.synchronize()
 dt = time.perf_counter() - t0
 best = g1["makespan"].cpu().numpy().astype(np.int64)
