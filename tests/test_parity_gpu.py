@@ -55,6 +55,27 @@ def test_simulate_random_valid_plans(O, max_p, seed):
     assert np.all(r["status"] == 0)
 
 
+@pytest.mark.parametrize("seed", [81, 82])
+def test_simulate_fast_path_random_valid_plans(O, seed):
+    """The bench kernel k_sim32 (stats only, stage stride 32, no timeline) on random instances (1-32
+    stages in one batch, 1-24 mb, 1-4 DCs, n_sub 1-4, DP tails, ZeRO-1) x 4 random valid plans each,
+    addressed through inst_of: status, makespan, peak and every stage's first / last / busy / peak."""
+    batch = K.random_instances(160, seed=seed, max_p=32, max_m=24)
+    plans, inst_of = [], []
+    for i in range(len(batch)):
+        ops, ln = PL.plans_host(batch, 4, seed=seed * 1000 + i, i=i, q=int(i % 5), stride=32)
+        c, l_ = unpack_plans(ops, ln)
+        for k in range(4):
+            plans.append([list(c[k, s, :l_[k, s]]) for s in range(int(batch.p[i]))])
+            inst_of.append(i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(batch, ops, ln, inst_of, stats=True, timeline=False)
+    codes, lens = unpack_plans(ops, ln)
+    for j, i in enumerate(inst_of):
+        compare_sim(O, batch.item(i), codes[j], lens[j], r, j, codes.shape[2], timeline=False)
+    assert np.all(r["status"] == 0)
+
+
 def test_simulate_static_plans_and_overflow_path(O):
     """1F1B and GPipe (combined B) on random instances; GPipe exceeds the memory budget, which
     also drives the lead past the shared-memory ring -> global-ring fix-up pass must agree."""
