@@ -12,8 +12,11 @@
 // 3. k_exact_eval: persistent grid-stride over all chunks of all instances; a thread walks its
 //    chunk's product indices as an odometer (last stage fastest) and simulates every plan
 //    sequentially (§3.5 start-time rule, FIFO link windows = first fit under UD, App. X1; ZeRO-1
-//    gate; DP tail).  A plan is abandoned once a stage's clock + its remaining work + its DP tail
-//    exceeds the instance's best makespan so far (strictly, so equal-makespan plans survive), and
+//    gate; DP tail).  Whenever the stages 0..p-2 change, the prefix is first simulated with the
+//    last stage relaxed (instantaneous, order-free: a lower bound for every plan of the prefix) and
+//    the prefix's whole run is skipped if that bound exceeds the incumbent.  A plan is abandoned
+//    once a stage's clock + its remaining work + its DP tail exceeds the instance's best makespan
+//    so far (strictly, so equal-makespan plans survive), and
 //    the finished ones race on a 64-bit atomicMin of (makespan << b | product index), b = the bits of
 //    the instance's product size: the result is the smallest-index optimum, independent of thread
 //    timing.
