@@ -231,18 +231,17 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
                      : "=r"(tb.x), "=r"(tb.y), "=r"(tb.z), "=r"(tb.w) : "r"(ta_addr));
         const int ch = (int)(x >> 2);
         const bool isF = (x & 3u) == CP_OP_F, isW = (x & 3u) == CP_OP_W;
-        // readiness: input produced (or the own turn-around / loss), room in the consumer's ring
-        const bool rF0 = (q.xF0 > nF0) & (nF0 - q.yF0 < R32);
-        const bool rF1 = (q.xF1 > nF1) & (nF1 - q.yF1 < R32);
-        const bool rD1 = (q.xD1 > nD1) & (nD1 - q.yD1 < R32);
-        const bool rD0 = (q.xD0 > nD0) & (nD0 - q.yD0 < R32);
-        const int wc = ch ? (wP >> 16) : (wP & 0xffff), ndc = ch ? nD1 : nD0;
-        const bool rW = kN1 ? wc < ndc : wc < ns * ndc;
-        const bool rdy = isF ? (ch ? rF1 : rF0) : (isW ? rW : (ch ? rD1 : rD0));
-        const bool go = (pos4 < plen4) & rdy;
-        const bool right = tb.w != 0;
         // the entry's own count of its stream addresses both its input slot and its message slot
         const int cnt = ((isF ? cF : cD) >> (ch ? 16 : 0)) & 0xffff;
+        // readiness of the entry's stream only: input produced (or the own turn-around / loss) and
+        // room in the consumer's ring, from that stream's producer count X and consumer count Y
+        const int X = isF ? (ch ? q.xF1 : q.xF0) : (ch ? q.xD1 : q.xD0);
+        const int Y = isF ? (ch ? q.yF1 : q.yF0) : (ch ? q.yD1 : q.yD0);
+        const int wc = ch ? (wP >> 16) : (wP & 0xffff), ndc = ch ? nD1 : nD0;
+        const bool rW = kN1 ? wc < ndc : wc < ns * ndc;
+        const bool rdy = isW ? rW : ((X > cnt) & (cnt - Y < R32));
+        const bool go = (pos4 < plen4) & rdy;
+        const bool right = tb.w != 0;
         int arr;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"((unsigned)tb.x + ((unsigned)(cnt & tb.y) << 2)));
         const int start = wmx(clk, arr);
