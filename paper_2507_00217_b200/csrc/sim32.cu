@@ -270,11 +270,13 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+2048];"
                      : "=r"(tb.x), "=r"(tb.y), "=r"(tb.z), "=r"(tb.w) : "r"(ta_addr));
         const bool isF = code == CP_OP_F, isW = code == CP_OP_W;
-        const bool rF = (leftF > nF) & (nF - rightF < R32);
-        const bool rD = (rightD > nD) & (nD - leftD < R32);
         const bool isDB = !isF & !isW;
-        const bool go = (pos2 < plen2) & ((isF & rF) | (isW & (went < nD)) | (isDB & rD));
-        const unsigned raddr = (unsigned)tb.x + ((unsigned)((isF ? nF : nD) & tb.y) << 2);
+        // readiness of the entry's own stream only: the producer count X and consumer count Y of F
+        // (left, right) or D (right, left) are selected first, then one test
+        const int n = isF ? nF : nD;
+        const int X = isF ? leftF : rightD, Y = isF ? rightF : leftD;
+        const bool go = (pos2 < plen2) & (isW ? (went < nD) : ((X > n) & (n - Y < R32)));
+        const unsigned raddr = (unsigned)tb.x + ((unsigned)(n & tb.y) << 2);
         int arr;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"(raddr));
         const int start = mx(clk, arr);
