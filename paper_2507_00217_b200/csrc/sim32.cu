@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   // per-warp smem (words): [paramA 4*32 int4][paramB 4*32 int4][ringF R*32][ringD R*32]
-  //                        [plan 2*(PW+1)*32][sink 32][zero 32][2 mbarriers]
+  //                        [plan 2*(PW+1)*32][sink 32][zero 32][2 mbarriers][link clocks 2*32]
   const int wbase = wib * A.smem_words_per_warp;
   const int rbase = wbase + kSim32TableWords;
   const int pbase0 = rbase + 2 * RW;
@@ -232,12 +232,16 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         tabA[1 * 32] = make_int4(tB, mB, bwB, latB);
         tabA[2 * 32] = make_int4(td, md, bwB, latB);
         tabA[3 * 32] = make_int4(tw, mw, 0, 0);
-        // shared-window byte addresses, masks on counts * 32
+        // shared-window byte addresses: {input ring column, slot mask on counts * 32, send offset,
+        // the FIFO clock of the link the entry's message takes (F: to s+1, D/B: to s-1)}
         const unsigned sb = (unsigned)__cvta_generic_to_shared(smem);
-        tabB[0 * 32] = make_int4((int)(sb + 4u * iF), Rm << 5, sendF ? 4 : 0, 0);
-        tabB[1 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, 0);
-        tabB[2 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, 0);
-        tabB[3 * 32] = make_int4((int)(sb + 4u * (wbase + zero_row + lane)), 0, 0, 0);
+        const int lkF = (int)(sb + 4u * (wbase + zero_row + 36 + lane)), lkB = lkF + 128;
+        tabB[0 * 32] = make_int4((int)(sb + 4u * iF), Rm << 5, sendF ? 4 : 0, lkF);
+        tabB[1 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, lkB);
+        tabB[2 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, lkB);
+        tabB[3 * 32] = make_int4((int)(sb + 4u * (wbase + zero_row + lane)), 0, 0, lkF);
+        smem[wbase + zero_row + 36 + lane] = 0;            // both link clocks start at 0
+        smem[wbase + zero_row + 68 + lane] = 0;
       }
       __syncwarp();
       clk = tag;
@@ -277,20 +281,22 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         const int X = isF ? leftF : rightD, Y = isF ? rightF : leftD;
         const bool go = (pos2 < plen2) & (isW ? (went < nD) : ((X > n) & (n - Y < R32)));
         const unsigned raddr = (unsigned)tb.x + ((unsigned)(n & tb.y) << 2);
-        int arr;
+        int arr, lk;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"(raddr));
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lk) : "r"(tb.w));     // the link's FIFO clock
         const int start = mx(clk, arr);
         const int end = start + ta.x;
-        const int nl = mx(end, isF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
-        if (go && tb.z != 0) asm volatile("st.shared.b32 [%0], %1;" :: "r"(raddr + tb.z), "r"(nl + ta.w) : "memory");
+        const int nl = mx(end, lk) + ta.z;                   // FIFO link clock (App. X1)
+        if (go && tb.z != 0) {
+          asm volatile("st.shared.b32 [%0], %1;" :: "r"(raddr + tb.z), "r"(nl + ta.w) : "memory");
+          asm volatile("st.shared.b32 [%0], %1;" :: "r"(tb.w), "r"(nl) : "memory");
+        }
         const int gi = go ? 1 : 0, gFi = (go & isF) ? 1 : 0, gWi = (go & isW) ? 1 : 0;
         const int gDi = (go & isDB) ? 1 : 0;
         clk = madd(gi, end - clk, clk);
         mem = madd(gi, ta.y, mem);
         peak = mx(peak, mem);
         pos2 = madd(gi, 2, pos2);
-        linkF = madd(gFi, nl - linkF, linkF);
-        linkB = madd(gDi, nl - linkB, linkB);
         nF = madd(gFi, 32, nF);
         nD = madd(gDi, 32, nD);
         went = madd(gWi, 32, went);
