@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
     // parameter tables, entry x = type | chunk << 2:
     //   tabA[x] = {duration, memory delta, link bw, latency} (W: first sub-block / whole W if n_sub 1)
     //   tabB[x] = {input ring column (zero row without a producer), slot mask, consumer column (0: no
-    //             message), 1 if the message uses the lkR clock}
+    //             message), the byte address of the message's link clock}
     {
       const int tW = ns == 1 ? tw : wq, mW = ns == 1 ? mw : 0;
       const int dF1 = kLoop ? 1 : 0, dD1 = kLoop ? 0 : 1;       // clock of F1 / D1 (F0: lkR, D0: lkL)
@@ -169,16 +169,21 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
       // columns as shared-window byte addresses (0: no consumer), masks on counts scaled by 32
       const auto B = [&](int col) { return col ? (int)(sb + 4u * (unsigned)col) : 0; };
       const int Rm32 = Rm << 5;
-      tabB[0 * 32] = make_int4(B(inF0 ? iF0 : iZ), inF0 ? Rm32 : 0, B(oF0), 1);
-      tabB[1 * 32] = make_int4(B(inD0 ? iD0 : iZ), inD0 ? Rm32 : 0, B(oD0), 0);
+      // .w: byte address of the FIFO clock of the link the message takes (right / forward, left /
+      // backward), two per-lane slots after the plan rows
+      const int lkR = B(iP + A.plan_words * 32), lkL = lkR + 128;
+      smem[iP + A.plan_words * 32] = 0;                // both link clocks start at 0
+      smem[iP + A.plan_words * 32 + 32] = 0;
+      tabB[0 * 32] = make_int4(B(inF0 ? iF0 : iZ), inF0 ? Rm32 : 0, B(oF0), lkR);
+      tabB[1 * 32] = make_int4(B(inD0 ? iD0 : iZ), inD0 ? Rm32 : 0, B(oD0), lkL);
       tabB[2 * 32] = tabB[1 * 32];
-      tabB[3 * 32] = make_int4(B(iZ), 0, 0, 0);
-      tabB[4 * 32] = make_int4(B(inF1 ? iF1 : iZ), inF1 ? Rm32 : 0, B(oF1), dF1);
-      tabB[5 * 32] = make_int4(B(inD1 ? iD1 : iZ), inD1 ? Rm32 : 0, B(oD1), dD1);
+      tabB[3 * 32] = make_int4(B(iZ), 0, 0, lkR);
+      tabB[4 * 32] = make_int4(B(inF1 ? iF1 : iZ), inF1 ? Rm32 : 0, B(oF1), dF1 ? lkR : lkL);
+      tabB[5 * 32] = make_int4(B(inD1 ? iD1 : iZ), inD1 ? Rm32 : 0, B(oD1), dD1 ? lkR : lkL);
       tabB[6 * 32] = tabB[5 * 32];
       tabB[7 * 32] = tabB[3 * 32];
     }
-    int clk = tag, mem = 0, peak = 0, pos = 0, lkR = 0, lkL = 0;
+    int clk = tag, mem = 0, peak = 0, pos = 0;
     int cF = 0, cD = 0, wP = 0;                        // wP: W sub-blocks of chunk 0 | chunk 1 << 16
     int lm = first_s ? 0xffff : 0, rm = last ? 0xffff : 0;      // no producer / no consumer
     asm("mov.b32 %0, %0;" : "+r"(lm));
@@ -241,9 +246,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
         const bool rW = kN1 ? wc < ndc : wc < ns * ndc;
         const bool rdy = isW ? rW : ((X > cnt) & (cnt - Y < R32));
         const bool go = (pos4 < plen4) & rdy;
-        const bool right = tb.w != 0;
-        int arr;
+        int arr, lk;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"((unsigned)tb.x + ((unsigned)(cnt & tb.y) << 2)));
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lk) : "r"(tb.w));     // the message's link clock
         const int start = wmx(clk, arr);
         int dur = ta.x, dm = ta.y;
         if (!kN1) {                                     // W sub-block k of its W block (Q12)
@@ -252,22 +257,20 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
           dm = isW ? (k == ns - 1 ? mw : 0) : dm;
         }
         const int end = start + dur;
-        const int nl = wmx(end, right ? lkR : lkL) + ta.z;   // FIFO link clock (App. X1)
-        if (go & (tb.z != 0))                           // (tb.z: consumer column, 0 = none)
+        const int nl = wmx(end, lk) + ta.z;             // FIFO link clock (App. X1)
+        // a link clock advances only with a message on it (Loop: stage 0's D0 and the last stage's F1
+        // send nothing, while the same clocks carry their wrap-around D1 / F0 messages)
+        if (go & (tb.z != 0)) {                         // (tb.z: consumer column, 0 = none)
           asm volatile("st.shared.b32 [%0], %1;" :: "r"((unsigned)tb.z + ((unsigned)(cnt & Rm32) << 2)), "r"(nl + ta.w)
                        : "memory");
+          asm volatile("st.shared.b32 [%0], %1;" :: "r"(tb.w), "r"(nl) : "memory");
+        }
         if (kTL && go && (pos4 >> 2) < A.len_stride)
           A.t_start[(item * A.stage_stride + s) * (long long)A.len_stride + (pos4 >> 2)] = start;
         const int gi = go ? 1 : 0;
         clk = wmadd(gi, end - clk, clk);
         mem = wmadd(gi, dm, mem);
         peak = wmx(peak, mem);
-        // a link clock advances only with a message on it (Loop: stage 0's D0 and the last stage's F1
-        // send nothing, while the same clocks carry their wrap-around D1 / F0 messages)
-        const bool sent = go & (tb.z != 0);
-        const int gR = (sent & right) ? 1 : 0, gL = (sent & !right) ? 1 : 0;
-        lkR = wmadd(gR, nl - lkR, lkR);
-        lkL = wmadd(gL, nl - lkL, lkL);
         const int inc = ch ? (32 << 16) : 32;
         cF = wmadd((go & isF) ? 1 : 0, inc, cF);
         cD = wmadd((go & !isF & !isW) ? 1 : 0, inc, cD);
