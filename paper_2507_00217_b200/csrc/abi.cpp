@@ -147,7 +147,7 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
       !getenv_nofast()) {
     // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row
     a.ring_slots = fast_ring_slots(in);
-    a.smem_words_per_warp = (cpk::kSim32TableWords + 2 * a.ring_slots * 32 + 2 * (a.plan_words + 1) * 32 + 64 + 4 + 64 + 3) & ~3;
+    a.smem_words_per_warp = (cpk::kSim32TableWords + 2 * a.ring_slots * 32 + 2 * (a.plan_words + 1) * 32 + 64 + 4 + 64 + 256 + 3) & ~3;
     const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
     if (per_warp * 2 <= kMaxSmemPerBlock) {
       const int wpb = 2, threads = 64;

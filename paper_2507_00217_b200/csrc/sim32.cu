@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
   // per-warp smem (words): [paramA 4*32 int4][paramB 4*32 int4][ringF R*32][ringD R*32]
   //                        [plan 2*(PW+1)*32][sink 32][zero 32][2 mbarriers][link clocks 2*32]
+  //                        [counter increments 4*32 int2]
   const int wbase = wib * A.smem_words_per_warp;
   const int rbase = wbase + kSim32TableWords;
   const int pbase0 = rbase + 2 * RW;
@@ -242,6 +243,12 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         tabB[3 * 32] = make_int4((int)(sb + 4u * (wbase + zero_row + lane)), 0, 0, lkF);
         smem[wbase + zero_row + 36 + lane] = 0;            // both link clocks start at 0
         smem[wbase + zero_row + 68 + lane] = 0;
+        // per code: the increments of the packed (nF | nD << 16) counters and of the W count
+        int2* const tabC = reinterpret_cast<int2*>(smem + wbase + zero_row + 100) + lane;
+        tabC[0 * 32] = make_int2(32, 0);
+        tabC[1 * 32] = make_int2(32 << 16, 0);
+        tabC[2 * 32] = make_int2(32 << 16, 0);
+        tabC[3 * 32] = make_int2(0, 32);
       }
       __syncwarp();
       clk = tag;
@@ -254,11 +261,13 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
       const unsigned tab0 = sb + 4u * (unsigned)(wbase + 4 * lane);        // tabA[0][lane]; tabB at +2048 B
       const unsigned iPb = sb + 4u * (unsigned)iP;
       const int R32 = R << 5, plen2 = 2 * plen;
-      int pos2 = 0;
+      const unsigned tc0 = sb + 4u * (unsigned)(wbase + zero_row + 100 + 2 * lane);   // tabC[0][lane]
+      int pos2 = 0, me = 0;                         // me: nF | nD << 16 (both scaled by 32)
       for (;;) {
-        const int me = madd(nD, 65536, nF);
         const int cu = __shfl_up_sync(FULLM, me, 1);
         const int cd = __shfl_down_sync(FULLM, me, 1);
+        nF = me & 0xffff;
+        nD = me >> 16;
         const int leftF = (cu & 0xffff) | lmF;
         const int leftD = cu >> 16;
         const int rightF = (cd & 0xffff) | rmF;
@@ -268,6 +277,8 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         code &= 3u;
         asm("mov.b32 %0, %0;" : "+r"(code));        // materialized once: LEA for the table row
         const unsigned ta_addr = tab0 + (code << 9);
+        int2 tc;                                    // counter increments (off the critical path)
+        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(tc.x), "=r"(tc.y) : "r"(tc0 + (code << 8)));
         int4 ta, tb;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(ta.x), "=r"(ta.y), "=r"(ta.z), "=r"(ta.w) : "r"(ta_addr));
@@ -291,22 +302,20 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
           asm volatile("st.shared.b32 [%0], %1;" :: "r"(raddr + tb.z), "r"(nl + ta.w) : "memory");
           asm volatile("st.shared.b32 [%0], %1;" :: "r"(tb.w), "r"(nl) : "memory");
         }
-        const int gi = go ? 1 : 0, gFi = (go & isF) ? 1 : 0, gWi = (go & isW) ? 1 : 0;
-        const int gDi = (go & isDB) ? 1 : 0;
+        const int gi = go ? 1 : 0;
         clk = madd(gi, end - clk, clk);
         mem = madd(gi, ta.y, mem);
         peak = mx(peak, mem);
         pos2 = madd(gi, 2, pos2);
-        nF = madd(gFi, 32, nF);
-        nD = madd(gDi, 32, nD);
-        went = madd(gWi, 32, went);
+        me = madd(gi, tc.x, me);                    // the entry's counter(s), from the table
+        went = madd(gi, tc.y, went);
         unsigned wa;                                // iPb + 4 * (pos2 & ~31): one LOP3 + one IMAD
         asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(wa) : "r"((unsigned)pos2 & ~31u), "r"(iPb));
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(wa));
         __syncwarp();                               // ring stores visible to the neighbours' next reads
         if (!__any_sync(FULLM, go)) break;
       }
-      nF >>= 5; nD >>= 5; went >>= 5; pos = pos2 >> 1;
+      nF = (me & 0xffff) >> 5; nD = (me >> 16) >> 5; went >>= 5; pos = pos2 >> 1;
     } else {
       rounds(std::false_type{});
     }
