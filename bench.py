@@ -78,7 +78,7 @@ def issue_roofline(evals_per_s, sm_hz):
     peak = 148 * 4 * sm_hz                       # warp-instructions/s: 148 SMs x 4 schedulers x SM clock
     ach = ipe * evals_per_s
     return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-instr/s", "frac": ach / peak,
-            "instructions_per_eval": ipe, "source": "ncu smsp__inst_executed.sum (profiles/ncu_sim32_v15_r01.txt)",
+            "instructions_per_eval": ipe, "source": "ncu smsp__inst_executed.sum (profiles/ncu_sim32_v16_r01.txt)",
             "sm_clock_hz": sm_hz}
 
 
