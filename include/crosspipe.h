@@ -190,13 +190,14 @@ int32_t cp_greedy(const cp_instances* inst, const cp_schedules* out, const cp_re
 int32_t cp_sweep_shard(const cp_grid* grid, int64_t point_lo, int64_t point_hi,
                        int64_t* keys, int32_t* cand_makespan, void* ws, size_t ws_bytes, void* stream);
 
-/* Build static plans (PAPER.md Table tab:ppschedules :468-473; readings Q22, Q23, Q31) for the
- * out->n items of `out`: item i uses instance inst_of[i] (NULL: instance i, or 0 if inst->n == 1)
- * and gets its (p, m) plan in the packed layout cp_simulate reads.  kind: CP_PLAN_GPIPE,
- * CP_PLAN_1F1B, CP_PLAN_ZBH1 (2-bit UD entries), CP_PLAN_IV1F1B (4-bit Loop entries, 8 per word;
- * an item with n_mb % n_pp != 0 gets all-zero rows) or CP_PLAN_ZBV (4-bit Wave entries, 6*n_mb per
- * row; Table :473, reading Q35; an item with n_pp > 32 gets all-zero rows).  Every word of out->ops and every row of out->len is written
- * (entries past a row's length and rows >= p are 0), so the result is fully defined.
+/* Build static plans (PAPER.md Table tab:ppschedules :468-473; readings Q22, Q23, Q31, Q34, Q35)
+ * for the out->n items of `out`: item i uses instance inst_of[i] (NULL: instance i, or 0 if
+ * inst->n == 1) and gets its (p, m) plan in the packed layout cp_simulate reads.  kind:
+ * CP_PLAN_GPIPE, CP_PLAN_1F1B, CP_PLAN_ZBH1 (2-bit UD entries), CP_PLAN_IV1F1B (4-bit Loop entries,
+ * 8 per word; an item with n_mb % n_pp != 0 gets all-zero rows) or CP_PLAN_ZBV (4-bit Wave entries,
+ * 6*n_mb per row; an item with n_pp > 32 gets all-zero rows).  Every word of out->ops and every row
+ * of out->len is written (entries past a row's length and rows >= p are 0), so the result is fully
+ * defined.
  * Errors: CP_EINVAL for an unknown kind, NULL / inconsistent descriptors, stage_stride < max_pp,
  * or the row capacity (16*words entries, 8*words for IV1F1B / ZB-V) < entries per row at max_mb
  * (2*max_mb; 3*max_mb for ZB-H1; 4*max_mb for IV1F1B; 6*max_mb for ZB-V).  An item whose own
@@ -210,9 +211,9 @@ int32_t cp_build_static(int32_t kind, const cp_instances* inst, const cp_schedul
  * model), and the makespan-optimal plan is returned -- the first optimum in the order "stage sequences
  * in lexicographic order F < D < W, the last stage varying fastest".  Deadlocking plans are skipped.
  * Limits: n_pp <= 8, n_mb <= 8, at most `cap` valid sequences per stage and `max_plans` (< 2^52)
- * plans per instance, horizon < 2^30 ticks and < 2^(63 - ceil(log2 plans)) (the packed key);
- * an instance beyond them gets status CPI_OVERFLOW and
- * makespan -1; one without any completing plan CPI_DEADLOCK.
+ * plans per instance, horizon < 2^30 ticks and < 2^(63 - ceil(log2 plans)) (the packed key); an
+ * instance beyond them gets status CPI_OVERFLOW and makespan -1, one without any completing plan
+ * CPI_DEADLOCK.
  * upper (nullable, device) [n] int32: a known feasible makespan per instance (e.g. cp_greedy's with
  * n_sub = 1), -1 for none; it only seeds the search's cut (plans longer than it are skipped early),
  * the result is the same.  An instance whose every plan is longer than its `upper` reports
