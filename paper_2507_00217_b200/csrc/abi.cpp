@@ -328,7 +328,7 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
     a.from_list = pass;
     a.ring_slots = pass == 0 ? fast_ring_slots(in) : 1 << lg2_ceil(in->max_mb);
     a.plan_words = sc->words + 1;                       // one spare row: finished lanes read past their row
-    a.smem_words_per_warp = (2048 + 4 * a.ring_slots * 32 + 32 + a.plan_words * 32 + 64 + 3) & ~3;   // tables, rings, zero row, plan, link clocks
+    a.smem_words_per_warp = (2048 + 4 * a.ring_slots * 32 + 32 + a.plan_words * 32 + 64 + 512 + 3) & ~3;   // tables, rings, zero row, plan, link clocks, increments
     const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
     if (per_warp > kMaxSmemPerBlock) return CP_EUNSUPPORTED;
     const int wpb = per_warp * 2 <= kMaxSmemPerBlock ? 2 : 1, threads = 32 * wpb;

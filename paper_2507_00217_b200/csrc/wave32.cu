@@ -174,6 +174,12 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
       const int lkR = B(iP + A.plan_words * 32), lkL = lkR + 128;
       smem[iP + A.plan_words * 32] = 0;                // both link clocks start at 0
       smem[iP + A.plan_words * 32 + 32] = 0;
+      // per entry x: the increments of the packed F counts (nF0 | nF1 << 16) and D counts
+      int2* const tabC = reinterpret_cast<int2*>(smem + iP - lane + A.plan_words * 32 + 64) + lane;
+      for (int e = 0; e < 8; ++e) {
+        const int t = e & 3, inc = (e >> 2) ? (32 << 16) : 32;
+        tabC[e * 32] = make_int2(t == (int)CP_OP_F ? inc : 0, (t == (int)CP_OP_B || t == (int)CP_OP_D) ? inc : 0);
+      }
       tabB[0 * 32] = make_int4(B(inF0 ? iF0 : iZ), inF0 ? Rm32 : 0, B(oF0), lkR);
       tabB[1 * 32] = make_int4(B(inD0 ? iD0 : iZ), inD0 ? Rm32 : 0, B(oD0), lkL);
       tabB[2 * 32] = tabB[1 * 32];
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
       // nibble): the entry code is one funnel shift, the table row tab + x * 512 B and the ring slot
       // column + ((count & mask) << 2) are single LEAs off shared-window byte addresses
       const unsigned tab0 = sb + 4u * (unsigned)(wbase + 4 * lane), iPb = sb + 4u * (unsigned)iP;
+      const unsigned tc0 = iPb + 4u * (unsigned)(A.plan_words * 32 + 64 + lane);   // tabC[0][lane]
       const int R32 = R << 5, Rm32 = Rm << 5, plen4 = 4 * plen;
       int pos4 = 0;
       for (;;) {
@@ -229,6 +236,8 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
         x &= 7u;
         asm("mov.b32 %0, %0;" : "+r"(x));
         const unsigned ta_addr = tab0 + (x << 9);
+        int2 tc;                                        // counter increments (off the critical path)
+        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(tc.x), "=r"(tc.y) : "r"(tc0 + (x << 8)));
         int4 ta, tb;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(ta.x), "=r"(ta.y), "=r"(ta.z), "=r"(ta.w) : "r"(ta_addr));
@@ -271,10 +280,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
         clk = wmadd(gi, end - clk, clk);
         mem = wmadd(gi, dm, mem);
         peak = wmx(peak, mem);
-        const int inc = ch ? (32 << 16) : 32;
-        cF = wmadd((go & isF) ? 1 : 0, inc, cF);
-        cD = wmadd((go & !isF & !isW) ? 1 : 0, inc, cD);
-        wP = wmadd((go & isW) ? 1 : 0, inc, wP);
+        cF = wmadd(gi, tc.x, cF);
+        cD = wmadd(gi, tc.y, cD);
+        wP = wmadd((go & isW) ? 1 : 0, ch ? (32 << 16) : 32, wP);
         pos4 = wmadd(gi, 4, pos4);
         __syncwarp();
         if (!__any_sync(WFULL, go)) break;
