@@ -911,3 +911,39 @@ def test_e1_grid_every_point(O):
     keys, cm = cp.sweep_shard(grid, cand=True)
     torch.cuda.synchronize()
     check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
+
+
+def test_large_n_sub_greedy_and_simulate(O):
+    """n_sub up to the GPU limit CP_MAX_SUB = 16 (W blocks in up to 16 sub-blocks; reading Q12: every
+    sub-block >= 1 tick): the greedy's plans and makespans, and cp_simulate of random valid plans with
+    those n_sub, against the oracle (the random-instance tests stop at n_sub = 4)."""
+    batch = K.random_instances(48, seed=91, max_p=12, max_m=6, intra_delay=True)
+    rng = np.random.default_rng(92)
+    for i in range(48):
+        ns = int(rng.choice([5, 8, 16]))
+        p = int(batch.p[i])
+        batch.n_sub[i] = ns
+        for fld in ("t_f", "t_d", "t_w"):
+            getattr(batch, fld)[i, :p] = np.maximum(getattr(batch, fld)[i, :p], ns)
+    inst = cp.Instances(batch)
+    g = to_host(cp.greedy(inst, stats=True))
+    gc, gl = unpack_plans(g["ops"].view(np.uint32), g["len"].view(np.uint16))
+    for i in range(48):
+        d = batch.item(i)
+        w = O.greedy(d)
+        assert int(g["status"][i]) == w["status"] and int(g["makespan"][i]) == w["makespan"], i
+        if w["makespan"] >= 0:
+            for s in range(d["p"]):
+                assert list(gc[i, s, :gl[i, s]]) == list(w["codes"][s, :w["len"][s]]), (i, s)
+    plans, inst_of = [], []
+    for i in range(48):
+        ops, ln = PL.plans_host(batch, 2, seed=9300 + i, i=i, stride=32)
+        c, l_ = unpack_plans(ops, ln)
+        for k in range(2):
+            plans.append([list(c[k, s, :l_[k, s]]) for s in range(int(batch.p[i]))])
+            inst_of.append(i)
+    ops, ln = codes_list_to_packed(plans, stride=32)
+    r = run_sim(batch, ops, ln, inst_of, stats=True, timeline=False)
+    codes, lens = unpack_plans(ops, ln)
+    for j, i in enumerate(inst_of):
+        compare_sim(O, batch.item(i), codes[j], lens[j], r, j, codes.shape[2], timeline=False)
