@@ -264,7 +264,8 @@ def run_ours(args):
     # each rank evaluates its own n schedules (ids rank*n ...): weak scaling
     ops, ln = PL.plans_device(b, n, seed=K.PERTURB_SEED, id0=rank * n)
     stream = torch.cuda.current_stream()
-    out = cp.api._results(n, 32, False, False, 0, ops.device, True)
+    # best_key carries global schedule ids (rank * n + i), so the cross-rank MIN names a traceable schedule
+    out = cp.api._results(n, 32, False, False, 0, ops.device, True, index_base=rank * n)
     ws_buf = cp.api._workspace(0, inst.desc(), n, ops.device)
 
     def step():
@@ -313,7 +314,7 @@ def run_ours(args):
     st_h = torch.empty(n, dtype=torch.int32, pin_memory=True)
     del ops, ln, out, ws_buf
     torch.cuda.empty_cache()
-    pipe = cp.HostPipeline(inst, n, ops_h.shape[1], ops_h.shape[2], chunks=args.chunks)
+    pipe = cp.HostPipeline(inst, n, ops_h.shape[1], ops_h.shape[2], chunks=args.chunks, index_base=rank * n)
     for _ in range(2):
         pipe.run(ops_h, ln_h, ms_h, pk_h, st_h)
     torch.cuda.synchronize()
@@ -376,13 +377,13 @@ def run_ours(args):
                                              loop=is_loop)
             kw = {"loop": True} if is_loop else {"wave": True}
             for _ in range(3):
-                wr = cp.simulate(winst, wops, wln, best=True, **kw)
+                wr = cp.simulate(winst, wops, wln, best=True, index_base=rank * nw, **kw)
             wsteps = max(1, min(args.steps, 5))
             barrier(ws)
             v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             v0.record(stream)
             for _ in range(wsteps):
-                wr = cp.simulate(winst, wops, wln, best=True, **kw)
+                wr = cp.simulate(winst, wops, wln, best=True, index_base=rank * nw, **kw)
             v1.record(stream)
             torch.cuda.synchronize()
             wms = max_over_ranks(v0.elapsed_time(v1), ws)

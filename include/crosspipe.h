@@ -1,5 +1,5 @@
 /*
- * crosspipe.h -- C ABI (v1) of the B200-native CrossPipe hot path (arXiv 2507.00217).
+ * crosspipe.h -- C ABI (v2, CP_ABI_VERSION) of the B200-native CrossPipe hot path (arXiv 2507.00217).
  *
  * What the calls compute (citations are PAPER.md line numbers):
  *   cp_simulate    §3.5 pipeline performance model (:257-260): per-stage block order ->
@@ -10,11 +10,13 @@
  *   cp_greedy      Alg. 1 "Greedy Generation for CrossUDSub" (:383-412) with the §4.2.2
  *                  scheduling loop (:415-432); returns the schedule and its timeline.
  *   cp_sweep_shard schedule selection "with the best simulation performance" (:535, :543)
- *                  over a grid of instances; candidates GPipe, 1F1B (tab:ppschedules :470),
- *                  greedy n_sub = 1, 2, 4.
+ *                  over a grid of instances; CP_N_CAND = 6 candidates: GPipe, 1F1B
+ *                  (tab:ppschedules :470), greedy n_sub = 1, 2, 4, ZB-H1 (:472, Q31).
+ *   cp_build_static  static plans of Table tab:ppschedules (:468-473).
+ *   cp_exact       exact optimum of tiny instances (§4.1 validity set :322-351).
  *   cp_quantize    SI (seconds, bytes, s/byte) -> integer ticks / memory units (tab:symbols
  *                  :98-115, Alg. 1 inputs :381).
- * Every ambiguity is resolved by the readings Q1-Q30 listed in DESIGN.md.
+ * Every ambiguity is resolved by the readings Q1-Q37 listed in DESIGN.md §2.
  *
  * Conventions
  *   - Pointers are DEVICE pointers unless marked (host).  The caller owns every buffer;
@@ -79,7 +81,7 @@ typedef enum {                /* per-item status bitmask */
  * Per-stage arrays are indexed by stage s < n_pp.  Boundary arrays are indexed by
  * boundary s < n_pp-1: *_f = link s -> s+1 (activations), *_b = link s+1 -> s (gradients).
  * Invariants (else CPI_BAD_INSTANCE): 1 <= n_pp <= 32, n_mb >= 1, n_sub >= 1; t_f, t_d,
- * t_w > 0; t_w >= n_sub; m_f > 0, m_d <= 0, m_w <= 0, m_f + m_d + m_w == 0; m_lim >= m_f;
+ * t_w > 0; every block >= n_sub ticks (t_f, t_d, t_w >= n_sub, Q12); m_f > 0, m_d <= 0, m_w <= 0, m_f + m_d + m_w == 0; m_lim >= m_f;
  * t_dp, t_ag >= 0; lat/bw >= 0.  flags bit0 = ZeRO-1 (t_ag gates the stage's F blocks). */
 typedef struct {
   uint8_t n_pp, n_dc, n_sub, flags;
@@ -170,13 +172,18 @@ const char* cp_status_string(int32_t code);   /* cp_rc (<0) or cp_item bitmask (
 size_t cp_workspace_bytes(int32_t which, const void* desc, int64_t n_items);
 
 /* Evaluate sched->n fixed plans.  Errors: CP_EINVAL (NULL/inconsistent descriptors,
- * stage_stride < max_pp, words < 1, len_stride < 0), CP_EUNSUPPORTED (max_pp > 32),
- * CP_EWORKSPACE, CP_ECUDA (launch failure). */
+ * stage_stride < max_pp, words < 1, len_stride < 1 with t_start, unknown pattern, inst_of NULL
+ * with 1 < inst->n < sched->n), CP_EUNSUPPORTED (max_pp > 32 or max_mb > 1024; Wave / Loop
+ * plans with max_mb > 256, or whose staged rows do not fit one block's shared memory),
+ * CP_EWORKSPACE, CP_ECUDA (launch failure).  A row longer than its capacity, or violating
+ * Q29, is the item's CPI_BAD_PLAN, not an API error. */
 int32_t cp_simulate(const cp_instances* inst, const cp_schedules* sched, const cp_results* res,
                     void* ws, size_t ws_bytes, void* stream /* cudaStream_t */);
 
 /* Generate one greedy schedule per instance (out->n must equal inst->n, out->inst_of NULL,
- * 16*out->words >= (2+n_sub)*n_mb).  Writes out->ops / out->len and res (its timeline). */
+ * stage_stride >= max_pp, words >= 1).  Writes out->ops / out->len and res (its timeline).  An
+ * item whose schedule does not fit the rows (16*out->words < (2+n_sub)*n_mb) gets CPI_BAD_PLAN.
+ * Errors as cp_simulate. */
 int32_t cp_greedy(const cp_instances* inst, const cp_schedules* out, const cp_results* res,
                   void* ws, size_t ws_bytes, void* stream);
 
@@ -184,7 +191,12 @@ int32_t cp_greedy(const cp_instances* inst, const cp_schedules* out, const cp_re
  * (the caller fills the rest with INT64_MAX; cp_sweep in python = fill + shard + all_reduce(MIN)).
  * Work is (point, candidate) tasks taken from a device counter (most expensive first) and combined
  * with a 64-bit atomicMin per point; p-classes run concurrently on streams forked from `stream`
- * and joined back to it.  ws: cp_workspace_bytes(2, grid, 0) bytes.
+ * and joined back to it.  ws: cp_workspace_bytes(2, grid, 0) bytes (256 B of task counters, plus
+ * global-memory arrival rings for any p-class whose in-flight bound min(m, M_L/m_f) does not fit
+ * one block's shared memory, about 900 microbatches).  Errors: CP_EINVAL for a malformed grid --
+ * axis sizes, negative axis values, or any point whose synthesized instance violates the record
+ * invariants (e.g. a p beyond the base record's stages, M_L < m_f or beyond int32) --,
+ * CP_EUNSUPPORTED (p > 32, m > 1024), CP_EWORKSPACE, CP_ECUDA.
  * cand_makespan (nullable) [n_points][CP_N_CAND] int32: makespan of each candidate, -1 if not run
  * or memory-infeasible.  grid is a HOST pointer, passed to the kernel by value. */
 int32_t cp_sweep_shard(const cp_grid* grid, int64_t point_lo, int64_t point_hi,

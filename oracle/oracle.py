@@ -207,6 +207,11 @@ def greedy(d, timeline=False) -> dict:
     return out
 
 
+def validate_instance(d) -> int:
+    """Instance invariants (Q10, Q12, Q19, Q21): 0 or BAD_INSTANCE (8)."""
+    return int(lib().or_validate_instance(C.byref(to_or_inst(d))))
+
+
 def check_plan(d, codes, lens=None) -> int:
     p = int(d["p"])
     c, ln, maxlen = _codes_arr(codes, lens, p)

@@ -6,6 +6,7 @@ and forwards raw pointers.  Names follow include/crosspipe.h.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 
 import numpy as np
@@ -33,6 +34,25 @@ def _ptr(t):
 def _stream(stream=None):
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+@contextlib.contextmanager
+def _on_stream(stream, *inputs):
+    """Run a call's allocation, initialization and launch on `stream` (default: torch's current
+    stream).  A non-current stream first waits for the current one, so inputs written there are
+    visible, and the input tensors are recorded on it, so the caching allocator keeps them alive
+    until the launch has consumed them.  Tensors allocated inside belong to `stream`: the caller
+    orders any other stream's use of the results after it (e.g. current.wait_stream(stream))."""
+    cur = torch.cuda.current_stream()
+    if stream is None or stream == cur:
+        yield cur
+        return
+    stream.wait_stream(cur)
+    for t in inputs:
+        if t is not None:
+            t.record_stream(stream)
+    with torch.cuda.stream(stream):
+        yield stream
 
 
 # ---------------------------------------------------------------------------------------- records
@@ -88,7 +108,7 @@ def _workspace(which, desc, n_items, device):
     return torch.empty(max(int(nb), 256), dtype=torch.uint8, device=device)
 
 
-def _results(n, stage_stride, stats, timeline, len_stride, device, best):
+def _results(n, stage_stride, stats, timeline, len_stride, device, best, index_base=0):
     r = {"makespan": torch.empty(n, dtype=torch.int64, device=device),
          "peak_mem": torch.empty(n, dtype=torch.int32, device=device),
          "status": torch.empty(n, dtype=torch.int32, device=device)}
@@ -100,32 +120,37 @@ def _results(n, stage_stride, stats, timeline, len_stride, device, best):
         r["best_key"] = torch.full((1,), KEY_NONE, dtype=torch.int64, device=device)
     cres = L.CpResults(r["makespan"].data_ptr(), r["peak_mem"].data_ptr(), r["status"].data_ptr(),
                        r["stage_stats"].data_ptr() if stats else None,
-                       r["t_start"].data_ptr() if timeline else None, int(len_stride if timeline else 0), 0,
-                       r["best_key"].data_ptr() if best else None)
+                       r["t_start"].data_ptr() if timeline else None, int(len_stride if timeline else 0),
+                       int(index_base), r["best_key"].data_ptr() if best else None)
     return r, cres
 
 
 # ---------------------------------------------------------------------------------------- calls
 def simulate(inst: Instances, ops: torch.Tensor, lens: torch.Tensor, inst_of: torch.Tensor = None, *,
              stats=False, timeline=False, len_stride=None, best=False, ring=None, stream=None, ws=None,
-             out=None, wave=False, loop=False):
+             out=None, wave=False, loop=False, index_base=0):
     """cp_simulate: evaluate ops.shape[0] fixed plans.  ops uint32-as-int32 [n, words, stride], lens int16 [n, stride].
     wave=True / loop=True: two-chunk Wave (reading Q32) / Loop (Q33) plans, 4-bit entries type | chunk << 2,
-    8 per word."""
+    8 per word.  index_base: global id of plan 0, carried by best_key (makespan << 32 | index_base + i), so
+    shards of one population (ranks, chunks) report traceable ids.  `stream`: see _on_stream; a
+    caller-supplied `out` / `ws` must not be in use by another stream."""
     _require_cuda(ops, lens, inst_of)
     n, words, stride = ops.shape
     dev = ops.device
     d = inst.desc(ring)
-    if out is None:
-        out = _results(n, stride, stats, timeline, len_stride or (8 if (wave or loop) else 16) * words, dev, best)
-    r, cres = out
-    if ws is None:
-        ws = _workspace(0, d, n, dev)
-    sc = L.CpSchedules(n, stride, words, 2 if loop else (1 if wave else 0), _ptr(inst_of), ops.data_ptr(), lens.data_ptr())
-    if best:
-        r["best_key"].fill_(KEY_NONE)
-    rc = L.load().cp_simulate(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(ws.data_ptr()), ws.numel(),
-                              _stream(stream))
+    with _on_stream(stream, ops, lens, inst_of, inst.dev) as s:
+        if out is None:
+            out = _results(n, stride, stats, timeline, len_stride or (8 if (wave or loop) else 16) * words, dev, best,
+                           index_base)
+        r, cres = out
+        if ws is None:
+            ws = _workspace(0, d, n, dev)
+        sc = L.CpSchedules(n, stride, words, 2 if loop else (1 if wave else 0), _ptr(inst_of), ops.data_ptr(),
+                           lens.data_ptr())
+        if best:
+            r["best_key"].fill_(KEY_NONE)
+        rc = L.load().cp_simulate(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(ws.data_ptr()), ws.numel(),
+                                  _stream(s))
     L.check(rc, "cp_simulate")
     return r
 
@@ -135,11 +160,12 @@ class HostPipeline:
 
     The batch is cut into chunks; chunk k+1's host->device copy (copy stream) overlaps chunk k's
     kernel (compute stream), and results of chunk k stream back while later chunks run.  Every
-    chunk is one cp_simulate call on device views with index_base = chunk start, so best_key
-    carries global schedule ids.  Device buffers and streams are allocated once and reused."""
+    chunk is one cp_simulate call on device views with index_base = index_base + chunk start, so
+    best_key carries global schedule ids.  Device buffers and streams are allocated once and reused."""
 
-    def __init__(self, inst: Instances, n: int, words: int, stride: int, chunks: int = 32, device="cuda"):
-        self.inst, self.n, self.chunks = inst, n, max(1, chunks)
+    def __init__(self, inst: Instances, n: int, words: int, stride: int, chunks: int = 32, device="cuda",
+                 index_base: int = 0):
+        self.inst, self.n, self.chunks, self.base = inst, n, max(1, chunks), int(index_base)
         self.ops_d = torch.empty((n, words, stride), dtype=torch.int32, device=device)
         self.len_d = torch.empty((n, stride), dtype=torch.int16, device=device)
         self.r, _ = _results(n, stride, False, False, 0, device, True)
@@ -170,7 +196,7 @@ class HostPipeline:
             sc = L.CpSchedules(b - a, self.stride, self.words, 0, None, self.ops_d[a].data_ptr(),
                                self.len_d[a].data_ptr())
             cres = L.CpResults(r["makespan"][a:].data_ptr(), r["peak_mem"][a:].data_ptr(), r["status"][a:].data_ptr(),
-                               None, None, 0, int(a), r["best_key"].data_ptr())
+                               None, None, 0, self.base + int(a), r["best_key"].data_ptr())
             rc = L.load().cp_simulate(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(self.ws.data_ptr()),
                                       self.ws.numel(), C.c_void_p(self.comp.cuda_stream))
             L.check(rc, "cp_simulate")
@@ -195,17 +221,18 @@ def greedy(inst: Instances, *, stats=False, timeline=False, stage_stride=None, w
     if words is None:
         words = ((2 + inst.max_sub) * inst.max_mb + 15) // 16
     d = inst.desc(ring)
-    if out is None:
-        r, cres = _results(n, stride, stats, timeline, 16 * words, dev, False)
-        r["ops"] = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
-        r["len"] = torch.empty((n, stride), dtype=torch.int16, device=dev)
-        out = (r, cres)
-    r, cres = out
-    if ws is None:
-        ws = _workspace(1, d, n, dev)
-    sc = L.CpSchedules(n, stride, words, 0, None, r["ops"].data_ptr(), r["len"].data_ptr())
-    rc = L.load().cp_greedy(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(ws.data_ptr()), ws.numel(),
-                            _stream(stream))
+    with _on_stream(stream, inst.dev) as s:
+        if out is None:
+            r, cres = _results(n, stride, stats, timeline, 16 * words, dev, False)
+            r["ops"] = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
+            r["len"] = torch.empty((n, stride), dtype=torch.int16, device=dev)
+            out = (r, cres)
+        r, cres = out
+        if ws is None:
+            ws = _workspace(1, d, n, dev)
+        sc = L.CpSchedules(n, stride, words, 0, None, r["ops"].data_ptr(), r["len"].data_ptr())
+        rc = L.load().cp_greedy(C.byref(d), C.byref(sc), C.byref(cres), C.c_void_p(ws.data_ptr()), ws.numel(),
+                                _stream(s))
     L.check(rc, "cp_greedy")
     return r
 
@@ -223,12 +250,14 @@ def build_static(kind: str, inst: Instances, n=None, inst_of=None, *, stage_stri
     if words is None:
         per_mb = {"zbh1": 3, "iv1f1b": 4, "zbv": 6}.get(kind, 2)
         words = (per_mb * inst.max_mb + 7) // 8 if kind in ("iv1f1b", "zbv") else (per_mb * inst.max_mb + 15) // 16
-    ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
-    ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
     d = inst.desc(None)
     io = inst_of.data_ptr() if inst_of is not None else None
-    sc = L.CpSchedules(n, stride, words, 0, io, ops.data_ptr(), ln.data_ptr())
-    L.check(L.load().cp_build_static(k, C.byref(d), C.byref(sc), _stream(stream)), "cp_build_static")
+    with _on_stream(stream, inst.dev, inst_of) as s:
+        ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
+        ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
+        sc = L.CpSchedules(n, stride, words, 0, io, ops.data_ptr(), ln.data_ptr())
+        rc = L.load().cp_build_static(k, C.byref(d), C.byref(sc), _stream(s))
+    L.check(rc, "cp_build_static")
     return ops, ln
 
 
@@ -243,17 +272,19 @@ def exact(inst: Instances, *, cap=65536, max_plans=1 << 32, upper=None, stage_st
     n = inst.n
     stride = stage_stride or inst.max_pp
     words = max(1, (3 * min(inst.max_mb, 8) + 15) // 16)
-    ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
-    ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
-    ms = torch.empty(n, dtype=torch.int32, device=dev)
-    st = torch.empty(n, dtype=torch.int32, device=dev)
     nb = int(L.load().cp_exact_workspace_bytes(n, cap))
-    ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
     d = inst.desc(None)
-    sc = L.CpSchedules(n, stride, words, 0, None, ops.data_ptr(), ln.data_ptr())
-    up = None if upper is None else upper.to(device=dev, dtype=torch.int32).contiguous()
-    L.check(L.load().cp_exact(C.byref(d), C.byref(sc), _ptr(up), C.c_void_p(ms.data_ptr()), C.c_void_p(st.data_ptr()), cap,
-                              int(max_plans), C.c_void_p(ws.data_ptr()), nb, _stream(stream)), "cp_exact")
+    with _on_stream(stream, inst.dev, upper) as s:
+        ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
+        ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
+        ms = torch.empty(n, dtype=torch.int32, device=dev)
+        st = torch.empty(n, dtype=torch.int32, device=dev)
+        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        sc = L.CpSchedules(n, stride, words, 0, None, ops.data_ptr(), ln.data_ptr())
+        up = None if upper is None else upper.to(device=dev, dtype=torch.int32).contiguous()
+        rc = L.load().cp_exact(C.byref(d), C.byref(sc), _ptr(up), C.c_void_p(ms.data_ptr()), C.c_void_p(st.data_ptr()),
+                               cap, int(max_plans), C.c_void_p(ws.data_ptr()), nb, _stream(s))
+    L.check(rc, "cp_exact")
     return {"ops": ops, "len": ln, "makespan": ms, "status": st}
 
 
@@ -301,6 +332,19 @@ def to_cp_grid(grid) -> L.CpGrid:
     return g
 
 
+def _sweep_buffers(g, npts, keys, cand, device):
+    """Key table (INT64_MAX = not owned), optional per-candidate makespans, workspace; allocated and
+    initialized on the current stream (the call's stream, under _on_stream)."""
+    if keys is None:
+        keys = torch.full((npts,), KEY_NONE, dtype=torch.int64, device=device)
+    if cand is True:
+        cm = torch.full((npts, L.N_CAND), -1, dtype=torch.int32, device=keys.device)
+    else:
+        cm = cand if cand is not False and cand is not None else None
+    ws = torch.empty(int(L.load().cp_workspace_bytes(2, C.byref(g), 0)), dtype=torch.uint8, device=keys.device)
+    return keys, cm, ws
+
+
 def sweep_shard(grid, lo=0, hi=None, *, keys=None, cand=False, stream=None, device="cuda", cgrid=None):
     """cp_sweep_shard over points [lo, hi).  Returns (keys uint64-as-int64 [n_points], cand_ms or None).
     Keys outside [lo, hi) are INT64_MAX when `keys` is allocated here."""
@@ -308,12 +352,10 @@ def sweep_shard(grid, lo=0, hi=None, *, keys=None, cand=False, stream=None, devi
     g = cgrid if cgrid is not None else to_cp_grid(grid)
     npts = grid.n_points
     hi = npts if hi is None else hi
-    if keys is None:
-        keys = torch.full((npts,), KEY_NONE, dtype=torch.int64, device=device)
-    cm = torch.full((npts, L.N_CAND), -1, dtype=torch.int32, device=device) if cand is True else (cand if cand is not False and cand is not None else None)
-    ws = torch.empty(int(L.load().cp_workspace_bytes(2, C.byref(g), 0)), dtype=torch.uint8, device=keys.device)
-    rc = L.load().cp_sweep_shard(C.byref(g), int(lo), int(hi), C.c_void_p(keys.data_ptr()),
-                                 _ptr(cm), C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
+    with _on_stream(stream, keys) as s:
+        keys, cm, ws = _sweep_buffers(g, npts, keys, cand, device)
+        rc = L.load().cp_sweep_shard(C.byref(g), int(lo), int(hi), C.c_void_p(keys.data_ptr()),
+                                     _ptr(cm), C.c_void_p(ws.data_ptr()), ws.numel(), _stream(s))
     L.check(rc, "cp_sweep_shard")
     return keys, cm
 
@@ -325,12 +367,10 @@ def sweep_shard_rank(grid, rank: int, world: int, *, keys=None, cand=False, stre
     _require_cuda()
     g = cgrid if cgrid is not None else to_cp_grid(grid)
     npts = grid.n_points
-    if keys is None:
-        keys = torch.full((npts,), KEY_NONE, dtype=torch.int64, device=device)
-    cm = torch.full((npts, L.N_CAND), -1, dtype=torch.int32, device=device) if cand is True else (cand if cand is not False and cand is not None else None)
-    ws = torch.empty(int(L.load().cp_workspace_bytes(2, C.byref(g), 0)), dtype=torch.uint8, device=keys.device)
-    rc = L.load().cp_sweep_shard_rank(C.byref(g), int(rank), int(world), C.c_void_p(keys.data_ptr()), _ptr(cm),
-                                      C.c_void_p(ws.data_ptr()), ws.numel(), _stream(stream))
+    with _on_stream(stream, keys) as s:
+        keys, cm, ws = _sweep_buffers(g, npts, keys, cand, device)
+        rc = L.load().cp_sweep_shard_rank(C.byref(g), int(rank), int(world), C.c_void_p(keys.data_ptr()), _ptr(cm),
+                                          C.c_void_p(ws.data_ptr()), ws.numel(), _stream(s))
     L.check(rc, "cp_sweep_shard_rank")
     return keys, cm
 

@@ -13,6 +13,7 @@
 
 #include "crosspipe.h"
 #include "engine.h"
+#include "grid_synth.cuh"
 
 
 namespace {
@@ -234,6 +235,36 @@ int check_grid(const cp_grid* g) {
     if (g->n_mb_vals[i] < 1) return CP_EINVAL;
     if (g->n_mb_vals[i] > CP_MAX_MB) return CP_EUNSUPPORTED;
   }
+  for (int i = 0; i < g->n_lat; ++i) if (g->lat[i] < 0) return CP_EINVAL;
+  for (int i = 0; i < g->n_bw; ++i) if (g->bw[i] < 0) return CP_EINVAL;
+  for (int i = 0; i < g->n_mem; ++i) if (g->mlim_x1000[i] < 0) return CP_EINVAL;
+  for (int i = 0; i < g->n_dp; ++i) if (g->tdp[i] < 0) return CP_EINVAL;
+  // Every point's synthesized instance must be valid: a malformed grid (a p beyond the base
+  // record's stages, bad memory deltas, a budget below m_f or beyond int32) is an API error, not
+  // "no feasible candidate".  Validity depends on (p, memory scale) only -- m, latency, bandwidth
+  // and DP time enter through the checks above -- so one synthesized record per pair is checked
+  // (grid_synth.cuh, the kernels' own synthesis).  The int32 horizon guard (CPI_OVERFLOW) stays
+  // per point: such points get KEY_OVER.
+  for (int ip = 0; ip < g->n_pp_n; ++ip)
+    for (int ix = 0; ix < g->n_mem; ++ix) {
+      const long long point = (((long long)ip * g->n_mb_n * g->n_lat * g->n_bw) * g->n_mem + ix) * g->n_dp;
+      cp_inst_v1 r;
+      std::memset(&r, 0, sizeof(r));
+      const int p = g->n_pp_vals[ip];
+      r.n_pp = (uint8_t)p;
+      r.n_mb = (uint16_t)g->n_mb_vals[0];
+      r.n_sub = 1;
+      r.flags = g->base.flags & 1;
+      r.version = 1;
+      for (int s = 0; s < p; ++s) {
+        if (((long long)g->mlim_x1000[ix] * p * g->base.m_f[s] + 500) / 1000 > INT32_MAX) return CP_EINVAL;
+        const cpk::GridLane L = cpk::grid_lane(*g, point, s);
+        r.t_f[s] = L.tf; r.t_d[s] = L.td; r.t_w[s] = L.tw;
+        r.m_f[s] = L.mf; r.m_d[s] = L.md; r.m_w[s] = L.mw; r.m_lim[s] = L.mlim;
+        r.t_dp[s] = L.tdp; r.t_ag[s] = L.tag;
+      }
+      if (cp_validate_instance(&r, nullptr, 0) == CPI_BAD_INSTANCE) return CP_EINVAL;
+    }
   return CP_OK;
 }
 
@@ -254,6 +285,21 @@ int sweep_ring_slots(const cp_grid* g, int p) {
   return (int)r;
 }
 
+// An engine sweep pass whose rings do not fit one block's shared memory (n_mb and M_L beyond ~900
+// in-flight microbatches) runs with global-memory rings in the workspace instead: one region per
+// p-class, since the classes run concurrently.  Returns that class's bytes (0 = shared memory).
+size_t sweep_class_ring_bytes(const cp_grid* g, int ip) {
+  const int slots = sweep_ring_slots(g, g->n_pp_vals[ip]);
+  if ((size_t)smem_words(false, slots, 0, 1, false) * 4 <= kMaxSmemPerBlock) return 0;
+  return align256((size_t)cpk::kFixWarps * ring_bytes_per_warp(slots));
+}
+
+size_t sweep_ws_bytes(const cp_grid* g) {
+  size_t b = kCtrlBytes;
+  for (int ip = 0; ip < g->n_pp_n; ++ip) b += sweep_class_ring_bytes(g, ip);
+  return b;
+}
+
 long long point_cost(const cp_grid* g, int i_pp, int i_mb) {
   static const int units[CP_N_CAND] = {2, 2, 3, 4, 6, 3};   // entries per microbatch: 2m GPipe/1F1B, (2+n_sub)m greedy, 3m ZB-H1
   long long u = 0;
@@ -272,7 +318,7 @@ const char* cp_status_string(int32_t code) {
   switch (code) {
     case CP_OK: return "ok";
     case CP_EINVAL: return "invalid argument / descriptor";
-    case CP_EUNSUPPORTED: return "unsupported shape (p > 32 or n_mb > 1024)";
+    case CP_EUNSUPPORTED: return "unsupported shape (p > 32, n_mb > 1024, two-chunk n_mb > 256, rows beyond shared memory)";
     case CP_ECUDA: return "CUDA launch error";
     case CP_EWORKSPACE: return "workspace too small";
     case CPI_DEADLOCK: return "deadlock: plan cannot complete";
@@ -285,7 +331,10 @@ const char* cp_status_string(int32_t code) {
 }
 
 size_t cp_workspace_bytes(int32_t which, const void* desc, int64_t n_items) {
-  if (which == 2) return kCtrlBytes;
+  if (which == 2) {
+    const cp_grid* g = static_cast<const cp_grid*>(desc);
+    return g && check_grid(g) == CP_OK ? sweep_ws_bytes(g) : kCtrlBytes;
+  }
   if (which != 0 && which != 1) return 0;
   const cp_instances* in = static_cast<const cp_instances*>(desc);
   if (!in || n_items < 0) return 0;
@@ -522,7 +571,15 @@ static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_l
       a.sweep_counter = counters + 4 * c;
       a.seg_lg = lg2_ceil(p);
       a.ring_slots = sweep_ring_slots(g, p);
-      rc = launch_pass(cpk::MODE_SWEEP, false, a, npts * __builtin_popcount(engine_mask), 32 >> a.seg_lg, fk.next());
+      cudaStream_t es = fk.next();
+      rc = launch_pass(cpk::MODE_SWEEP, false, a, npts * __builtin_popcount(engine_mask), 32 >> a.seg_lg, es);
+      if (rc == CP_EUNSUPPORTED) {
+        // rings beyond shared memory: this class's global-memory rings in the workspace
+        size_t off = kCtrlBytes;
+        for (int q = 0; q < ip; ++q) off += sweep_class_ring_bytes(g, q);
+        a.ring_g = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + off);
+        rc = launch_pass(cpk::MODE_SWEEP, true, a, npts * __builtin_popcount(engine_mask), 32 >> a.seg_lg, es);
+      }
     }
     if (rc) break;
   }
@@ -537,7 +594,7 @@ int32_t cp_sweep_shard(const cp_grid* g, int64_t lo, int64_t hi, int64_t* keys, 
   if (rc) return rc;
   const long long np = grid_points(g);
   if (!keys || lo < 0 || hi < lo || hi > np) return CP_EINVAL;
-  if (!ws || ws_bytes < kCtrlBytes) return CP_EWORKSPACE;
+  if (!ws || ws_bytes < sweep_ws_bytes(g)) return CP_EWORKSPACE;
   if (lo == hi) return CP_OK;
   return sweep_run(g, lo, hi, 0, 0, keys, cand_ms, ws, stream);
 }
@@ -547,7 +604,7 @@ int32_t cp_sweep_shard_rank(const cp_grid* g, int32_t rank, int32_t world, int64
   int rc = check_grid(g);
   if (rc) return rc;
   if (!keys || world < 1 || rank < 0 || rank >= world) return CP_EINVAL;
-  if (!ws || ws_bytes < kCtrlBytes) return CP_EWORKSPACE;
+  if (!ws || ws_bytes < sweep_ws_bytes(g)) return CP_EWORKSPACE;
   const long long inner = (long long)g->n_lat * g->n_bw * g->n_mem * g->n_dp;
   const int own_lo = (int)(inner * rank / world), own_hi = (int)(inner * (rank + 1) / world);
   if (own_lo == own_hi) return CP_OK;

@@ -577,7 +577,7 @@ static void* pick(Mode mode, bool rg, bool tl) {
     case MODE_GREEDY:
       return rg ? (tl ? kernel_ptr<MODE_GREEDY, true, true>() : kernel_ptr<MODE_GREEDY, true, false>())
                 : (tl ? kernel_ptr<MODE_GREEDY, false, true>() : kernel_ptr<MODE_GREEDY, false, false>());
-    default: return kernel_ptr<MODE_SWEEP, false, false>();
+    default: return rg ? kernel_ptr<MODE_SWEEP, true, false>() : kernel_ptr<MODE_SWEEP, false, false>();
   }
 }
 

@@ -23,7 +23,8 @@ struct GridLane {      // one lane's (stage's) view of a synthesized instance
   int latF, bwF, latB, bwB;       // s -> s+1 (F) and s -> s-1 (D) link delays
 };
 
-__device__ __forceinline__ GridLane grid_lane(const cp_grid& G, long long point, int s) {
+// host + device: the host validates every synthesized instance class in check_grid (abi.cpp)
+__host__ __device__ __forceinline__ GridLane grid_lane(const cp_grid& G, long long point, int s) {
   GridLane g = {};
   long long k = point;
   const int i_dp = (int)(k % G.n_dp); k /= G.n_dp;
@@ -66,6 +67,7 @@ __host__ __device__ __forceinline__ long long sweep_point_of(const SweepSet& q, 
   return (q.lo + j / span) * q.inner + q.own_lo + j % span;
 }
 
+#ifdef __CUDACC__
 // (point, candidate) of sweep task t: active candidates of `mask` as the slowest axis, visited in
 // reverse so the most expensive tasks (highest candidate id, largest m) start first and
 // neighbouring segments of a warp get the same candidate.  Returns the point (or -1).
@@ -80,5 +82,7 @@ __device__ __forceinline__ long long sweep_task(unsigned mask, const SweepSet& q
   cand = __ffs(mm) - 1;
   return sweep_point_of(q, tid % npts);
 }
+
+#endif  // __CUDACC__
 
 }  // namespace cpk

@@ -151,3 +151,66 @@ def test_argument_errors_before_any_device_work():
     assert lib.cp_exact(C.byref(inst), C.byref(good), None, ms, st, 16, 100, None, 0, None) == L.CP_EWORKSPACE
     assert lib.cp_exact_workspace_bytes(0, 16) == 0
     assert lib.cp_exact_workspace_bytes(4, 16) >= 4 * 8 * 16 * 8
+
+
+def test_validator_each_invariant_through_the_abi():
+    """cp_validate_instance (host side of the C ABI) rejects each single-invariant violation of
+    SPEC.md:46-50 / Q10 / Q12 / Q19 that tests/test_oracle_pins.py pins on the oracle, accepts the
+    adjacent valid value, and names the violated invariant."""
+    from tests.test_oracle_pins import _INVARIANT_CASES
+    for why, fields, stage, bad, ok in _INVARIANT_CASES:
+        p0 = 32 if ("p" in fields and bad[0] > 4) else 4
+        for vals, want in ((bad, 8), (ok, 0)):
+            b = K.uniform_instance(p0, 3, 2, 10, 10, 10, lat=5, bw=3, mlim_x1000=1000)
+            for f, x in zip(fields, vals):
+                if stage is None:
+                    getattr(b, f)[0] = x
+                else:
+                    getattr(b, f)[0, stage] = x
+            st, msg = cp.validate_record(cp.pack_instances(b))
+            assert st == want, (why, vals, st, msg)
+            if want:
+                assert msg, why
+
+
+def _grid(pp=(4,), mb=(8,), mlim=(1000,), lat=(0, 50), bw=(0, 20), tdp=(0,), p_base=4, m_f=2):
+    from workloads.core import Grid
+    base = K.uniform_instance(p_base, 8, 2, 100, 100, 100, m_f=m_f, m_d=-(m_f // 2), m_w=-(m_f - m_f // 2))
+    return Grid(base=base, n_dc=2, pp_vals=list(pp), mb_vals=list(mb), lat=np.array(lat), bw=np.array(bw),
+                mlim_x1000=np.array(mlim), tdp=np.array(tdp), cand_mask=0b11111)
+
+
+def test_sweep_grid_validation_through_the_abi():
+    """check_grid (cp_sweep_shard / cp_sweep_shard_rank / cp_sweep_partition) rejects grids whose
+    synthesized instances would be invalid with CP_EINVAL, synchronously and before any device work,
+    instead of reporting their points as "no feasible candidate": a p beyond the base record's stages
+    (zero durations), a memory budget below m_f, a budget beyond int32, negative axes."""
+    lib = cp._lib.load()
+    b = (C.c_int64 * 3)()
+    assert lib.cp_sweep_partition(C.byref(cp.api.to_cp_grid(_grid())), 2, b) == 0
+    bad = {
+        "p beyond the base record": cp.api.to_cp_grid(_grid(pp=(4, 8))),
+        "M_L < m_f": cp.api.to_cp_grid(_grid(mlim=(1000, 100))),
+        "M_L beyond int32": cp.api.to_cp_grid(_grid(mlim=(1000, 2**31 - 1), m_f=1000)),
+    }
+    g = cp.api.to_cp_grid(_grid())
+    g.lat[1] = -5
+    bad["negative latency"] = g
+    g = cp.api.to_cp_grid(_grid())
+    g.tdp[0] = -1
+    bad["negative DP time"] = g
+    for why, cg in bad.items():
+        assert lib.cp_sweep_partition(C.byref(cg), 2, b) == -1, why              # CP_EINVAL
+        assert lib.cp_sweep_shard(C.byref(cg), 0, 1, None, None, None, 0, None) == -1, why
+        assert lib.cp_sweep_shard_rank(C.byref(cg), 0, 1, None, None, None, 0, None) == -1, why
+
+
+def test_sweep_workspace_covers_global_rings():
+    """A grid whose in-flight bound min(m, M_L / m_f) exceeds what one block's shared memory holds
+    gets global-memory rings per p-class in the sweep workspace (cp_workspace_bytes(2, grid))."""
+    lib = cp._lib.load()
+    small = cp.api.to_cp_grid(_grid())
+    assert lib.cp_workspace_bytes(2, C.byref(small), 0) == 256
+    big = cp.api.to_cp_grid(_grid(pp=(2, 4), mb=(1024,), mlim=(600000,)))
+    nb = lib.cp_workspace_bytes(2, C.byref(big), 0)
+    assert nb >= 256 + 2 * 148 * 4 * 2 * 1024 * 32 * 4, nb

@@ -672,3 +672,91 @@ def test_e1_orderings_spec_acceptance_5(oracle_lib):
     for (a, b), r in res.items():
         if (a, b) != (0, 0):
             assert r["iv1f1b"] >= max(r["zbv"], r["zbh1"], r["greedy"]), ((a, b), r)
+
+
+# --------------------------------------------------------------------------- instance invariants
+# One hand-built violation per invariant of SPEC.md:46-50 (ProblemSpec invariants) and of the
+# readings that add to them (Q10 memory signs, Q12 every block >= n_sub ticks, Q19 DP times >= 0,
+# CP_MAX_STAGES).  Each starts from a valid instance and changes one invariant at one stage (the
+# memory cases move a second delta so that only the named invariant breaks), so a validator that
+# skips, mis-indexes or inverts any single test fails here.  The boundary value that must stay
+# VALID (equality case or zero) is checked beside each.
+_INVARIANT_CASES = [
+    # (SPEC / reading, fields, stage, bad values, still-valid values)
+    ("SPEC.md:46 n_pp >= 1", ("p",), None, (0,), (1,)),
+    ("SPEC.md:46 n_mb >= 1", ("m",), None, (0,), (1,)),
+    ("SPEC.md:46 n_sub >= 1", ("n_sub",), None, (0,), (1,)),
+    ("CP_MAX_STAGES p <= 32", ("p",), None, (33,), (32,)),
+    ("SPEC.md:46 durations > 0 (F)", ("t_f",), 2, (0,), (1,)),
+    ("SPEC.md:46 durations > 0 (D)", ("t_d",), 0, (-5,), (1,)),
+    ("SPEC.md:46 durations > 0 (W)", ("t_w",), 3, (0,), (1,)),
+    ("SPEC.md:46 alpha >= 0 (fwd latency)", ("lat_f",), 1, (-1,), (0,)),
+    ("SPEC.md:46 beta >= 0 (fwd window)", ("bw_f",), 0, (-1,), (0,)),
+    ("SPEC.md:46 alpha >= 0 (bwd latency)", ("lat_b",), 2, (-3,), (0,)),
+    ("SPEC.md:46 beta >= 0 (bwd window)", ("bw_b",), 1, (-2,), (0,)),
+    ("SPEC.md:37 m_f > 0", ("m_f", "m_d", "m_w"), 1, (0, 0, 0), (1, 0, -1)),
+    ("SPEC.md:37 m_d <= 0", ("m_d", "m_w"), 2, (1, -3), (0, -2)),
+    ("SPEC.md:37 m_w <= 0", ("m_w", "m_d"), 0, (1, -3), (0, -2)),
+    ("SPEC.md:48 m_f + m_d + m_w = 0", ("m_w",), 3, (-2,), (-1,)),
+    ("SPEC.md:49 m_limit >= m_f", ("m_lim",), 1, (1,), (2,)),
+    ("Q19 t_dp >= 0", ("t_dp",), 2, (-1,), (0,)),
+    ("Q19 t_ag >= 0", ("t_ag",), 0, (-1,), (0,)),
+]
+
+
+def _full(batch, i=0):
+    """Instance i as a dict with all 32 per-stage / per-boundary slots (item() trims to p)."""
+    d = {"p": int(batch.p[i]), "m": int(batch.m[i]), "n_sub": int(batch.n_sub[i]), "zero1": int(batch.zero1[i])}
+    for k in ("t_f", "t_d", "t_w", "m_f", "m_d", "m_w", "m_lim", "t_dp", "t_ag", "lat_f", "bw_f", "lat_b", "bw_b"):
+        d[k] = np.array(getattr(batch, k)[i], copy=True)
+    return d
+
+
+@pytest.mark.parametrize("why,fields,stage,bad,ok", _INVARIANT_CASES, ids=[c[0] for c in _INVARIANT_CASES])
+def test_validate_instance_each_invariant(oracle_lib, why, fields, stage, bad, ok):
+    b = K.uniform_instance(4, 3, 2, 10, 10, 10, lat=5, bw=3, mlim_x1000=1000)
+    if "p" in fields and bad[0] > 4:          # a 33- / 32-stage variant: fill every slot validly
+        b = K.uniform_instance(32, 3, 2, 10, 10, 10, lat=5, bw=3, mlim_x1000=1000)
+    base = _full(b)
+    assert oracle_lib.validate_instance(base) == 0
+
+    def with_values(vals):
+        d = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in base.items()}
+        for f, x in zip(fields, vals):
+            if stage is None:
+                d[f] = x
+            else:
+                d[f][stage] = x
+        return d
+
+    bad_d = with_values(bad)
+    assert oracle_lib.validate_instance(bad_d) == 8, why
+    assert oracle_lib.validate_instance(with_values(ok)) == 0, why
+    if 1 <= bad_d["p"] <= 32 and bad_d["m"] >= 1 and bad_d["n_sub"] >= 1:
+        # the greedy and the simulator refuse it with the same status
+        assert oracle_lib.greedy(bad_d)["status"] == 8, why
+        c, ln = oracle_lib.build_static("1f1b", bad_d["p"], bad_d["m"])
+        assert oracle_lib.simulate(bad_d, c, ln)["status"] == 8, why
+
+
+@pytest.mark.parametrize("n_sub", [2, 4])
+@pytest.mark.parametrize("fld", ["t_f", "t_d", "t_w"])
+def test_validate_instance_every_block_at_least_n_sub(oracle_lib, n_sub, fld):
+    """Q12 (changed from t_w only): every sub-block of every block (PAPER.md:377 splits every
+    computation block into n_sub) lasts >= 1 tick, so each of t_f, t_d, t_w must be >= n_sub."""
+    d = _full(K.uniform_instance(3, 2, 1, 10, 10, 10, n_sub=n_sub))
+    d[fld][1] = n_sub - 1
+    assert oracle_lib.validate_instance(d) == 8
+    d[fld][1] = n_sub
+    assert oracle_lib.validate_instance(d) == 0
+
+
+def test_validate_instance_ignores_padding_and_unused_boundary(oracle_lib):
+    """Only stages s < p and boundaries s < p - 1 are inspected: garbage past p (and in boundary
+    p - 1, the Loop wrap slot, unused under UD) leaves a valid instance valid."""
+    d = _full(K.uniform_instance(3, 2, 1, 10, 10, 10))
+    for k in ("t_f", "t_d", "t_w", "m_f", "m_lim"):
+        d[k][3:] = -7
+    for k in ("lat_f", "bw_f", "lat_b", "bw_b"):
+        d[k][2:] = -9
+    assert oracle_lib.validate_instance(d) == 0

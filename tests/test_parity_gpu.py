@@ -319,6 +319,20 @@ def test_sweep_config5_sample_and_shards(O):
         assert torch.equal(acc_r.cpu(), torch.from_numpy(full_h)), ("rank shards", world)
 
 
+def test_sweep_global_ring_fallback(O):
+    """n_mb = 1024 with a budget that admits every microbatch in flight: the lead bound (1024 slots,
+    256 KB of rings per warp) exceeds one block's shared memory, so the engine pass of that p-class
+    runs with global-memory rings from the sweep workspace; greedy candidates fall back to it too.
+    Every point and candidate against the oracle."""
+    from workloads.core import Grid
+    grid = Grid(base=K.uniform_instance(4, 8, 2, 100, 90, 80), n_dc=2, pp_vals=[2, 4], mb_vals=[1024],
+                lat=np.array([0, 50]), bw=np.array([30]), mlim_x1000=np.array([600000]), tdp=np.array([0, 70]),
+                cand_mask=0b111111)
+    keys, cm = cp.sweep_shard(grid, cand=True)
+    torch.cuda.synchronize()
+    check_sweep(O, grid, keys.cpu().numpy(), cm.cpu().numpy(), range(grid.n_points))
+
+
 # ------------------------------------------------------------------------------------- config 4 at full size
 def test_config4_full_size_sampled(O):
     """Config 4 at BASELINE size (1e6 perturbed valid schedules, p=32, 4 DCs, m=64) in the bench

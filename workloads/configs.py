@@ -85,9 +85,10 @@ def gpt16_grid() -> Grid:
 
 # ---------------------------------------------------------------------------------------
 # config 3 -- greedy generation for 1e5 instances varying memory limit and DP overlap
-def greedy_batch(n=100_000, seed=SEED, p=16, n_dc=2, m=32) -> InstanceBatch:
+def greedy_batch(n=100_000, seed=SEED, p=16, n_dc=2, m=32, id0=0) -> InstanceBatch:
+    """Instances id0 .. id0+n-1 of the config-3 population (each drawn from its own id)."""
     b = InstanceBatch.empty(n)
-    ids = np.arange(n, dtype=np.uint64)
+    ids = np.arange(id0, id0 + n, dtype=np.uint64)
 
     def draw(tag, k):
         return (splitmix64(np.uint64(seed) ^ (ids * np.uint64(64)) ^ np.uint64(tag)) % np.uint64(k)).astype(np.int64)
