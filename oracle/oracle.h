@@ -122,6 +122,26 @@ void or_build_zbh1(int32_t p, int32_t m, int8_t* codes, int32_t* len, int32_t ma
 int64_t or_enumerate_opt(const or_inst* I, int64_t max_plans, int8_t* best_codes, int32_t* best_len,
                          int32_t maxlen, or_result* best);
 
+/* Exact optimum over the same plan set by branch and bound (bnb.c): DFS over block appends with the
+ * greedy's makespan as incumbent, Jackson-preemptive per-stage lower bounds and dominance on
+ * interface times.  Tiny instances: p <= 8, m <= 16, n_sub = 1.  Returns 1 if proven optimal, 0 if
+ * max_nodes ran out (best = best plan found, info->bound = root lower bound), -1 if not applicable.
+ * max_table_bytes caps the dominance table (a full table only stops recording).  flags (tests):
+ * OR_BNB_NO_DOMINANCE disables the dominance cut, OR_BNB_NO_JPS replaces the per-stage preemptive
+ * bound by the per-block head + duration + tail bound -- independent cut logic, same optimum. */
+#define OR_BNB_NO_DOMINANCE 1
+#define OR_BNB_NO_JPS 2
+typedef struct {
+  int64_t greedy;        /* incumbent: or_greedy makespan (n_sub = 1) */
+  int64_t root_bound;    /* lower bound at the root */
+  int64_t bound;         /* proven lower bound: the optimum if proven, else root_bound */
+  int64_t nodes;         /* search nodes visited */
+  int64_t table_bytes;   /* dominance vectors recorded */
+  int32_t proven;
+} or_bnb_info;
+int32_t or_bnb_opt(const or_inst* I, int64_t max_nodes, int64_t max_table_bytes, int32_t flags, int8_t* best_codes,
+                   int32_t* best_len, int32_t maxlen, or_result* best, or_bnb_info* info);
+
 /* SI -> ticks / units quantization; returns 0 or OR_ST_BAD_INSTANCE. */
 int32_t or_quantize(const or_spec_si* S, or_inst* out);
 

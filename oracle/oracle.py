@@ -35,6 +35,11 @@ class OrResult(C.Structure):
 D64A = C.c_double * MAXP
 
 
+class OrBnbInfo(C.Structure):
+    _fields_ = [("greedy", C.c_int64), ("root_bound", C.c_int64), ("bound", C.c_int64), ("nodes", C.c_int64),
+                ("table_bytes", C.c_int64), ("proven", C.c_int32)]
+
+
 class OrSpecSI(C.Structure):
     _fields_ = [("p", C.c_int32), ("m", C.c_int32), ("n_sub", C.c_int32), ("zero1", C.c_int32),
                 ("n_dc", C.c_int32), ("dc_of_stage", C.c_int32 * MAXP)] + [
@@ -59,7 +64,8 @@ class OrGrid(C.Structure):
 
 def build(force=False):
     src = os.path.join(_HERE, "oracle.c")
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(src), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+    srcs = [src, os.path.join(_HERE, "bnb.c"), os.path.join(_HERE, "oracle.h")]
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(x) for x in srcs):
         subprocess.check_call(["make", "-s", "-C", _HERE, "-B"] if force else ["make", "-s", "-C", _HERE])
     return _LIB
 
@@ -93,6 +99,9 @@ def lib():
         L.or_build_iv1f1b.argtypes = [C.c_int32, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32]
         L.or_enumerate_opt.restype = C.c_int64
         L.or_enumerate_opt.argtypes = [P(OrInst), C.c_int64, P(C.c_int8), P(C.c_int32), C.c_int32, P(OrResult)]
+        L.or_bnb_opt.restype = C.c_int32
+        L.or_bnb_opt.argtypes = [P(OrInst), C.c_int64, C.c_int64, C.c_int32, P(C.c_int8), P(C.c_int32), C.c_int32, P(OrResult),
+                                 P(OrBnbInfo)]
         L.or_quantize.restype = C.c_int32
         L.or_quantize.argtypes = [P(OrSpecSI), P(OrInst)]
         L.or_validate_instance.restype = C.c_int32
@@ -258,6 +267,26 @@ def enumerate_opt(d, max_plans=2_000_000) -> dict:
                                ln.ctypes.data_as(C.POINTER(C.c_int32)), maxlen, C.byref(res))
     out = _result(res, p)
     out["evaluated"], out["codes"], out["len"] = n, c, ln
+    return out
+
+
+BNB_NO_DOMINANCE, BNB_NO_JPS = 1, 2
+
+
+def bnb_opt(d, max_nodes=50_000_000, max_table_bytes=4 << 30, flags=0) -> dict:
+    """Exact optimum (n_sub = 1 split plans) by branch and bound (bnb.c).  Returns the re-simulated best
+    plan's result plus proven / bound / nodes / greedy / root_bound; rc -1 = not applicable."""
+    p, m = int(d["p"]), int(d["m"])
+    maxlen = 3 * m
+    c = np.zeros((p, maxlen), dtype=np.int8)
+    ln = np.zeros(p, dtype=np.int32)
+    res, info = OrResult(), OrBnbInfo()
+    rc = lib().or_bnb_opt(C.byref(to_or_inst(d)), int(max_nodes), int(max_table_bytes), int(flags),
+                          c.ctypes.data_as(C.POINTER(C.c_int8)), ln.ctypes.data_as(C.POINTER(C.c_int32)), maxlen,
+                          C.byref(res), C.byref(info))
+    out = _result(res, p)
+    out.update(rc=rc, codes=c, len=ln, proven=bool(info.proven), bound=info.bound, nodes=info.nodes,
+               greedy=info.greedy, root_bound=info.root_bound, table_bytes=info.table_bytes)
     return out
 
 
