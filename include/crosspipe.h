@@ -1,5 +1,5 @@
 /*
- * crosspipe.h -- C ABI (v2, CP_ABI_VERSION) of the B200-native CrossPipe hot path (arXiv 2507.00217).
+ * crosspipe.h -- C ABI (v3, CP_ABI_VERSION) of the B200-native CrossPipe hot path (arXiv 2507.00217).
  *
  * What the calls compute (citations are PAPER.md line numbers):
  *   cp_simulate    §3.5 pipeline performance model (:257-260): per-stage block order ->
@@ -40,7 +40,8 @@
 extern "C" {
 #endif
 
-#define CP_ABI_VERSION 2u      /* v2: ZB-H1 sweep candidate (6 candidates), cp_build_static */
+#define CP_ABI_VERSION 3u      /* v2: ZB-H1 sweep candidate (6 candidates), cp_build_static;
+                                  v3: cp_exact_bnb, CPI_INCOMPLETE, grid-sized sweep workspace */
 #define CP_MAX_STAGES 32      /* lane-per-stage design: p <= 32 */
 #define CP_MAX_MB 1024        /* microbatches per instance */
 #define CP_MAX_SUB 16         /* n_sub limit of the GPU path */
@@ -74,7 +75,8 @@ typedef enum {                /* per-item status bitmask */
   CPI_MEM_EXCEEDED = 2,       /* completed, but a stage's peak > m_lim */
   CPI_BAD_PLAN = 4,           /* static plan check failed (reading Q29) */
   CPI_BAD_INSTANCE = 8,       /* instance invariant violated (Q10, Q12) */
-  CPI_OVERFLOW = 16           /* exceeds int32 horizon (U >= 2^30) or GPU size limits */
+  CPI_OVERFLOW = 16,          /* exceeds int32 horizon (U >= 2^30) or GPU size limits */
+  CPI_INCOMPLETE = 64         /* cp_exact_bnb: a node / round / frontier limit stopped the search */
 } cp_item;
 
 /* Instance record v1: 1792 B, 128-B aligned, int32 ticks / memory units.
@@ -238,6 +240,34 @@ int32_t cp_build_static(int32_t kind, const cp_instances* inst, const cp_schedul
 size_t cp_exact_workspace_bytes(int32_t n, int32_t cap);
 int32_t cp_exact(const cp_instances* inst, const cp_schedules* out, const int32_t* upper, int32_t* makespan,
                  int32_t* status, int32_t cap, int64_t max_plans, void* ws, size_t ws_bytes, void* stream);
+
+/* Exact optimum of tiny instances by parallel branch and bound (exact_bnb.cu; SURVEY.md §8(f)
+ * NEXT 3, §8(c) c5): the same optimum as cp_exact -- min over every plan of split blocks (F, D, W;
+ * n_sub must be 1) in microbatch order per type, D_j after F_j, W_j after D_j, within m_lim along the
+ * sequence, of its §3.5 makespan (§4.1 :313-363) -- found by search instead of
+ * enumeration, which reaches the paper's 4 x 8 E1 setup (:486, :491).  Nodes are partial schedules
+ * extended one block at a time; a node is cut by a lower bound (per-stage Jackson preemptive
+ * schedule with dependency heads and tails) against the instance's incumbent, or by dominance (a
+ * recorded node with the same block counts and no later interface times).  Warps search depth
+ * first for at most `budget` nodes per work item and return the rest of their stack to a frontier;
+ * the call repeats rounds until the frontier is empty, so it SYNCHRONIZES `stream` once per round.
+ * Per instance: makespan [n] int32 and the plan in out (2-bit entries, 3m per row, rows >= n_pp
+ * zero); status 0 = proven optimal; CPI_INCOMPLETE = stopped by max_nodes (nodes searched over all
+ * instances), max_rounds or a full frontier: makespan / plan = best found, bound = lower bound
+ * proven at the root; CPI_DEADLOCK = no plan reaches upper; CPI_OVERFLOW = outside the limits
+ * (n_pp <= 8, n_mb <= 16, n_sub = 1, horizon < 2^29 ticks, record invariants).
+ * upper (nullable, device) [n] int32: a feasible makespan per instance (e.g. cp_greedy's with
+ * n_sub = 1), -1 for none; the search returns a plan of makespan <= upper, so pass one some plan
+ * reaches.  bound (nullable) [n] int32: proven lower bound (= makespan when status 0).  nodes
+ * (nullable) [n] int64: nodes searched.  front_cap: frontier items per round; table_entries: the
+ * per-instance dominance table, a power of two.  ws: cp_exact_bnb_workspace_bytes(...) bytes.
+ * out: n == inst->n, inst_of NULL, stage_stride >= max_pp, 16*words >= 3*max_mb.  Errors:
+ * CP_EINVAL, CP_EWORKSPACE, CP_ECUDA. */
+size_t cp_exact_bnb_workspace_bytes(const cp_instances* inst, int32_t front_cap, int64_t table_entries);
+int32_t cp_exact_bnb(const cp_instances* inst, const cp_schedules* out, const int32_t* upper, int32_t* makespan,
+                     int32_t* status, int32_t* bound, int64_t* nodes, int32_t budget, int64_t max_nodes,
+                     int32_t max_rounds, int32_t front_cap, int64_t table_entries, void* ws, size_t ws_bytes,
+                     void* stream);
 
 /* Evaluate the points owned by `rank` of `world` under blocked ownership: every (n_pp, n_mb) block
  * of inner = n_lat*n_bw*n_mem*n_dp consecutive points is cut into `world` contiguous slices,

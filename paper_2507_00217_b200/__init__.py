@@ -9,10 +9,10 @@ from . import _lib
 _lib.load()
 
 from .api import (  # noqa: E402,F401
-    KEY_NONE, KEY_OVER, HostPipeline, Instances, bubble_ratios, build_static, decode_key, exact, greedy, pack_instances, quantize,
+    KEY_NONE, KEY_OVER, HostPipeline, Instances, bubble_ratios, build_static, decode_key, exact, exact_bnb, greedy, pack_instances, quantize,
     records_to_device, ring_hint, sweep_shard_rank,
     simulate, sweep_partition, sweep_shard, to_cp_grid, validate_record,
 )
 
-__all__ = ["Instances", "simulate", "greedy", "exact", "build_static", "bubble_ratios", "sweep_shard", "sweep_shard_rank", "sweep_partition", "quantize", "decode_key",
+__all__ = ["Instances", "simulate", "greedy", "exact", "exact_bnb", "build_static", "bubble_ratios", "sweep_shard", "sweep_shard_rank", "sweep_partition", "quantize", "decode_key",
            "pack_instances", "records_to_device", "ring_hint", "to_cp_grid", "validate_record"]

@@ -75,8 +75,9 @@ class CpSpecSI(C.Structure):
 
 EXPORTS = ("cp_abi_version", "cp_status_string", "cp_workspace_bytes", "cp_simulate", "cp_greedy",
            "cp_build_static", "cp_sweep_shard", "cp_sweep_shard_rank", "cp_sweep_partition", "cp_quantize",
-           "cp_validate_instance", "cp_exact", "cp_exact_workspace_bytes")
-ABI_VERSION = 2
+           "cp_validate_instance", "cp_exact", "cp_exact_workspace_bytes", "cp_exact_bnb",
+           "cp_exact_bnb_workspace_bytes")
+ABI_VERSION = 3
 N_CAND = 6                    # sweep candidates: 0 GPipe, 1 1F1B, 2/3/4 greedy n_sub 1/2/4, 5 ZB-H1
 PLAN_KINDS = {"gpipe": 0, "1f1b": 1, "zbh1": 5, "iv1f1b": 6, "zbv": 7}   # iv1f1b: Loop, zbv: Wave plans (4-bit)
 
@@ -116,6 +117,12 @@ def load():
     L.cp_exact.restype = C.c_int32
     L.cp_exact.argtypes = [P(CpInstances), P(CpSchedules), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64,
                            C.c_void_p, C.c_size_t, C.c_void_p]
+    L.cp_exact_bnb_workspace_bytes.restype = C.c_size_t
+    L.cp_exact_bnb_workspace_bytes.argtypes = [P(CpInstances), C.c_int32, C.c_int64]
+    L.cp_exact_bnb.restype = C.c_int32
+    L.cp_exact_bnb.argtypes = [P(CpInstances), P(CpSchedules), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_int64, C.c_void_p,
+                               C.c_size_t, C.c_void_p]
     L.cp_quantize.restype = C.c_int32
     L.cp_quantize.argtypes = [P(CpSpecSI), C.c_void_p]
     L.cp_validate_instance.restype = C.c_int32

@@ -288,6 +288,38 @@ def exact(inst: Instances, *, cap=65536, max_plans=1 << 32, upper=None, stage_st
     return {"ops": ops, "len": ln, "makespan": ms, "status": st}
 
 
+def exact_bnb(inst: Instances, *, upper=None, budget=2048, max_nodes=1 << 34, max_rounds=100000,
+              front_cap=1 << 20, table_entries=1 << 20, stage_stride=None, stream=None):
+    """cp_exact_bnb: the makespan-optimal split plan (n_sub = 1) of every tiny instance by parallel
+    branch and bound on the GPU -> dict(ops, len, makespan, status, bound, nodes).  status 0 = proven
+    optimal, CPI_INCOMPLETE (64) = stopped by a limit (bound = root lower bound).  upper: optional
+    int32 [n] device tensor of feasible makespans (e.g. the greedy's), seeding the incumbent.  The
+    call synchronizes its stream once per search round."""
+    _require_cuda(inst.dev)
+    dev = inst.dev.device
+    n = inst.n
+    stride = stage_stride or inst.max_pp
+    words = max(1, (3 * min(inst.max_mb, 16) + 15) // 16)
+    d = inst.desc(None)
+    nb = int(L.load().cp_exact_bnb_workspace_bytes(C.byref(d), int(front_cap), int(table_entries)))
+    with _on_stream(stream, inst.dev, upper) as s:
+        ops = torch.empty((n, words, stride), dtype=torch.int32, device=dev)
+        ln = torch.empty((n, stride), dtype=torch.int16, device=dev)
+        ms = torch.empty(n, dtype=torch.int32, device=dev)
+        st = torch.empty(n, dtype=torch.int32, device=dev)
+        bd = torch.empty(n, dtype=torch.int32, device=dev)
+        nd = torch.empty(n, dtype=torch.int64, device=dev)
+        ws = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        sc = L.CpSchedules(n, stride, words, 0, None, ops.data_ptr(), ln.data_ptr())
+        up = None if upper is None else upper.to(device=dev, dtype=torch.int32).contiguous()
+        rc = L.load().cp_exact_bnb(C.byref(d), C.byref(sc), _ptr(up), C.c_void_p(ms.data_ptr()),
+                                   C.c_void_p(st.data_ptr()), C.c_void_p(bd.data_ptr()), C.c_void_p(nd.data_ptr()),
+                                   int(budget), int(max_nodes), int(max_rounds), int(front_cap), int(table_entries),
+                                   C.c_void_p(ws.data_ptr()), nb, _stream(s))
+    L.check(rc, "cp_exact_bnb")
+    return {"ops": ops, "len": ln, "makespan": ms, "status": st, "bound": bd, "nodes": nd}
+
+
 def bubble_ratios(result: dict, n_pp):
     """Per-stage bubble ratios from simulate(..., stats=True) (reading Q7): local =
     1 - busy / (last_end - first_start) over the stage's active window, global = 1 - busy / makespan.

@@ -438,6 +438,39 @@ int32_t cp_exact(const cp_instances* in, const cp_schedules* out, const int32_t*
                            out->len, makespan, status, stream) == cudaSuccess ? CP_OK : CP_ECUDA;
 }
 
+static void bnb_dims(const cp_instances* in, int* lmax, int* vlen) {
+  const int p = std::min(in->max_pp, cpk::kBnbMaxP), m = std::min(in->max_mb, cpk::kBnbMaxM);
+  *lmax = 3 * p * m;
+  *vlen = 3 * p - 1 + 2 * (p - 1) * m;
+}
+
+size_t cp_exact_bnb_workspace_bytes(const cp_instances* in, int32_t front_cap, int64_t table_entries) {
+  if (!in || in->n < 1 || front_cap < 1 || table_entries < 1) return 0;
+  int lmax, vlen;
+  bnb_dims(in, &lmax, &vlen);
+  return cpk::bnb_layout(in->n, lmax, vlen, front_cap, table_entries).bytes;
+}
+
+int32_t cp_exact_bnb(const cp_instances* in, const cp_schedules* out, const int32_t* upper, int32_t* makespan,
+                     int32_t* status, int32_t* bound, int64_t* nodes, int32_t budget, int64_t max_nodes,
+                     int32_t max_rounds, int32_t front_cap, int64_t table_entries, void* ws, size_t ws_bytes,
+                     void* stream) {
+  int rc = check_instances(in);
+  if (rc) return rc;
+  if (!out || out->n != in->n || out->inst_of || !out->ops || !out->len || !makespan || !status) return CP_EINVAL;
+  if (out->stage_stride < in->max_pp || out->words < 1 || 16LL * out->words < 3LL * std::min(in->max_mb, cpk::kBnbMaxM))
+    return CP_EINVAL;
+  if (budget < 1 || max_nodes < 1 || max_rounds < 1 || front_cap < 1 || table_entries < 1 ||
+      (table_entries & (table_entries - 1)))
+    return CP_EINVAL;
+  if (!ws || ws_bytes < cp_exact_bnb_workspace_bytes(in, front_cap, table_entries)) return CP_EWORKSPACE;
+  int lmax, vlen;
+  bnb_dims(in, &lmax, &vlen);
+  return cpk::launch_bnb(in->inst, in->n, upper, lmax, vlen, front_cap, table_entries, budget, max_nodes, max_rounds,
+                         ws, out->stage_stride, out->words, out->ops, out->len, makespan, status, bound,
+                         reinterpret_cast<long long*>(nodes), stream) == cudaSuccess ? CP_OK : CP_ECUDA;
+}
+
 int32_t cp_greedy(const cp_instances* in, const cp_schedules* out, const cp_results* res, void* ws, size_t ws_bytes,
                   void* stream) {
   int rc = check_instances(in);

@@ -80,6 +80,18 @@ int launch_exact(const cp_inst_v1* inst, int n, int cap, long long max_plans, co
                  void* stream);
 size_t exact_ws_seq_bytes(int n, int cap);
 size_t exact_ws_bytes(int n, int cap);
+// cp_exact_bnb (exact_bnb.cu): batched parallel branch and bound for tiny instances
+constexpr int kBnbMaxP = 8;            // stages
+constexpr int kBnbMaxM = 16;           // microbatches
+struct BnbLayout {
+  size_t off_bi, off_ctl, off_plan, off_cnt, off_front0, off_front1, off_table, bytes;
+  int front_stride, table_stride;
+};
+BnbLayout bnb_layout(int n, int lmax, int vlen_max, int front_cap, long long table_cap);
+int launch_bnb(const cp_inst_v1* inst, int n, const int32_t* upper, int lmax, int vlen_max, int front_cap,
+               long long table_cap, int budget, long long max_nodes, int max_rounds, void* ws, int stage_stride,
+               int words, uint32_t* ops, uint16_t* len, int32_t* makespan, int32_t* status, int32_t* bound,
+               long long* nodes_out, void* stream);
 int launch_sweep_init(unsigned long long* keys, int32_t* cand_ms, long long lo, long long hi, long long inner, int own_lo,
                       int own_hi, void* stream);
 

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_strings():
     lib = L.load()
-    assert lib.cp_abi_version() == 2
+    assert lib.cp_abi_version() == 3
     assert b"workspace" in lib.cp_status_string(-4)
     assert b"deadlock" in lib.cp_status_string(1)
 

@@ -1,0 +1,56 @@
+#!/usr/bin/env python3
+"""cp_exact_bnb on the GPU vs the oracle's branch and bound: the 16-point 4 x 8 E1 grid (config 1)
+in one batch, then harder uniform instances (4 x 12, 6 x 8, 4 x 16).  Writes profiles/bnb_gpu_r02.json."""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2507_00217_b200 as cp  # noqa: E402
+from workloads import InstanceBatch, configs as K  # noqa: E402
+
+
+def run(batch, **kw):
+    inst = cp.Instances(batch)
+    g = cp.greedy(inst)
+    up = g["makespan"].to(torch.int32)
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    r = cp.exact_bnb(inst, upper=up, **kw)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t
+    return r, up.cpu().tolist(), dt
+
+
+def main():
+    out = {}
+    pts = [(a, b) for a in (0, 0.5, 1, 2) for b in (0, 0.5, 1, 2)]
+    batch = InstanceBatch.concat([K.tiny(a, b) for a, b in pts])
+    r, up, dt = run(batch)
+    r, up, dt = run(batch)                          # warm
+    out["tiny_4x8_16pts"] = {"seconds": dt, "points": [
+        {"lat_ratio": a, "bw_ratio": b, "optimum": int(r["makespan"][i]), "status": int(r["status"][i]),
+         "greedy": up[i], "nodes": int(r["nodes"][i])} for i, (a, b) in enumerate(pts)]}
+    print("tiny", dt, [int(x) for x in r["makespan"]], [int(x) for x in r["status"]], flush=True)
+    for (p, m) in ((4, 12), (6, 8), (4, 16), (8, 8)):
+        sel = [(1, 0.5), (2, 2), (0.5, 1)]
+        batch = InstanceBatch.concat([K.uniform_instance(p, m, 2, 100, 100, 100, lat=int(a * 100), bw=int(b * 100),
+                                                         mlim_x1000=1000) for a, b in sel])
+        r, up, dt = run(batch, max_nodes=int(os.environ.get("BNB_MAX_NODES", 4_000_000_000)),
+                        table_entries=1 << 22, front_cap=1 << 21)
+        out[f"uniform_{p}x{m}"] = {"seconds": dt, "points": [
+            {"lat_ratio": a, "bw_ratio": b, "makespan": int(r["makespan"][i]), "bound": int(r["bound"][i]),
+             "status": int(r["status"][i]), "greedy": up[i], "nodes": int(r["nodes"][i])} for i, (a, b) in enumerate(sel)]}
+        print(p, m, dt, out[f"uniform_{p}x{m}"]["points"], flush=True)
+    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    with open(os.path.join(ROOT, "profiles", "bnb_gpu_r02.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
