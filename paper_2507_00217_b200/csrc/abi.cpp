@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cstdint>
 #include <vector>
 
 #include "crosspipe.h"
@@ -144,21 +145,43 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
   const int nseg = 32 >> a.seg_lg;
   a.plan_words = sc->words <= kPlanCapWords ? sc->words : 0;
 #ifndef CP_DEBUG
-  if (mode == cpk::MODE_SIM && nseg == 1 && sc->stage_stride == 32 && a.plan_words > 0 && !res->t_start &&
+  // k_sim32 with a timeline writes each lane's start ticks 8 at a time (two 16-B stores): rows must be
+  // 32-B aligned and hold every entry a valid row can have
+  const bool tl_vec = !res->t_start || (res->len_stride % 8 == 0 && res->len_stride >= 16 * sc->words &&
+                                        (reinterpret_cast<uintptr_t>(res->t_start) & 31) == 0);
+  if (mode == cpk::MODE_SIM && nseg == 1 && sc->stage_stride == 32 && a.plan_words > 0 && tl_vec &&
       !getenv_nofast()) {
-    // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row
+    // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row.  When every
+    // item uses instance 0, a 4-warp block shares one cost / increment table (24 resident warps).
+    const bool tl = res->t_start != nullptr;
     a.ring_slots = fast_ring_slots(in);
-    a.smem_words_per_warp = (cpk::kSim32TableWords + 2 * a.ring_slots * 32 + 2 * (a.plan_words + 1) * 32 + 64 + 4 + 64 + 256 + 3) & ~3;
-    const size_t per_warp = (size_t)a.smem_words_per_warp * 4;
-    if (per_warp * 2 <= kMaxSmemPerBlock) {
-      const int wpb = 2, threads = 64;
-      const size_t smem = per_warp * wpb;
-      int bps = smsp_balanced(cpk::sim32_blocks_per_sm(threads, smem), wpb);
+    a.shared_tab = (!sc->inst_of && in->n == 1 && !std::getenv("CP_SIM32_NOSHARE")) ? 1 : 0;
+    const cpk::Sim32Layout L1 = cpk::sim32_layout(a.ring_slots, a.plan_words, a.shared_tab != 0, tl);
+    a.smem_words_per_warp = L1.per_warp;
+    const int wpb = a.shared_tab ? 4 : 2, threads = 32 * wpb;
+    const size_t smem = ((size_t)L1.hdr + (size_t)wpb * L1.per_warp) * 4;
+    if (smem <= kMaxSmemPerBlock) {
+      int bps = smsp_balanced(cpk::sim32_blocks_per_sm(tl, threads, smem), wpb);
       if (const char* v = std::getenv("CP_SIM32_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
       const long long need = (n + wpb - 1) / wpb;
       const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
-      if (cpk::launch_sim32(a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      if (cpk::launch_sim32(tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      // Items that stalled on a full 8-slot ring (cyclic backpressure) are re-run from the
+      // overflow list by the same kernel with rings of R > n_mb slots, where no ring can fill (every
+      // producer -> consumer lead is <= n_mb); only when such rings exceed shared memory does the
+      // generic engine with global-memory rings take them.  An empty list costs one short launch.
       a.from_list = 1;
+      a.ring_slots = 1 << lg2_ceil((long long)in->max_mb + 1);
+      a.shared_tab = 0;
+      const cpk::Sim32Layout L2 = cpk::sim32_layout(a.ring_slots, a.plan_words, false, tl);
+      const size_t smem2 = ((size_t)L2.hdr + L2.per_warp) * 4;
+      if (smem2 <= kMaxSmemPerBlock && !std::getenv("CP_SIM32_ENGINE_FIXUP")) {
+        a.smem_words_per_warp = L2.per_warp;
+        const int bps2 = cpk::sim32_blocks_per_sm(tl, 32, smem2);
+        if (cpk::launch_sim32(tl, a, cpk::device_sm_count() * std::max(1, bps2), 32, smem2, stream) != cudaSuccess)
+          return CP_ECUDA;
+        return cudaGetLastError() == cudaSuccess ? CP_OK : CP_ECUDA;
+      }
       a.tma = 0;
       a.ring_slots = big_ring_slots(in);
       a.ring_g = rings;

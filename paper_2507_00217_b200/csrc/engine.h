@@ -54,16 +54,18 @@ struct Args {
   int64_t blk_inner;
   int32_t own_lo, own_hi;
   int32_t chunk_pattern;               // two-chunk plans: CP_PATTERN_WAVE or CP_PATTERN_LOOP
+  int32_t shared_tab;                  // k_sim32: one cost / increment table per block (all items use instance 0)
   cp_grid grid;
 };
 
 // launchers (return cudaError_t as int)
 int launch_engine(Mode mode, bool ring_global, const Args& a, int blocks, int threads, size_t smem, void* stream);
-// fast path of cp_simulate (sim32.cu): one item per warp, stage_stride 32, smem plans (TMA), no timeline
-int launch_sim32(const Args& a, int blocks, int threads, size_t smem, void* stream);
+// fast path of cp_simulate (sim32.cu): one item per warp, stage_stride 32, smem plans (TMA); with a
+// timeline, start ticks are staged in shared memory and written 32 B per lane
+int launch_sim32(bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream);
+int sim32_blocks_per_sm(bool timeline, int threads, size_t smem);
 int launch_wave32(const Args& a, int blocks, int threads, size_t smem, void* stream);
 int wave32_blocks_per_sm(int threads, size_t smem);
-int sim32_blocks_per_sm(int threads, size_t smem);
 // fast path of cp_greedy (greedy_fast.cu): compile-time segment width W in {8, 16, 32}, no timeline
 // grid = false: cp_greedy; grid = true: the greedy candidates of cp_sweep_shard
 int launch_greedy_fast(int W, bool grid, const Args& a, int blocks, int threads, size_t smem, void* stream);
@@ -106,6 +108,37 @@ constexpr int kGreedyTableWords = 256;   // k_greedy_fast per-warp parameter tab
 // k_greedy_fast: 12 two-warp blocks per SM (6 warps per scheduler) fit its 9 KB per warp; the bound
 // caps registers at 85 (78 used)
 constexpr int kGreedyMinBlocks = 12;
-constexpr int kSim32TableWords = 1024;  // k_sim32 per-warp parameter tables: 2 x [4 codes][32 lanes] int4
+
+// k_sim32 shared-memory layout, in 32-bit words (host and device compute it the same way).
+// Block header: the per-code uniform table U (8 int4) and -- when every item uses one instance --
+// the cost table tabA [4 codes][32 lanes] int4.  Per warp: the F and D arrival rings [R][32] each,
+// two plan buffers of (words + 1) rows, a store-sink row, the zero row, 2 mbarriers, 2 x 32 link
+// clocks, tabA unless the block holds it, and with a timeline a [16][32] start-tick staging ring.
+struct Sim32Layout {
+  int uni, rings, plan, dum, zero, bars, link, tabA, stage, per_warp, hdr;
+};
+__host__ __device__ inline Sim32Layout sim32_layout(int R, int plan_words, bool shared_tab, bool timeline) {
+  Sim32Layout L;
+  L.uni = 0;                             // block-relative
+  L.rings = 0;
+  L.plan = 2 * R * 32;
+  L.dum = L.plan + 2 * (plan_words + 1) * 32;
+  L.zero = L.dum + 32;
+  L.bars = L.zero + 32;                  // 8-B aligned: every region above is a multiple of 32 words
+  L.link = L.bars + 4;
+  int w = L.link + 64;
+  if (shared_tab) {
+    L.tabA = 32;                         // block-relative, after U
+    L.hdr = 32 + 512;
+  } else {
+    L.tabA = w;
+    w += 512;
+    L.hdr = 32;
+  }
+  L.stage = w;
+  if (timeline) w += 512;
+  L.per_warp = (w + 3) & ~3;
+  return L;
+}
 
 }  // namespace cpk

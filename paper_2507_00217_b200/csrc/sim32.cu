@@ -1,13 +1,19 @@
 // sim32.cu -- fast path of cp_simulate for the dominant shape: one item per warp (17..32
 // stages, stage_stride 32), plan rows staged in shared memory by double-buffered TMA bulk
-// copies, arrival rings in shared memory, no per-entry timeline.
+// copies, arrival rings in shared memory; optionally the per-entry timeline (kTL), staged in
+// shared memory and written 8 start ticks (32 B) per lane at a time.
 //
 // Same semantics as k_engine<MODE_SIM> (engine.cu), which remains the reference GPU path for
-// every other shape and for the fix-up pass; both are parity-tested.
-// What makes this kernel fast is what it leaves out: the warp is one segment, so the "no block
-// executed this round" test is a single ballot with a warp-uniform branch; the state is the
-// minimum the §3.5 recurrence needs; the plan buffers carry one spare row so finished lanes
-// read without clamping.
+// every other shape; both are parity-tested.  What makes this kernel fast is what
+// it leaves out: the warp is one segment, so the "no block executed this round" test is a single
+// ballot with a warp-uniform branch; the state is the minimum the §3.5 recurrence needs; entries
+// past a row's end read as a never-ready D, so the round has no position test.  The round is
+// bound by shared-memory wavefronts and issue together: per-code values that are
+// the same for every lane come from broadcast rows, per-lane costs from one 128-bit row.
+//
+// Launches (abi.cpp): a first pass with 8-slot rings and occupancy backpressure over all items;
+// items that stalled on a full ring (cyclic backpressure) are re-run by a second launch of this
+// kernel over the overflow list with rings of R > n_mb slots, where no ring can fill.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,8 +42,17 @@ __device__ __forceinline__ int madd(int g, int d, int x) {
   asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(g), "r"(d), "r"(x));
   return r;
 }
+// timeline staging: the 8 start ticks in the lane's slots [k][lane], k < 8, -> two 16-B global stores
+__device__ __forceinline__ void tl_flush8(unsigned stg, int32_t* dst) {
+  int v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v[k]) : "r"(stg + 128u * k));
+  __stcs(reinterpret_cast<int4*>(dst), make_int4(v[0], v[1], v[2], v[3]));
+  __stcs(reinterpret_cast<int4*>(dst) + 1, make_int4(v[4], v[5], v[6], v[7]));
+}
 }  // namespace
 
+template <bool kTL>   // kTL: per-entry start ticks requested (A.t_start; len_stride % 8 == 0, 32-B aligned rows)
 __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args A) {
   extern __shared__ __align__(128) int32_t smem[];
   const int lane = threadIdx.x & 31;
@@ -48,32 +63,35 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
   const int PWr = PW + 1;                         // one spare row per buffer
   const long long gwarp = (long long)blockIdx.x * (blockDim.x >> 5) + wib;
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
-  // per-warp smem (words): [paramA 4*32 int4][paramB 4*32 int4][ringF R*32][ringD R*32]
-  //                        [plan 2*(PW+1)*32][sink 32][zero 32][2 mbarriers][link clocks 2*32]
-  //                        [counter increments 4*32 int2]
-  const int wbase = wib * A.smem_words_per_warp;
-  const int rbase = wbase + kSim32TableWords;
-  const int pbase0 = rbase + 2 * RW;
-  const int dum_row = kSim32TableWords + 2 * RW + 2 * PWr * 32;   // relative to wbase
-  const int zero_row = dum_row + 32;
+  const Sim32Layout Ly = sim32_layout(R, PW, A.shared_tab != 0, kTL);
+  const int wbase = Ly.hdr + wib * Ly.per_warp;
+  const int rbase = wbase + Ly.rings;
+  const int pbase0 = wbase + Ly.plan;
+  const int dum_row = Ly.dum;                     // relative to wbase
+  const int zero_row = Ly.zero;
+  const int tbase = A.shared_tab ? Ly.tabA : wbase + Ly.tabA;   // tabA (and tabC after it): block or warp
   uint32_t* const plan = reinterpret_cast<uint32_t*>(smem + pbase0);
-  uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + wbase + zero_row + 32);
-  int4* const tabA = reinterpret_cast<int4*>(smem + wbase) + lane;          // [code][lane]
-  int4* const tabB = reinterpret_cast<int4*>(smem + wbase + 512) + lane;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(smem + wbase + Ly.bars);
+  int4* const tabA = reinterpret_cast<int4*>(smem + tbase) + lane;          // [code][lane]
+  int4* const U = reinterpret_cast<int4*>(smem + Ly.uni);                  // [8] int4, block header
   const uint32_t plan_bytes = (uint32_t)A.words * 32u * 4u;
+  // items: [0, n_items), or (fix-up pass) the overflow list of the first pass
+  const long long n_items = A.from_list ? (long long)*(volatile int32_t*)A.ovf_count : (long long)A.n_items;
+  auto item_of = [&](long long t) -> long long { return A.from_list ? (long long)A.ovf_list[t] : t; };
 
-  long long item = gwarp;
+  long long t_it = gwarp;
   // the rings never written by a producer (stage 0's F ring) and the zero row read by W entries
   // must hold 0: clear both ring blocks and the zero row once
   for (int k = lane; k < 2 * RW; k += 32) smem[rbase + k] = 0;
   smem[wbase + zero_row + lane] = 0;
   if (lane == 0) { mbar_init(&bars[0]); mbar_init(&bars[1]); }
   __syncwarp();
-  if (lane == 0 && item < A.n_items) tma_load_1d(plan, A.ops + item * A.words * 32, plan_bytes, &bars[0]);
+  if (lane == 0 && t_it < n_items) tma_load_1d(plan, A.ops + item_of(t_it) * A.words * 32, plan_bytes, &bars[0]);
   uint32_t phase = 0;
   int buf = 0;
 
-  for (; item < A.n_items; item += nwarps) {
+  for (; t_it < n_items; t_it += nwarps) {
+    const long long item = item_of(t_it);
     // ------------------------------------------------------------------ load (warp-uniform)
     const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
     const cp_inst_v1* I = A.inst + ii;
@@ -107,8 +125,9 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
     // this item's rows were prefetched into plan[buf]: wait, then prefetch the next item's
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
     phase ^= 1u << buf;
-    if (lane == 0 && item + nwarps < A.n_items)
-      tma_load_1d(plan + (buf ^ 1) * PWr * 32, A.ops + (item + nwarps) * A.words * 32, plan_bytes, &bars[buf ^ 1]);
+    if (lane == 0 && t_it + nwarps < n_items)
+      tma_load_1d(plan + (buf ^ 1) * PWr * 32, A.ops + item_of(t_it + nwarps) * A.words * 32, plan_bytes,
+                  &bars[buf ^ 1]);
     buf ^= 1;
     if (st0) {
       if (lane == 0) {
@@ -140,11 +159,11 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         const int n = mn(16, plen - 16 * k);
         const uint32_t valid = (n == 16 ? 0xffffffffu : ((1u << (2 * n)) - 1u)) & 0x55555555u;
         const uint32_t lo = w & 0x55555555u, hi = (w >> 1) & 0x55555555u;
-        cF += __popc(~lo & ~hi & valid);
         cB += __popc(lo & ~hi & valid);
         cD += __popc(~lo & hi & valid);
         cW += __popc(lo & hi & valid);
       }
+      cF = plen - cB - cD - cW;
       bad_static = cF != m || cB + cD != m || (cB > 0 && cD + cW > 0) || cW != nsub * cD;
     }
     if (__any_sync(FULLM, bad_static)) {
@@ -192,6 +211,7 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         const int nl = mx(end, isF ? linkF : linkB) + (isF ? bwF : bwB);   // FIFO link clock (App. X1)
         const bool send = go & (isF ? sendF : (isDB & sendD));
         smem[send ? (isF ? hF + 1 : hD - 1) : iDum] = nl + (isF ? latF : latB);
+        if (kTL && go) A.t_start[(item * 32 + s) * (long long)A.len_stride + pos] = start;
         const int gi = go ? 1 : 0, gFi = (go & isF) ? 1 : 0, gDi = (go & isDB) ? 1 : 0;
         clk = madd(gi, end - clk, clk);
         mem = madd(gi, dm, mem);
@@ -229,40 +249,57 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
       if (last && s < 31)                           // its D ring may hold a larger item's arrivals
         for (int k = 0; k < R; ++k) smem[iD + (k << 5)] = 0;
       {                                             // every lane: idle lanes get safe entries
-        tabA[0 * 32] = make_int4(tf, mf, bwF, latF);
-        tabA[1 * 32] = make_int4(tB, mB, bwB, latB);
-        tabA[2 * 32] = make_int4(td, md, bwB, latB);
-        tabA[3 * 32] = make_int4(tw, mw, 0, 0);
-        // shared-window byte addresses: {input ring column, slot mask on counts * 32, send offset,
-        // the FIFO clock of the link the entry's message takes (F: to s+1, D/B: to s-1)}
-        const unsigned sb = (unsigned)__cvta_generic_to_shared(smem);
-        const int lkF = (int)(sb + 4u * (wbase + zero_row + 36 + lane)), lkB = lkF + 128;
-        tabB[0 * 32] = make_int4((int)(sb + 4u * iF), Rm << 5, sendF ? 4 : 0, lkF);
-        tabB[1 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, lkB);
-        tabB[2 * 32] = make_int4((int)(sb + 4u * iD), Rm << 5, sendD ? -4 : 0, lkB);
-        tabB[3 * 32] = make_int4((int)(sb + 4u * (wbase + zero_row + lane)), 0, 0, lkF);
-        smem[wbase + zero_row + 36 + lane] = 0;            // both link clocks start at 0
-        smem[wbase + zero_row + 68 + lane] = 0;
-        // per code: the increments of the packed (nF | nD << 16) counters and of the W count
-        int2* const tabC = reinterpret_cast<int2*>(smem + wbase + zero_row + 100) + lane;
-        tabC[0 * 32] = make_int2(32, 0);
-        tabC[1 * 32] = make_int2(32 << 16, 0);
-        tabC[2 * 32] = make_int2(32 << 16, 0);
-        tabC[3 * 32] = make_int2(0, 32);
+        // per lane and entry code: {duration, memory delta, link bandwidth, latency of its message};
+        // latency -1 marks an entry that sends nothing (W; F on the last stage; D/B on stage 0)
+        tabA[0 * 32] = make_int4(tf, mf, bwF, sendF ? latF : -1);
+        tabA[1 * 32] = make_int4(tB, mB, bwB, sendD ? latB : -1);
+        tabA[2 * 32] = make_int4(td, md, bwB, sendD ? latB : -1);
+        tabA[3 * 32] = make_int4(tw, mw, 0, -1);
+        // per entry code, the same for every lane (a broadcast read: one smem wavefront), byte offsets
+        // from the lane's own F ring column / F link clock: {input ring, slot mask on counts * 32,
+        // send offset (the consumer's column: +1 lane for F, -1 for D/B), link clock (F: to s+1, D/B:
+        // to s-1)}; then {increment of the packed (nF | nD << 16) counters, of the W count}
+        if (lane < 4) {
+          const int c = lane;
+          const int ring = c == CP_OP_F ? 0 : (c == CP_OP_W ? 4 * (Ly.zero - Ly.rings) : 4 * RW);
+          U[c] = make_int4(ring, c == CP_OP_W ? 0 : Rm << 5, c == CP_OP_F ? 4 : (c == CP_OP_W ? 0 : -4),
+                           (c == CP_OP_F || c == CP_OP_W) ? 0 : 128);
+          U[4 + c] = make_int4(c == CP_OP_F ? 32 : (c == CP_OP_W ? 0 : 32 << 16), c == CP_OP_W ? 32 : 0, 0, 0);
+        }
+        smem[wbase + Ly.link + lane] = 0;                  // both link clocks start at 0
+        smem[wbase + Ly.link + 32 + lane] = 0;
+        // entries past the row's end read as D, which is never ready once the row is done (its D count
+        // is m, and no neighbour's D count -- nor, on the last stage, its own F count -- exceeds m), so
+        // the round needs no position test; the rest of the staged row and the spare row are
+        // overwritten (they are not part of the plan)
+        for (int k = plen >> 4; k <= PW; ++k) {
+          const int sh = 2 * (plen - 16 * k);
+          const uint32_t pad = sh <= 0 ? 0xffffffffu : (0xffffffffu << sh);   // bits of entries >= plen
+          smem[iP + (k << 5)] = (int)(((uint32_t)smem[iP + (k << 5)] & ~pad) | (0xaaaaaaaau & pad));
+        }
       }
       __syncwarp();
       clk = tag;
       // Counters are kept scaled by 32 (one ring slot = 32 words) and the plan position doubled,
       // so that every address is one LEA off a shared-window base: the entry code comes from one
-      // funnel shift of the staged word, the table row is tab + code * 512 B, the ring slot is
-      // column + ((count & mask) << 2).  (A row holds at most 1024 >= 2m entries, so 32 * m <= 16384
-      // fits the 16-bit halves of the neighbour shuffle.)
+      // funnel shift of the staged word, the lane's cost row is tabA + code * 512 B, the code's
+      // uniform row U + code * 16 B, the ring slot column + ((count & mask) << 2).  (A row holds at
+      // most 1024 >= 2m entries, so 32 * m <= 16384 fits the 16-bit halves of the neighbour shuffle.)
+      // Shared-memory wavefronts, not instructions, bound this loop (ncu: the LSU data pipe at 95% of
+      // peak with per-lane address tables): per round one 4-wavefront cost row, two 1-wavefront
+      // broadcast rows, three scalar loads, two predicated stores and the two shuffles.
       const unsigned sb = (unsigned)__cvta_generic_to_shared(smem);
-      const unsigned tab0 = sb + 4u * (unsigned)(wbase + 4 * lane);        // tabA[0][lane]; tabB at +2048 B
+      const unsigned tab0 = sb + 4u * (unsigned)(tbase + 4 * lane);        // tabA[0][lane]
+      const unsigned ub = sb + 4u * (unsigned)Ly.uni;                      // U[0] (block header)
+      unsigned colF = sb + 4u * (unsigned)iF;                              // own F ring column
+      asm volatile("mov.b32 %0, %0;" : "+r"(colF));
+      const unsigned lkF = sb + 4u * (unsigned)(wbase + Ly.link + lane);   // own F link clock
       const unsigned iPb = sb + 4u * (unsigned)iP;
-      const int R32 = R << 5, plen2 = 2 * plen;
-      const unsigned tc0 = sb + 4u * (unsigned)(wbase + zero_row + 100 + 2 * lane);   // tabC[0][lane]
+      const int R32 = R << 5;
+      const unsigned stg = sb + 4u * (unsigned)(wbase + Ly.stage + lane);  // timeline staging [16][32]
+      int32_t* const trow = kTL ? A.t_start + (item * 32 + s) * (long long)A.len_stride : nullptr;
       int pos2 = 0, me = 0;                         // me: nF | nD << 16 (both scaled by 32)
+      int rr = 0, fg = 0;                           // timeline: round counter, next group to write
       for (;;) {
         const int cu = __shfl_up_sync(FULLM, me, 1);
         const int cd = __shfl_down_sync(FULLM, me, 1);
@@ -275,40 +312,55 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         unsigned code;
         asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(code) : "r"(wv), "r"(pos2));
         code &= 3u;
-        asm("mov.b32 %0, %0;" : "+r"(code));        // materialized once: LEA for the table row
-        const unsigned ta_addr = tab0 + (code << 9);
+        asm("mov.b32 %0, %0;" : "+r"(code));        // materialized once: LEA for the table rows
+        const unsigned ta_addr = tab0 + (code << 9), u_addr = ub + (code << 4);
+        int4 ta, tu;
         int2 tc;                                    // counter increments (off the critical path)
-        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(tc.x), "=r"(tc.y) : "r"(tc0 + (code << 8)));
-        int4 ta, tb;
         asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(ta.x), "=r"(ta.y), "=r"(ta.z), "=r"(ta.w) : "r"(ta_addr));
-        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+2048];"
-                     : "=r"(tb.x), "=r"(tb.y), "=r"(tb.z), "=r"(tb.w) : "r"(ta_addr));
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(tu.x), "=r"(tu.y), "=r"(tu.z), "=r"(tu.w) : "r"(u_addr));
+        // one broadcast word (one wavefront) for the packed counter increment; the W count's
+        // increment is a select
+        asm volatile("ld.shared.b32 %0, [%1+64];" : "=r"(tc.x) : "r"(u_addr));
         const bool isF = code == CP_OP_F, isW = code == CP_OP_W;
-        const bool isDB = !isF & !isW;
+        tc.y = isW ? 32 : 0;
         // readiness of the entry's own stream only: the producer count X and consumer count Y of F
         // (left, right) or D (right, left) are selected first, then one test
         const int n = isF ? nF : nD;
         const int X = isF ? leftF : rightD, Y = isF ? rightF : leftD;
-        const bool go = (pos2 < plen2) & (isW ? (went < nD) : ((X > n) & (n - Y < R32)));
-        const unsigned raddr = (unsigned)tb.x + ((unsigned)(n & tb.y) << 2);
+        const bool go = isW ? (went < nD) : ((X > n) & (n - Y < R32));
+        const unsigned raddr = colF + (unsigned)tu.x + ((unsigned)(n & tu.y) << 2);
+        const unsigned laddr = lkF + (unsigned)tu.w;
         int arr, lk;
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"(raddr));
-        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lk) : "r"(tb.w));     // the link's FIFO clock
+        asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lk) : "r"(laddr));     // the link's FIFO clock
         const int start = mx(clk, arr);
         const int end = start + ta.x;
         const int nl = mx(end, lk) + ta.z;                   // FIFO link clock (App. X1)
-        if (go && tb.z != 0) {
-          asm volatile("st.shared.b32 [%0], %1;" :: "r"(raddr + tb.z), "r"(nl + ta.w) : "memory");
-          asm volatile("st.shared.b32 [%0], %1;" :: "r"(tb.w), "r"(nl) : "memory");
+        if (go && ta.w >= 0) {
+          asm volatile("st.shared.b32 [%0], %1;" :: "r"(raddr + tu.z), "r"(nl + ta.w) : "memory");
+          asm volatile("st.shared.b32 [%0], %1;" :: "r"(laddr), "r"(nl) : "memory");
         }
         const int gi = go ? 1 : 0;
+        if (kTL)   // start tick of entry pos into staging slot pos & 15 (predicated, no branch)
+          asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}"
+                       :: "r"(stg + (((unsigned)pos2 & 30u) << 6)), "r"(start), "r"(gi) : "memory");
         clk = madd(gi, end - clk, clk);
         mem = madd(gi, ta.y, mem);
         peak = mx(peak, mem);
         pos2 = madd(gi, 2, pos2);
         me = madd(gi, tc.x, me);                    // the entry's counter(s), from the table
         went = madd(gi, tc.y, went);
+        if (kTL && (++rr & 7) == 0) {               // warp-uniform: every 8th round
+          // a lane advances <= 8 entries in 8 rounds, so at most one aligned group of 8 has completed
+          // since the last flush, and the 16-slot staging ring still holds it: two 16-B stores, one
+          // full 32-B sector of the lane's timeline row
+          if ((pos2 >> 4) > fg) {
+            tl_flush8(stg + ((unsigned)(fg & 1) << 10), trow + 8 * fg);
+            ++fg;
+          }
+        }
         unsigned wa;                                // iPb + 4 * (pos2 & ~31): one LOP3 + one IMAD
         asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(wa) : "r"((unsigned)pos2 & ~31u), "r"(iPb));
         asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(wa));
@@ -316,6 +368,8 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
         if (!__any_sync(FULLM, go)) break;
       }
       nF = (me & 0xffff) >> 5; nD = (me >> 16) >> 5; went >>= 5; pos = pos2 >> 1;
+      if (kTL)                                      // entries not yet written (< 16)
+        for (int k = 8 * fg; k < pos; ++k) trow[k] = smem[wbase + Ly.stage + ((k & 15) << 5) + lane];
     } else {
       rounds(std::false_type{});
     }
@@ -341,7 +395,7 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
       }
       int st;
       if (__any_sync(FULLM, badc)) st = CPI_BAD_PLAN;
-      else if (!complete && __any_sync(FULLM, ring_full)) st = -1;
+      else if (!complete && !A.from_list && __any_sync(FULLM, ring_full)) st = -1;
       else if (!complete) st = CPI_DEADLOCK;
       else st = __any_sync(FULLM, s < p && peak > mlim) ? CPI_MEM_EXCEEDED : 0;
       if (st == -1) {                            // ring capacity reached: hand to the fix-up pass
@@ -381,8 +435,8 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
   }
 }
 
-int launch_sim32(const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  const void* fn = (const void*)k_sim32;
+int launch_sim32(bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream) {
+  const void* fn = timeline ? (const void*)k_sim32<true> : (const void*)k_sim32<false>;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
@@ -391,8 +445,8 @@ int launch_sim32(const Args& a, int blocks, int threads, size_t smem, void* stre
   return (int)cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
 }
 
-int sim32_blocks_per_sm(int threads, size_t smem) {
-  const void* fn = (const void*)k_sim32;
+int sim32_blocks_per_sm(bool timeline, int threads, size_t smem) {
+  const void* fn = timeline ? (const void*)k_sim32<true> : (const void*)k_sim32<false>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;
