@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """cp_exact_bnb on the GPU vs the oracle's branch and bound: the 16-point 4 x 8 E1 grid (config 1)
-in one batch, then harder uniform instances (4 x 12, 6 x 8, 4 x 16).  Writes profiles/bnb_gpu_r02.json."""
+in one batch, then harder uniform instances (4 x 12, 6 x 8, 4 x 16, 8 x 8).
+usage: python tools/bnb_gpu.py [out.json]   (default profiles/bnb_gpu_r02.json)"""
 import json
 import os
 import sys
@@ -47,8 +48,9 @@ def main():
             {"lat_ratio": a, "bw_ratio": b, "makespan": int(r["makespan"][i]), "bound": int(r["bound"][i]),
              "status": int(r["status"][i]), "greedy": up[i], "nodes": int(r["nodes"][i])} for i, (a, b) in enumerate(sel)]}
         print(p, m, dt, out[f"uniform_{p}x{m}"]["points"], flush=True)
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    with open(os.path.join(ROOT, "profiles", "bnb_gpu_r02.json"), "w") as f:
+    path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "bnb_gpu_r02.json")
+    os.makedirs(os.path.dirname(path) or ".", exist_ok=True)
+    with open(path, "w") as f:
         json.dump(out, f, indent=1)
 
 

@@ -10,7 +10,7 @@ import numpy as np, torch
 import paper_2507_00217_b200 as cp
 from workloads import configs as K
 
-out = sys.argv[1] if len(sys.argv) > 1 else "profiles/e1_delay_sensitivity_r01.json"
+out = sys.argv[1] if len(sys.argv) > 1 else "profiles/e1_delay_sensitivity_r02.json"
 grid = K.e1_grid()
 keys, cm = cp.sweep_shard(grid, cand=True)
 torch.cuda.synchronize()
@@ -113,7 +113,10 @@ for k in rng.choice(grid.n_points, 24, replace=False):
     checked += 1
 doc = {"workload": "E1: p=4, 2 DCs (2+2), m=8, F=D=W=T_F=38000 ticks, M_L = 1F1B budget, zero DP",
        "axes": {"T_lat/T_F": ratios, "T_bw/T_F": ratios}, "candidates": names + ["IV1F1B (Loop)", "ZBV (Wave)"],
-       "slowdown_vs_zbv_zero_delay": table, "summary": summary, "oracle_spot_checked_points": checked}
+       "slowdown_vs_zbv_zero_delay": table, "summary": summary, "oracle_spot_checked_points": checked,
+       "zbv_note": "ZBV = reading Q35's stand-in: unit-time list schedule of the Wave data flow with ZB-V's "
+                   "published properties (zero bubble at zero delay, 2p chunk activations), not Qi et al.'s exact "
+                   "block order; every slowdown here is normalised to it and its delayed column inherits that choice"}
 os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
 with open(out, "w") as f:
     json.dump(doc, f)

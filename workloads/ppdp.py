@@ -58,6 +58,12 @@ def dp_cost_s(alpha_s: float, bw_bytes_s: float, c=LLAMA3_405B) -> float:
     return 2.0 * alpha_s + 2.0 * c["n_params"] * (2.0 / bw_bytes_s)
 
 
+def dp_cost_literal_s(alpha_s: float, bw_bytes_s: float, c=LLAMA3_405B) -> float:
+    """App. E :858 read literally: 2 x (alpha + 2 x N/2 x beta) with beta the time of ONE byte -- each of
+    the two rounds moves N/2 parameters of 2 bytes, 2N bytes in total (half of Q36's 4N)."""
+    return 2.0 * alpha_s + 2.0 * c["n_params"] / bw_bytes_s
+
+
 def ticks(seconds: float, tick_s: float = TICK_S) -> int:
     return int(seconds / tick_s + 0.5)
 
