@@ -396,7 +396,32 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(a.ovf_count, 0, sizeof(int32_t), st) != cudaSuccess) return CP_ECUDA;
   const int sms = cpk::device_sm_count();
-  for (int pass = 0; pass < 2; ++pass) {
+  int first_pass = 0;
+#ifndef CP_DEBUG
+  // First pass on k_chunk32f (chunk_fast.cu) for stage_stride-32 plans that fit shared memory: it
+  // finishes every n_sub = 1, n_mb <= 127 item that does not stall on its small rings and lists the
+  // rest; k_chunk32 then evaluates the listed items exactly (pass 1 below).
+  if (sc->stage_stride == 32 && sc->words <= kPlanCapWords && !getenv_nofast() && !std::getenv("CP_CHUNKF_OFF")) {
+    const bool loop = sc->pattern == CP_PATTERN_LOOP, tl = res->t_start != nullptr;
+    a.from_list = 0;
+    a.ring_slots = std::max(2, std::min(64, fast_ring_slots(in)));   // W readiness needs R >= 2; R << 24 fits
+    a.plan_words = sc->words;
+    a.shared_tab = (!sc->inst_of && in->n == 1) ? 1 : 0;
+    const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0);
+    const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;
+    const size_t smem = ((size_t)L.hdr + (size_t)wpb * L.per_warp) * 4;
+    if (smem <= kMaxSmemPerBlock) {
+      int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(loop, threads, smem), wpb);
+      if (const char* v = std::getenv("CP_CHUNKF_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
+      const long long need = (n + wpb - 1) / wpb;
+      const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
+      if (cpk::launch_chunkf(loop, tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      first_pass = 1;
+    }
+    a.shared_tab = 0;
+  }
+#endif
+  for (int pass = first_pass; pass < 2; ++pass) {
     a.from_list = pass;
     a.ring_slots = pass == 0 ? fast_ring_slots(in) : 1 << lg2_ceil(in->max_mb);
     a.plan_words = sc->words + 1;                       // one spare row: finished lanes read past their row
