@@ -394,7 +394,7 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
   a.ovf_count = reinterpret_cast<int32_t*>(base);
   a.ovf_list = reinterpret_cast<int32_t*>(base + kCtrlBytes);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(a.ovf_count, 0, sizeof(int32_t), st) != cudaSuccess) return CP_ECUDA;
+  if (cudaMemsetAsync(a.ovf_count, 0, kCtrlBytes, st) != cudaSuccess) return CP_ECUDA;
   const int sms = cpk::device_sm_count();
   int first_pass = 0;
 #ifndef CP_DEBUG
@@ -415,7 +415,10 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
       if (const char* v = std::getenv("CP_CHUNKF_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
       const long long need = (n + wpb - 1) / wpb;
       const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
+      // dynamic item counter in the workspace control block (zeroed with the overflow count above)
+      a.work_counter = std::getenv("CP_CHUNKF_STATIC") ? nullptr : reinterpret_cast<int32_t*>(base + 128);
       if (cpk::launch_chunkf(loop, tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      a.work_counter = nullptr;
       first_pass = 1;
     }
     a.shared_tab = 0;

@@ -99,8 +99,9 @@ __device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLay
   T1[192] = T1[160];
   T0[224] = make_int4(tw, mw, 0, -1);
   T1[224] = make_int4(z, z, lkR, 0);
-  // W-deficit increments (the byte of chunk c holds 128 - (#D - #W)): D -1, W +1, F / B 0
-  if (s < 8) U[4 * s] = s == 2 ? -1 : s == 3 ? 1 : s == 6 ? -256 : s == 7 ? 256 : 0;
+  // W-deficit increments (the byte of chunk c holds 128 - (#D - #W)): D -1, W +1
+  // and B +1 << 16 (byte 2 counts B blocks: the mixing rule)
+  if (s < 8) U[4 * s] = s == 2 ? -1 : s == 3 ? 1 : s == 6 ? -256 : s == 7 ? 256 : (s & 3) == 1 ? 1 << 16 : 0;
 }
 }  // namespace
 
@@ -136,7 +137,17 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
   const uint32_t opq = (uint32_t)A.words >> 30;
   const uint32_t fifteen = 15u | (opq << 20);       // (bits >= 16 of a PRMT selector are ignored)
 
-  for (long long item = gwarp; item < A.n_items; item += nwarps) {
+  // items are handed out by a counter (A.work_counter), the next index fetched one item ahead; without
+  // a counter, warp w takes items w, w + warps, ...
+  const bool dyn = A.work_counter != nullptr;
+  long long item = gwarp, nxt = 0;
+  if (dyn) {
+    int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(A.work_counter, 1);
+    item = __shfl_sync(FMASK, t0, 0);
+  }
+  for (; item < A.n_items; item = dyn ? (long long)__shfl_sync(FMASK, (int)nxt, 0) : item + nwarps) {
+    if (dyn && lane == 0) nxt = atomicAdd(A.work_counter, 1);
     // the previous item's generic-proxy writes to the plan rows are ordered before the bulk copy
     if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (lane == 0) tma_load_1d(plan, A.ops + item * PW * 32, (uint32_t)PW * 128u, bar);
@@ -167,33 +178,19 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
     ok = __all_sync(FMASK, ok) && u < (long long)CINF;
     mbar_wait(bar, phase);
     phase ^= 1u;
-    // stage the row: Q29's count and mixing rules per chunk and codes < 8 (nibble popcounts), pad
-    // past the end with D0, pre-rotate by one entry
+    // stage the row: codes < 8, pad past the end with D0, pre-rotate by one entry.  Q29's count and
+    // mixing rules are checked on the final counts of a completed row (below); the W-prefix rule is
+    // dynamic (a W ahead of its D never becomes ready).  No count can wrap its byte: an entry runs
+    // only while its own count is below its producer's (<= 255), and a W only while a D is owed.
     if (ok) {
       bool bplan = false;
-      int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int k = 0; k <= PW; ++k) {
         uint32_t w = (uint32_t)plan[(k << 5) + lane];
         const int n = s < p ? min(max(plen - 8 * k, 0), 8) : 0;
-        const uint32_t vm = (n == 8 ? 0xffffffffu : ((1u << (4 * n)) - 1u)) & 0x11111111u;
-        if (n > 0) {
-          if ((w >> 3) & vm) bplan = true;
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            const uint32_t t = w ^ (0x11111111u * (uint32_t)v);
-            cnt[v] += __popc(~(t | (t >> 1) | (t >> 2) | (t >> 3)) & vm);
-          }
-        }
-        const uint32_t keep = vm * 15u;
+        const uint32_t keep = n == 8 ? 0xffffffffu : ((1u << (4 * n)) - 1u);
+        bplan |= ((w & keep & 0x88888888u) != 0u);
         w = (w & keep) | (0x22222222u & ~keep);
         plan[(k << 5) + lane] = (int32_t)((w << 4) | (w >> 28));
-      }
-      if (s < p) {
-        for (int ch = 0; ch < 2; ++ch)
-          if (cnt[4 * ch + CP_OP_F] != m || cnt[4 * ch + CP_OP_B] + cnt[4 * ch + CP_OP_D] != m ||
-              cnt[4 * ch + CP_OP_W] != cnt[4 * ch + CP_OP_D])
-            bplan = true;
-        if (cnt[CP_OP_B] + cnt[4 + CP_OP_B] > 0 && cnt[CP_OP_D] + cnt[4 + CP_OP_D] > 0) bplan = true;
       }
       ok = !__any_sync(FMASK, bplan);
     }
@@ -301,8 +298,13 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
       if (!__any_sync(FMASK, go)) break;
     }
     const int pos = pos4 >> 2;
-    const bool complete = !__any_sync(FMASK, s < p && pos < plen);
-    if (!complete) {                                // stalled: the exact pass classifies it
+    // completed, with Q29's counts: F, D + B of each chunk m (c), as many W as D per chunk (deficit
+    // bytes back at 128), B and D not mixed on a stage (#B, byte 2 of w, is 0 or 2m)
+    const uint32_t bcnt = (w >> 16) & 0xffu;
+    const bool rowok = s >= p || (pos == plen && c == 0x01010101u * (uint32_t)(128 + m) && (w & 0xffffu) == 0x8080u &&
+                                  (bcnt == 0u || bcnt == (uint32_t)(2 * m)));
+    const bool complete = __all_sync(FMASK, rowok);
+    if (!complete) {                                // stalled or invalid: the exact pass classifies it
       if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
       __syncwarp();
       continue;

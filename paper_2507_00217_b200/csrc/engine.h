@@ -55,6 +55,7 @@ struct Args {
   int32_t own_lo, own_hi;
   int32_t chunk_pattern;               // two-chunk plans: CP_PATTERN_WAVE or CP_PATTERN_LOOP
   int32_t shared_tab;                  // k_sim32: one cost / increment table per block (all items use instance 0)
+  int32_t* work_counter;               // k_chunk32f: dynamic item counter (workspace; nullptr: static)
   cp_grid grid;
 };
 
