@@ -140,7 +140,7 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
   a.ovf_list = reinterpret_cast<int32_t*>(base + kCtrlBytes);
   int32_t* rings = reinterpret_cast<int32_t*>(base + kCtrlBytes + align256(sizeof(int32_t) * (size_t)std::max(1LL, n)));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (cudaMemsetAsync(a.ovf_count, 0, sizeof(int32_t), st) != cudaSuccess) return CP_ECUDA;
+  if (cudaMemsetAsync(a.ovf_count, 0, kCtrlBytes, st) != cudaSuccess) return CP_ECUDA;
 
   const int nseg = 32 >> a.seg_lg;
   a.plan_words = sc->words <= kPlanCapWords ? sc->words : 0;
@@ -154,18 +154,39 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
     // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row.  When every
     // item uses instance 0, a 4-warp block shares one cost / increment table (24 resident warps).
     const bool tl = res->t_start != nullptr;
+    // Without a timeline the first pass is k_chunk32f (chunk_fast.cu, byte-count readiness, dynamic item
+    // counter); with one, k_sim32 (its start ticks are staged in shared memory and written 32 B per lane).
+    // Either lists the items it does not finish for the exact second pass below.
+    bool first_done = false;
+    if (!tl && !std::getenv("CP_CHUNKF_OFF")) {
+      a.ring_slots = std::max(2, fast_ring_slots(in));   // W readiness needs R >= 2
+      a.shared_tab = (!sc->inst_of && in->n == 1) ? 1 : 0;
+      const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0, 2);
+      const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;
+      const size_t smem = ((size_t)L.hdr + (size_t)wpb * L.per_warp) * 4;
+      if (smem <= kMaxSmemPerBlock) {
+        int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(CP_PATTERN_UD, threads, smem), wpb);
+        if (const char* v = std::getenv("CP_CHUNKF_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
+        const long long need = (n + wpb - 1) / wpb;
+        const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
+        a.work_counter = std::getenv("CP_CHUNKF_STATIC") ? nullptr : reinterpret_cast<int32_t*>(base + 128);
+        if (cpk::launch_chunkf(CP_PATTERN_UD, false, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+        a.work_counter = nullptr;
+        first_done = true;
+      }
+    }
     a.ring_slots = fast_ring_slots(in);
     a.shared_tab = (!sc->inst_of && in->n == 1 && !std::getenv("CP_SIM32_NOSHARE")) ? 1 : 0;
     const cpk::Sim32Layout L1 = cpk::sim32_layout(a.ring_slots, a.plan_words, a.shared_tab != 0, tl);
     a.smem_words_per_warp = L1.per_warp;
     const int wpb = a.shared_tab ? 4 : 2, threads = 32 * wpb;
     const size_t smem = ((size_t)L1.hdr + (size_t)wpb * L1.per_warp) * 4;
-    if (smem <= kMaxSmemPerBlock) {
+    if (first_done || smem <= kMaxSmemPerBlock) {
       int bps = smsp_balanced(cpk::sim32_blocks_per_sm(tl, threads, smem), wpb);
       if (const char* v = std::getenv("CP_SIM32_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
       const long long need = (n + wpb - 1) / wpb;
       const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
-      if (cpk::launch_sim32(tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      if (!first_done && cpk::launch_sim32(tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
       // Items that stalled on a full 8-slot ring (cyclic backpressure) are re-run from the
       // overflow list by the same kernel with rings of R > n_mb slots, where no ring can fill (every
       // producer -> consumer lead is <= n_mb); only when such rings exceed shared memory does the
@@ -402,22 +423,22 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
   // finishes every n_sub = 1, n_mb <= 127 item that does not stall on its small rings and lists the
   // rest; k_chunk32 then evaluates the listed items exactly (pass 1 below).
   if (sc->stage_stride == 32 && sc->words <= kPlanCapWords && !getenv_nofast() && !std::getenv("CP_CHUNKF_OFF")) {
-    const bool loop = sc->pattern == CP_PATTERN_LOOP, tl = res->t_start != nullptr;
+    const bool tl = res->t_start != nullptr;
     a.from_list = 0;
     a.ring_slots = std::max(2, std::min(64, fast_ring_slots(in)));   // W readiness needs R >= 2; R << 24 fits
     a.plan_words = sc->words;
     a.shared_tab = (!sc->inst_of && in->n == 1) ? 1 : 0;
-    const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0);
+    const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0, 4);
     const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;
     const size_t smem = ((size_t)L.hdr + (size_t)wpb * L.per_warp) * 4;
     if (smem <= kMaxSmemPerBlock) {
-      int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(loop, threads, smem), wpb);
+      int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(sc->pattern, threads, smem), wpb);
       if (const char* v = std::getenv("CP_CHUNKF_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
       const long long need = (n + wpb - 1) / wpb;
       const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));
       // dynamic item counter in the workspace control block (zeroed with the overflow count above)
       a.work_counter = std::getenv("CP_CHUNKF_STATIC") ? nullptr : reinterpret_cast<int32_t*>(base + 128);
-      if (cpk::launch_chunkf(loop, tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      if (cpk::launch_chunkf(sc->pattern, tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
       a.work_counter = nullptr;
       first_pass = 1;
     }

@@ -1,11 +1,12 @@
-// chunk_fast.cu -- first pass of cp_simulate for two-chunk plans (Wave, reading Q32; Loop, Q33):
-// one item per warp, lane = stage, round-synchronous like k_sim32.  Items it does not finish (a
-// stall, which may be an artefact of its 8-slot rings, n_sub > 1, n_mb > 127, anything invalid) go to
-// the overflow list and are evaluated exactly by k_chunk32 (wave32.cu) with rings of n_mb slots.
+// chunk_fast.cu -- first pass of cp_simulate for one-chunk UD plans (the config-4 bench shape) and
+// two-chunk plans (Wave, reading Q32; Loop, Q33): one item per warp, lane = stage, round-synchronous.
+// Items it does not finish (a stall, which may be an artefact of its 8-slot rings, n_sub > 1,
+// n_mb > 127, anything invalid) go to the overflow list and are evaluated exactly by the second pass
+// with rings of n_mb slots: k_sim32 (sim32.cu) for UD, k_chunk32 (wave32.cu) for Wave / Loop.
 //
 // What makes the round short:
-//  * Block counts are bytes.  c = {F0, F1, D0, D1} counts + 128 (so every byte has its top bit set),
-//    one register; one shuffle per direction hands a lane its neighbours' four counts.
+//  * Block counts are bytes.  c = {F0, F1, D0, D1} counts + 128 (UD: {F, D, -, -}; every byte has its
+//    top bit set), one register; one shuffle per direction hands a lane its neighbours' counts.
 //  * Readiness of the entry's own stream in three PRMTs and three compares: the producer count X,
 //    the consumer count Y and the own count n are byte-selected into the top byte (X from the left /
 //    right neighbour, or the own count at a turn-around / the loss, or 0xFF = "no producer" by sign
@@ -17,8 +18,9 @@
 //    shared by the block when every item uses one instance.
 //  * Ring slot = own count mod R, read from the top byte of n; a message goes to the consumer's ring
 //    at the same slot (producer count = consumer's index of that message).
-//  * Entries past a row's end read as D0, never ready once the row is done, so there is no position
-//    test; the plan word is pre-rotated by one entry so the decode is one funnel shift and one LOP3.
+//  * Entries past a row's end read as D (D0), never ready once the row is done, so there is no
+//    position test; the plan word is pre-rotated by 4 bits so the decode is one funnel shift and one
+//    LOP3 (UD codes are 2 bits, 16 per word; two-chunk entries 4 bits, 8 per word).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -53,8 +55,9 @@ __device__ __forceinline__ void pack_sel(const int (&ix)[8], uint32_t& lo, uint3
 
 // Per-lane table rows of instance I (entry x = type | chunk << 2).  T0/T1 point at [x = 0][lane],
 // rows 32 int4 apart; U at [0] (16-B rows).  Addresses are byte offsets from the warp region.
-template <bool kLoop>
+template <int kPat>   // CP_PATTERN_UD / _WAVE / _LOOP
 __device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLayout& Ly, int4* T0, int4* T1, int* U) {
+  constexpr bool kUD = kPat == CP_PATTERN_UD, kLoop = kPat == CP_PATTERN_LOOP;
   const int p = I->n_pp < 1 ? 1 : (I->n_pp > CP_MAX_STAGES ? CP_MAX_STAGES : I->n_pp);   // (other p: not run here)
   const bool live = s < p, first = s == 0, last = s == p - 1;
   int tf = 0, td = 0, tw = 0, mf = 0, md = 0, mw = 0, latR = 0, bwR = 0, latL = 0, bwL = 0;
@@ -70,6 +73,21 @@ __device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLay
   const int rF0 = Ly.rings * 4 + col, rF1 = rF0 + RB, rD0 = rF0 + 2 * RB, rD1 = rF0 + 3 * RB;
   const int z = Ly.zero * 4 + col, lkR = Ly.lk * 4 + col, lkL = lkR + 128;
   const auto L = [&](int lat) { return live ? lat : -1; };   // latency -1: the entry sends nothing
+  if (kUD) {
+    // rings F (0) and D (1); F goes right, D / B left; entry x = code, rows 4..7 repeat 0..3
+    for (int h = 0; h < 256; h += 128) {
+      T0[h] = make_int4(tf, mf, bwR, L(last ? -1 : latR));
+      T1[h] = make_int4(rF0, rF0 + 4, lkR, 1);
+      T0[h + 32] = make_int4(td + tw, md + mw, bwL, L(first ? -1 : latL));
+      T1[h + 32] = make_int4(rF1, rF1 - 4, lkL, 1 << 8);
+      T0[h + 64] = make_int4(td, md, bwL, L(first ? -1 : latL));
+      T1[h + 64] = T1[h + 32];
+      T0[h + 96] = make_int4(tw, mw, 0, -1);
+      T1[h + 96] = make_int4(z, z, lkR, 0);
+    }
+    if (s < 8) U[4 * s] = (s & 3) == 2 ? -1 : (s & 3) == 3 ? 1 : (s & 3) == 1 ? 1 << 16 : 0;
+    return;
+  }
   // chunk 0: F0 goes right (Loop: the last stage's F0 takes the wrap link into stage 0's F1 ring);
   // D0 / B0 go left (stage 0's have no consumer)
   T0[0] = make_int4(tf, mf, bwR, L(kLoop || !last ? latR : -1));
@@ -105,12 +123,16 @@ __device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLay
 }
 }  // namespace
 
-template <bool kLoop, bool kTL>   // kTL: per-entry start ticks requested (A.t_start)
+template <int kPat, bool kTL>   // kPat: CP_PATTERN_UD / _WAVE / _LOOP; kTL: per-entry start ticks (A.t_start)
 __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(const __grid_constant__ Args A) {
+  constexpr bool kUD = kPat == CP_PATTERN_UD, kLoop = kPat == CP_PATTERN_LOOP;
+  constexpr int kRings = kUD ? 2 : 4, kEPW = kUD ? 16 : 8, kStep = 32 / kEPW;   // entries per word, bits per entry
+  constexpr int kChunks = kUD ? 1 : 2;
+  constexpr uint32_t kPad = kUD ? 0xaaaaaaaau : 0x22222222u;   // D (UD) / D0 entries: never ready at the end
   extern __shared__ __align__(128) int32_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, s = lane;
   const int R = A.ring_slots, Rm = R - 1, PW = A.words;
-  const ChunkFLayout Ly = chunkf_layout(R, PW, A.shared_tab != 0);
+  const ChunkFLayout Ly = chunkf_layout(R, PW, A.shared_tab != 0, kRings);
   const int wbase = Ly.hdr + wib * Ly.per_warp;
   const int tbase = A.shared_tab ? 0 : wbase + Ly.tab;
   const unsigned sb = smem_u32(smem), wb = sb + 4u * (unsigned)wbase;
@@ -123,10 +145,10 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
 
   // zero block (zero rows + link clocks) and rings start at 0; the zero rows are never written
-  for (int k = lane; k < (Ly.zrows + 4 * R) * 32; k += 32) smem[wbase + Ly.zero + k] = 0;
+  for (int k = lane; k < (Ly.zrows + kRings * R) * 32; k += 32) smem[wbase + Ly.zero + k] = 0;
   if (lane == 0) mbar_init(bar);
   if (A.shared_tab) {                               // every item uses instance 0 (host guarantees)
-    if (wib == 0) chunkf_tables<kLoop>(A.inst, lane, R, Ly, T0, T1, U);
+    if (wib == 0) chunkf_tables<kPat>(A.inst, lane, R, Ly, T0, T1, U);
     __syncthreads();
   }
   __syncwarp();
@@ -170,9 +192,9 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
     if (ok && s < p)
       ok = tf >= 1 && td >= 1 && tw >= 1 && mf > 0 && md <= 0 && mw <= 0 && (long long)mf + md + mw == 0 &&
            mlim >= mf && tdp >= 0 && I->t_ag[s] >= 0 && latR >= 0 && bwR >= 0 && lat_b_s >= 0 && bw_b_s >= 0 &&
-           plen <= 8 * PW;
-    long long u = (s < p && ok) ? 2LL * m * ((long long)tf + td + tw) + tag + tdp +
-                                      2LL * m * ((long long)latR + bwR + latL + bwL)
+           plen <= kEPW * PW;
+    long long u = (s < p && ok) ? kChunks * (long long)m * ((long long)tf + td + tw) + tag + tdp +
+                                      kChunks * (long long)m * ((long long)latR + bwR + latL + bwL)
                                 : 0;
     for (int d = 16; d > 0; d >>= 1) u += __shfl_xor_sync(FMASK, u, d);
     ok = __all_sync(FMASK, ok) && u < (long long)CINF;
@@ -186,10 +208,10 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
       bool bplan = false;
       for (int k = 0; k <= PW; ++k) {
         uint32_t w = (uint32_t)plan[(k << 5) + lane];
-        const int n = s < p ? min(max(plen - 8 * k, 0), 8) : 0;
-        const uint32_t keep = n == 8 ? 0xffffffffu : ((1u << (4 * n)) - 1u);
-        bplan |= ((w & keep & 0x88888888u) != 0u);
-        w = (w & keep) | (0x22222222u & ~keep);
+        const int n = s < p ? min(max(plen - kEPW * k, 0), kEPW) : 0;
+        const uint32_t keep = n == kEPW ? 0xffffffffu : ((1u << (kStep * n)) - 1u);
+        if (!kUD) bplan |= ((w & keep & 0x88888888u) != 0u);
+        w = (w & keep) | (kPad & ~keep);
         plan[(k << 5) + lane] = (int32_t)((w << 4) | (w >> 28));
       }
       ok = !__any_sync(FMASK, bplan);
@@ -200,17 +222,19 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
       continue;
     }
     if (!A.shared_tab && ii != tab_inst) {
-      chunkf_tables<kLoop>(I, lane, R, Ly, T0, T1, U);
+      chunkf_tables<kPat>(I, lane, R, Ly, T0, T1, U);
       tab_inst = ii;
     }
     // ring columns read without a producer in this item but written by a larger previous one
-    // (Wave: the last stage's F1 / D0 inputs; Loop: the last stage's D1 input) must read 0
+    // (UD: the last stage's D input; Wave: the last stage's F1 / D0 inputs; Loop: its D1 input) must read 0
     if (p < 32)
       for (int k = lane; k < R; k += 32) {
         const int c0 = wbase + Ly.rings + (k << 5) + (p - 1);
-        smem[c0 + R * 32] = 0;                      // F1
-        smem[c0 + 2 * R * 32] = 0;                  // D0
-        smem[c0 + 3 * R * 32] = 0;                  // D1
+        smem[c0 + R * 32] = 0;                      // UD: D; F1
+        if (!kUD) {
+          smem[c0 + 2 * R * 32] = 0;                // D0
+          smem[c0 + 3 * R * 32] = 0;                // D1
+        }
       }
     smem[wbase + Ly.lk + lane] = 0;                 // both link clocks start at 0
     smem[wbase + Ly.lk + 32 + lane] = 0;
@@ -220,7 +244,11 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
     uint32_t kxl, kxh, kyl, kyh, knl, knh;
     {
       int ix[8], iy[8];
-      if (kLoop) {
+      if (kUD) {
+        const int tx[8] = {first ? 8 : 0, last ? 4 : 5, last ? 4 : 5, 8, first ? 8 : 0, last ? 4 : 5, last ? 4 : 5, 8};
+        const int ty[8] = {last ? 8 : 4, first ? 8 : 1, first ? 8 : 1, 8, last ? 8 : 4, first ? 8 : 1, first ? 8 : 1, 8};
+        for (int x = 0; x < 8; ++x) { ix[x] = tx[x]; iy[x] = ty[x]; }
+      } else if (kLoop) {
         const int tx[8] = {first ? 8 : 0, 6, 6, 8, first ? 0 : 1, 7, 7, 8};
         const int ty[8] = {last ? 5 : 4, first ? 8 : 2, first ? 8 : 2, 8, last ? 8 : 5, first ? 2 : 3, first ? 2 : 3, 8};
         for (int x = 0; x < 8; ++x) { ix[x] = tx[x]; iy[x] = ty[x]; }
@@ -229,7 +257,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
         const int ty[8] = {last ? 8 : 4, first ? 8 : 2, first ? 8 : 2, 8, first ? 8 : 1, last ? 8 : 7, last ? 8 : 7, 8};
         for (int x = 0; x < 8; ++x) { ix[x] = tx[x]; iy[x] = ty[x]; }
       }
-      const int tn[8] = {0, 2, 2, 12, 1, 3, 3, 13};
+      const int tn[8] = {0, kUD ? 1 : 2, kUD ? 1 : 2, 12, kUD ? 0 : 1, kUD ? 1 : 3, kUD ? 1 : 3, kUD ? 12 : 13};
       pack_sel(ix, kxl, kxh);
       pack_sel(iy, kyl, kyh);
       pack_sel(tn, knl, knh);
@@ -261,7 +289,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
       if (kLoop) Rv = prmt(Rv, c, fixR);
       uint32_t r, x4;
       asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(wv), "r"(pos4));
-      asm("lop3.b32 %0, %1, 0x70, %2, 0xEA;" : "=r"(x4) : "r"(r), "r"(fifteen));   // entry << 4 | 15
+      asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x4) : "r"(r), "n"(kUD ? 0x30 : 0x70), "r"(fifteen));   // entry << 4 | 15
       const unsigned ta = tab0m + (x4 << 5);
       int4 t0, t1;
       int iw;
@@ -283,26 +311,27 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
         asm volatile("st.shared.b32 [%0], %1;" :: "r"(oa), "r"(nl + t0.w) : "memory");
         asm volatile("st.shared.b32 [%0], %1;" :: "r"(la), "r"(nl) : "memory");
       }
-      if (kTL && go && (pos4 >> 2) < A.len_stride) trow[pos4 >> 2] = start;
+      if (kTL && go && pos4 / kStep < A.len_stride) trow[pos4 / kStep] = start;
       const int gi = go ? 1 : 0;
       clk = cmadd(gi, end - clk, clk);
       mem = cmadd(gi, t0.y, mem);
       peak = cmax(peak, mem);
       c = (uint32_t)cmadd(gi, t1.w, (int)c);
       w = (uint32_t)cmadd(gi, iw, (int)w);
-      pos4 = cmadd(gi, 4, pos4);
+      pos4 = cmadd(gi, kStep, pos4);
       unsigned wa;
       asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(wa) : "r"((unsigned)pos4 & ~31u), "r"(iPb));
       asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(wa));
       __syncwarp();
       if (!__any_sync(FMASK, go)) break;
     }
-    const int pos = pos4 >> 2;
+    const int pos = pos4 / kStep;
     // completed, with Q29's counts: F, D + B of each chunk m (c), as many W as D per chunk (deficit
-    // bytes back at 128), B and D not mixed on a stage (#B, byte 2 of w, is 0 or 2m)
+    // bytes back at 128), B and D not mixed on a stage (#B, byte 2 of w, is 0 or kChunks m)
     const uint32_t bcnt = (w >> 16) & 0xffu;
-    const bool rowok = s >= p || (pos == plen && c == 0x01010101u * (uint32_t)(128 + m) && (w & 0xffffu) == 0x8080u &&
-                                  (bcnt == 0u || bcnt == (uint32_t)(2 * m)));
+    const uint32_t cwant = kUD ? 0x80808080u + 0x0101u * (uint32_t)m : 0x01010101u * (uint32_t)(128 + m);
+    const bool rowok = s >= p || (pos == plen && c == cwant && (w & 0xffffu) == 0x8080u &&
+                                  (bcnt == 0u || bcnt == (uint32_t)(kChunks * m)));
     const bool complete = __all_sync(FMASK, rowok);
     if (!complete) {                                // stalled or invalid: the exact pass classifies it
       if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
@@ -323,7 +352,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
         atomicMin(A.best_key, ((unsigned long long)ms << 32) | (unsigned long long)(uint32_t)(item + A.index_base));
     }
     if (A.stage_stats) {
-      // busy = 2m (t_f + t_d + t_w); first[s] = max(t_ag[s], first[s-1] + t_f + bw + lat of s-1): the
+      // busy = chunks * m (t_f + t_d + t_w); first[s] = max(t_ag[s], first[s-1] + t_f + bw + lat of s-1): the
       // max-plus prefix P_s + max_{k<=s}(ag_k - P_k) along chunk 0's forward path (as k_chunk32)
       const int cfw = s < p ? tf + bwR + latR : 0;
       int Pp = cfw;
@@ -331,7 +360,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
       Pp -= cfw;
       int xq = (s < p ? tag : 0) - Pp;
       for (int d = 1; d < 32; d <<= 1) { const int t2 = __shfl_up_sync(FMASK, xq, d); if (s >= d) xq = cmax(xq, t2); }
-      const int busy = 2 * m * (tf + td + tw);
+      const int busy = kChunks * m * (tf + td + tw);
       for (int rr = s; rr < A.stage_stride; rr += 32) {
         const int4 v = (rr == s && s < p) ? make_int4(Pp + xq, clk, busy, peak) : make_int4(0, 0, 0, 0);
         *reinterpret_cast<int4*>(A.stage_stats + (item * A.stage_stride + rr) * 4) = v;
@@ -342,14 +371,17 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
 }
 
 namespace {
-const void* chunkf_fn(bool loop, bool tl) {
-  return loop ? (tl ? (const void*)k_chunk32f<true, true> : (const void*)k_chunk32f<true, false>)
-              : (tl ? (const void*)k_chunk32f<false, true> : (const void*)k_chunk32f<false, false>);
+const void* chunkf_fn(int pat, bool tl) {
+  switch (pat) {
+    case CP_PATTERN_UD: return tl ? (const void*)k_chunk32f<CP_PATTERN_UD, true> : (const void*)k_chunk32f<CP_PATTERN_UD, false>;
+    case CP_PATTERN_WAVE: return tl ? (const void*)k_chunk32f<CP_PATTERN_WAVE, true> : (const void*)k_chunk32f<CP_PATTERN_WAVE, false>;
+    default: return tl ? (const void*)k_chunk32f<CP_PATTERN_LOOP, true> : (const void*)k_chunk32f<CP_PATTERN_LOOP, false>;
+  }
 }
 }  // namespace
 
-int launch_chunkf(bool loop, bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  const void* fn = chunkf_fn(loop, timeline);
+int launch_chunkf(int pattern, bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream) {
+  const void* fn = chunkf_fn(pattern, timeline);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
@@ -358,8 +390,8 @@ int launch_chunkf(bool loop, bool timeline, const Args& a, int blocks, int threa
   return (int)cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
 }
 
-int chunkf_blocks_per_sm(bool loop, int threads, size_t smem) {
-  const void* fn = chunkf_fn(loop, false);
+int chunkf_blocks_per_sm(int pattern, int threads, size_t smem) {
+  const void* fn = chunkf_fn(pattern, false);
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;

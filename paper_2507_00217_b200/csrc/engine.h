@@ -149,14 +149,15 @@ __host__ __device__ inline Sim32Layout sim32_layout(int R, int plan_words, bool 
 // U [8] int4 {W-deficit increment, -, -, -}.  Per warp: an mbarrier row; a block of zrows rows whose rows
 // 0 and R-1 stay zero (the input of W entries, whose ring slot is 0 or R-1) and which holds the two
 // link-clock rows (rows 1 and 2 when R >= 4, else appended); the four arrival rings F0, F1, D0, D1
-// [R][32] each; the plan rows (words + 1, the last a padding row); the tables unless the block holds them.
+// [R][32] each (UD: F, D); the plan rows (words + 1, the last a padding row); the tables unless the block
+// holds them.
 constexpr int kChunkFTabWords = 2 * 8 * 32 * 4 + 8 * 4;
 constexpr int kChunkFThreads = 128;
 constexpr int kChunkFMinBlocks = 5;
 struct ChunkFLayout {
   int hdr, bars, zero, zrows, lk, rings, plan, tab, per_warp;
 };
-__host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool shared_tab) {
+__host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool shared_tab, int rings) {
   ChunkFLayout L;
   L.hdr = shared_tab ? kChunkFTabWords : 0;
   L.bars = 0;
@@ -164,14 +165,14 @@ __host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool sha
   L.zrows = R >= 4 ? R : R + 2;
   L.lk = R >= 4 ? L.zero + 32 : L.zero + R * 32;
   L.rings = L.zero + L.zrows * 32;
-  L.plan = L.rings + 4 * R * 32;
+  L.plan = L.rings + rings * R * 32;
   int w = L.plan + (words + 1) * 32;
   L.tab = shared_tab ? -1 : w;
   if (!shared_tab) w += kChunkFTabWords;
   L.per_warp = w;
   return L;
 }
-int launch_chunkf(bool loop, bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream);
-int chunkf_blocks_per_sm(bool loop, int threads, size_t smem);
+int launch_chunkf(int pattern, bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream);
+int chunkf_blocks_per_sm(int pattern, int threads, size_t smem);
 
 }  // namespace cpk
