@@ -79,7 +79,8 @@ def issue_roofline(evals_per_s, sm_hz):
     peak = 148 * 4 * sm_hz                       # warp-instructions/s: 148 SMs x 4 schedulers x SM clock
     ach = ipe * evals_per_s
     return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-instr/s", "frac": ach / peak,
-            "instructions_per_eval": ipe, "source": "ncu smsp__inst_executed.sum (profiles/ncu_sim32_v16_r01.txt)",
+            "instructions_per_eval": ipe,
+            "source": "ncu smsp__inst_executed.sum (" + str(traffic_per_launch("simulate_config4_source")) + ")",
             "sm_clock_hz": sm_hz}
 
 
@@ -551,7 +552,7 @@ def run_ours(args):
                                   ": 2e5 random valid plans/GPU of one p=32, 4-DC, m=32 instance (L=T_F, T_bw=T_F/2), "
                                   "makespan + peak memory + argmin",
                       "ms_per_launch": t, "status_ok": bool((wr["status"] == 0).all().item()),
-                      "roofline": alu_roofline(w_ops, t["median"], alu_peak, alu_src, "k_chunk32 (cp_simulate, two-chunk)")}
+                      "roofline": alu_roofline(w_ops, t["median"], alu_peak, alu_src, "k_chunk32f<Wave|Loop> (cp_simulate first pass, two-chunk)")}
             if want_cpu:
                 line_w["cpu_baseline"] = dict(oracle_rate(name, cores), unit="evals/s")
             if is_loop:
@@ -603,7 +604,8 @@ def run_ours(args):
             # from the median launch
             "roofline": {"bound": "alu", "achieved": alu_ach, "peak": alu_peak, "unit": "Tops/s",
                          "frac": alu_ach / alu_peak, "traffic": traffic_per_launch(),
-                         "peak_source": alu_src, "kernel": "k_sim32 (cp_simulate fast path)",
+                         "peak_source": alu_src,
+                         "kernel": traffic_per_launch("simulate_config4_kernel") or "cp_simulate first pass",
                          "kernel_ms": kern_ms, "kernel_ms_median": kern_med, "kernel_ms_best": kern_best,
                          "ops_per_eval": OPS_PER_EVAL, "evals_per_launch": n},
             # the integer-issue ceiling SURVEY.md §8(d) names: 4 warp-instructions per clock per SM; the

@@ -27,6 +27,18 @@
 #include "engine.h"
 #include "ptx.cuh"
 
+#ifndef CHUNKF_UD_LKREG
+// UD: the two FIFO link clocks in registers (one select, two predicated updates) instead of a
+// shared-memory load and store per round: measured +1.7% on config 4 (77.5 -> 78.8 M evals/s)
+#define CHUNKF_UD_LKREG 1
+#endif
+#ifndef CHUNKF_2C_LKREG
+#define CHUNKF_2C_LKREG 0   // the same for Wave / Loop (the link is the one the table's link address names)
+#endif
+#ifndef CHUNKF_UD_MINB
+#define CHUNKF_UD_MINB 6   // UD: 24 resident warps at <= 80 registers (measured +0.6% over 20 warps; 28, 32: no further gain)
+#endif
+
 namespace cpk {
 
 namespace {
@@ -74,18 +86,19 @@ __device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLay
   const int z = Ly.zero * 4 + col, lkR = Ly.lk * 4 + col, lkL = lkR + 128;
   const auto L = [&](int lat) { return live ? lat : -1; };   // latency -1: the entry sends nothing
   if (kUD) {
-    // rings F (0) and D (1); F goes right, D / B left; entry x = code, rows 4..7 repeat 0..3
+    // rings F (0) and D (1); F goes right, D / B left; entry x = code, rows 4..7 repeat 0..3.  One
+    // count register c = {F, D, W deficit, #B} (+128 each): F +1; B: D +1, #B +1; D: D +1, deficit -1;
+    // W: deficit +1
     for (int h = 0; h < 256; h += 128) {
       T0[h] = make_int4(tf, mf, bwR, L(last ? -1 : latR));
       T1[h] = make_int4(rF0, rF0 + 4, lkR, 1);
       T0[h + 32] = make_int4(td + tw, md + mw, bwL, L(first ? -1 : latL));
-      T1[h + 32] = make_int4(rF1, rF1 - 4, lkL, 1 << 8);
+      T1[h + 32] = make_int4(rF1, rF1 - 4, lkL, (1 << 8) + (1 << 24));
       T0[h + 64] = make_int4(td, md, bwL, L(first ? -1 : latL));
-      T1[h + 64] = T1[h + 32];
+      T1[h + 64] = make_int4(rF1, rF1 - 4, lkL, (1 << 8) - (1 << 16));
       T0[h + 96] = make_int4(tw, mw, 0, -1);
-      T1[h + 96] = make_int4(z, z, lkR, 0);
+      T1[h + 96] = make_int4(z, z, lkR, 1 << 16);
     }
-    if (s < 8) U[4 * s] = (s & 3) == 2 ? -1 : (s & 3) == 3 ? 1 : (s & 3) == 1 ? 1 << 16 : 0;
     return;
   }
   // chunk 0: F0 goes right (Loop: the last stage's F0 takes the wrap link into stage 0's F1 ring);
@@ -124,7 +137,7 @@ __device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLay
 }  // namespace
 
 template <int kPat, bool kTL>   // kPat: CP_PATTERN_UD / _WAVE / _LOOP; kTL: per-entry start ticks (A.t_start)
-__global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(const __grid_constant__ Args A) {
+__global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF_UD_MINB : kChunkFMinBlocks) k_chunk32f(const __grid_constant__ Args A) {
   constexpr bool kUD = kPat == CP_PATTERN_UD, kLoop = kPat == CP_PATTERN_LOOP;
   constexpr int kRings = kUD ? 2 : 4, kEPW = kUD ? 16 : 8, kStep = 32 / kEPW;   // entries per word, bits per entry
   constexpr int kChunks = kUD ? 1 : 2;
@@ -145,7 +158,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
   const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
 
   // zero block (zero rows + link clocks) and rings start at 0; the zero rows are never written
-  for (int k = lane; k < (Ly.zrows + kRings * R) * 32; k += 32) smem[wbase + Ly.zero + k] = 0;
+  for (int k = lane; k < (kRings * R + Ly.zrows) * 32; k += 32) smem[wbase + Ly.rings + k] = 0;   // rings, zero block
   if (lane == 0) mbar_init(bar);
   if (A.shared_tab) {                               // every item uses instance 0 (host guarantees)
     if (wib == 0) chunkf_tables<kPat>(A.inst, lane, R, Ly, T0, T1, U);
@@ -257,7 +270,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
         const int ty[8] = {last ? 8 : 4, first ? 8 : 2, first ? 8 : 2, 8, first ? 8 : 1, last ? 8 : 7, last ? 8 : 7, 8};
         for (int x = 0; x < 8; ++x) { ix[x] = tx[x]; iy[x] = ty[x]; }
       }
-      const int tn[8] = {0, kUD ? 1 : 2, kUD ? 1 : 2, 12, kUD ? 0 : 1, kUD ? 1 : 3, kUD ? 1 : 3, kUD ? 12 : 13};
+      const int tn[8] = {0, kUD ? 1 : 2, kUD ? 1 : 2, kUD ? 10 : 12, kUD ? 0 : 1, kUD ? 1 : 3, kUD ? 1 : 3, kUD ? 10 : 13};
       pack_sel(ix, kxl, kxh);
       pack_sel(iy, kyl, kyh);
       pack_sel(tn, knl, knh);
@@ -271,12 +284,13 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
     const uint32_t fixR = (kLoop && last) ? 0x5310u : 0x3210u;
     __syncwarp();
 
-    uint32_t c = 0x80808080u, w = 0x80008080u;     // counts + 128; W deficits (bytes 0, 1), sign byte 3
-    int clk = tag, mem = 0, peak = 0, pos4 = 0;
+    // counts + 128; two-chunk: W deficits (bytes 0, 1), #B (byte 2), sign byte 3 in w
+    uint32_t c = 0x80808080u, w = 0x80008080u;
+    int clk = tag, mem = 0, peak = 0, pos4 = 0, lkR = 0, lkL = 0;
     const unsigned tab0m = sb + 4u * (unsigned)tbase + 16u * (unsigned)lane - 480u;   // T0[x][lane] - 15*32
     const unsigned ubm = sb + 4u * (unsigned)(tbase + 2048) - 15u;                    // U[x] - 15
     const unsigned iPb = wb + 4u * (unsigned)(Ly.plan + lane);
-    const int R24 = R << 24, Rm7 = Rm << 7;
+    const int R24 = R << 24, Rm7 = Rm << 7, lk_off_r = 4 * (Ly.lk + lane);
     int32_t* const trow = kTL ? A.t_start + (item * A.stage_stride + s) * (long long)A.len_stride : nullptr;
     uint32_t wv;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(iPb));
@@ -295,21 +309,29 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
       int iw;
       asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(t0.x), "=r"(t0.y), "=r"(t0.z), "=r"(t0.w) : "r"(ta));
       asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+4096];" : "=r"(t1.x), "=r"(t1.y), "=r"(t1.z), "=r"(t1.w) : "r"(ta));
-      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iw) : "r"(ubm + x4));
+      if (!kUD) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(iw) : "r"(ubm + x4));
       const uint32_t sX = prmt(kxl, kxh, x4), sY = prmt(kyl, kyh, x4), sN = prmt(knl, knh, x4);
-      const uint32_t X = prmt(Lv, Rv, sX), Y = prmt(Lv, Rv, sY), n = prmt(c, w, sN);
+      const uint32_t X = prmt(Lv, Rv, sX), Y = prmt(Lv, Rv, sY), n = prmt(c, kUD ? c : w, sN);
       const bool go = (X > n) & ((int)(n - Y) < R24);
       const unsigned slot = (n >> 17) & (unsigned)Rm7;
+      const bool isF = kUD ? (x4 & 0xF0u) == 0u : t1.z == lk_off_r;   // the message takes the right link
       const unsigned ia = wb + (unsigned)t1.x + slot, oa = wb + (unsigned)t1.y + slot, la = wb + (unsigned)t1.z;
       int arr, lk;
       asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"(ia));
-      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lk) : "r"(la));
+      constexpr bool kLkReg = kUD ? CHUNKF_UD_LKREG : CHUNKF_2C_LKREG;
+      if (kLkReg) lk = isF ? lkR : lkL;
+      else asm volatile("ld.shared.b32 %0, [%1];" : "=r"(lk) : "r"(la));
       const int start = cmax(clk, arr);
       const int end = start + t0.x;
       const int nl = cmax(end, lk) + t0.z;          // FIFO link clock (App. X1)
-      if (go & (t0.w >= 0)) {
+      const bool snd = go & (t0.w >= 0);
+      if (snd) {
         asm volatile("st.shared.b32 [%0], %1;" :: "r"(oa), "r"(nl + t0.w) : "memory");
-        asm volatile("st.shared.b32 [%0], %1;" :: "r"(la), "r"(nl) : "memory");
+        if (!kLkReg) asm volatile("st.shared.b32 [%0], %1;" :: "r"(la), "r"(nl) : "memory");
+      }
+      if (kLkReg) {
+        lkR = (snd & isF) ? nl : lkR;
+        lkL = (snd & !isF) ? nl : lkL;
       }
       if (kTL && go && pos4 / kStep < A.len_stride) trow[pos4 / kStep] = start;
       const int gi = go ? 1 : 0;
@@ -317,7 +339,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
       mem = cmadd(gi, t0.y, mem);
       peak = cmax(peak, mem);
       c = (uint32_t)cmadd(gi, t1.w, (int)c);
-      w = (uint32_t)cmadd(gi, iw, (int)w);
+      if (!kUD) w = (uint32_t)cmadd(gi, iw, (int)w);
       pos4 = cmadd(gi, kStep, pos4);
       unsigned wa;
       asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(wa) : "r"((unsigned)pos4 & ~31u), "r"(iPb));
@@ -328,10 +350,16 @@ __global__ void __launch_bounds__(kChunkFThreads, kChunkFMinBlocks) k_chunk32f(c
     const int pos = pos4 / kStep;
     // completed, with Q29's counts: F, D + B of each chunk m (c), as many W as D per chunk (deficit
     // bytes back at 128), B and D not mixed on a stage (#B, byte 2 of w, is 0 or kChunks m)
-    const uint32_t bcnt = (w >> 16) & 0xffu;
-    const uint32_t cwant = kUD ? 0x80808080u + 0x0101u * (uint32_t)m : 0x01010101u * (uint32_t)(128 + m);
-    const bool rowok = s >= p || (pos == plen && c == cwant && (w & 0xffffu) == 0x8080u &&
-                                  (bcnt == 0u || bcnt == (uint32_t)(kChunks * m)));
+    bool rowok;
+    if (kUD) {   // c = {F, D, deficit, #B} + 128
+      const uint32_t bcnt = c >> 24;
+      rowok = s >= p || (pos == plen && (c & 0xffffffu) == 0x808080u + 0x0101u * (uint32_t)m &&
+                         (bcnt == 128u || bcnt == 128u + (uint32_t)m));
+    } else {
+      const uint32_t bcnt = (w >> 16) & 0xffu;
+      rowok = s >= p || (pos == plen && c == 0x01010101u * (uint32_t)(128 + m) && (w & 0xffffu) == 0x8080u &&
+                         (bcnt == 0u || bcnt == (uint32_t)(2 * m)));
+    }
     const bool complete = __all_sync(FMASK, rowok);
     if (!complete) {                                // stalled or invalid: the exact pass classifies it
       if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }

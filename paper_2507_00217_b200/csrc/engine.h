@@ -147,9 +147,9 @@ __host__ __device__ inline Sim32Layout sim32_layout(int R, int plan_words, bool 
 // int4 {duration, memory delta, link bandwidth, latency}, T1 [8][32] int4 {input ring slot-0 address,
 // message slot-0 address, link-clock address, count increment} (addresses relative to the warp region),
 // U [8] int4 {W-deficit increment, -, -, -}.  Per warp: an mbarrier row; a block of zrows rows whose rows
-// 0 and R-1 stay zero (the input of W entries, whose ring slot is 0 or R-1) and which holds the two
-// link-clock rows (rows 1 and 2 when R >= 4, else appended); the four arrival rings F0, F1, D0, D1
-// [R][32] each (UD: F, D); the plan rows (words + 1, the last a padding row); the tables unless the block
+// the arrival rings F0, F1, D0, D1 [R][32] each (UD: F, D); a block of zrows rows whose rows 0 and R-1
+// stay zero (the input of W entries, whose ring slot is 0 or R-1) and which holds the two link-clock
+// rows (rows 1 and 2 when R >= 4, else appended); the plan rows (words + 1, the last a padding row); the tables unless the block
 // holds them.
 constexpr int kChunkFTabWords = 2 * 8 * 32 * 4 + 8 * 4;
 constexpr int kChunkFThreads = 128;
@@ -161,11 +161,11 @@ __host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool sha
   ChunkFLayout L;
   L.hdr = shared_tab ? kChunkFTabWords : 0;
   L.bars = 0;
-  L.zero = 32;
+  L.rings = 32;
+  L.zero = L.rings + rings * R * 32;
   L.zrows = R >= 4 ? R : R + 2;
   L.lk = R >= 4 ? L.zero + 32 : L.zero + R * 32;
-  L.rings = L.zero + L.zrows * 32;
-  L.plan = L.rings + rings * R * 32;
+  L.plan = L.zero + L.zrows * 32;
   int w = L.plan + (words + 1) * 32;
   L.tab = shared_tab ? -1 : w;
   if (!shared_tab) w += kChunkFTabWords;
