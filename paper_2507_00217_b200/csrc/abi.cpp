@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 #include "crosspipe.h"
@@ -555,41 +556,76 @@ int32_t cp_greedy(const cp_instances* in, const cp_schedules* out, const cp_resu
 
 // Evaluate a point set: contiguous points [lo, hi) (own_hi == own_lo), or the blocked ownership of
 // cp_sweep_shard_rank: slice [own_lo, own_hi) of every (n_pp, n_mb) block of `inner` points.
-// Streams forked from `parent` on demand (one per launch) and joined back to it in join(); each
-// stream is released by the runtime once its queued work completes.
+// Launches go to streams forked from `parent` (one per launch) and joined back to it in join().
+// The streams and events are created once per device and reused by later calls (a call that finds
+// the pool in use by another host thread creates its own and destroys them at the join).
+constexpr int kForkMax = 40;
+struct ForkPool {
+  std::mutex mu;
+  int dev = -1;
+  cudaEvent_t fork = nullptr, joins[kForkMax] = {};
+  cudaStream_t sub[kForkMax] = {};
+};
+ForkPool g_fork_pool;
+
 struct Forker {
   cudaStream_t parent;
-  cudaEvent_t fork = nullptr;
-  cudaStream_t sub[40] = {};
+  std::unique_lock<std::mutex> lk;
+  bool pooled = false;
+  cudaEvent_t fork = nullptr, joins[kForkMax] = {};
+  cudaStream_t sub[kForkMax] = {};
   int n = 0;
-  explicit Forker(cudaStream_t p) : parent(p) {}
   bool used_parent = false;
-  // the first launch runs on the parent itself (a single-launch call creates no stream); the fork
-  // point is recorded before it, so later launches do not wait for it
-  cudaStream_t next() {
-    if (!fork) {
-      if (cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return parent;
-      cudaEventRecord(fork, parent);
+  explicit Forker(cudaStream_t p) : parent(p), lk(g_fork_pool.mu, std::try_to_lock) {
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (lk.owns_lock() && (g_fork_pool.dev == dev || g_fork_pool.dev < 0)) {
+      pooled = true;
+      if (g_fork_pool.dev < 0) {                    // first call on this device: create the pool
+        g_fork_pool.dev = dev;
+        cudaEventCreateWithFlags(&g_fork_pool.fork, cudaEventDisableTiming);
+        for (int i = 0; i < kForkMax; ++i) {
+          cudaStreamCreateWithFlags(&g_fork_pool.sub[i], cudaStreamNonBlocking);
+          cudaEventCreateWithFlags(&g_fork_pool.joins[i], cudaEventDisableTiming);
+        }
+      }
+      fork = g_fork_pool.fork;
+      for (int i = 0; i < kForkMax; ++i) { sub[i] = g_fork_pool.sub[i]; joins[i] = g_fork_pool.joins[i]; }
     }
-    if (!used_parent) { used_parent = true; return parent; }
-    if (n == 40) return parent;
-    if (cudaStreamCreateWithFlags(&sub[n], cudaStreamNonBlocking) != cudaSuccess) return parent;
+  }
+  ~Forker() { join(); }
+  // the first launch runs on the parent itself (a single-launch call forks nothing); the fork point
+  // is recorded before it, so later launches do not wait for it
+  cudaStream_t next() {
+    if (!used_parent) {
+      if (!fork && cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return parent;
+      cudaEventRecord(fork, parent);
+      used_parent = true;
+      return parent;
+    }
+    if (n == kForkMax) return parent;
+    if (!pooled) {
+      if (cudaStreamCreateWithFlags(&sub[n], cudaStreamNonBlocking) != cudaSuccess) return parent;
+      if (cudaEventCreateWithFlags(&joins[n], cudaEventDisableTiming) != cudaSuccess) {
+        cudaStreamDestroy(sub[n]);
+        return parent;
+      }
+    }
     cudaStreamWaitEvent(sub[n], fork, 0);
     return sub[n++];
   }
   void join() {
     for (int i = 0; i < n; ++i) {
-      cudaEvent_t j;
-      if (cudaEventCreateWithFlags(&j, cudaEventDisableTiming) == cudaSuccess) {
-        cudaEventRecord(j, sub[i]);
-        cudaStreamWaitEvent(parent, j, 0);
-        cudaEventDestroy(j);
+      cudaEventRecord(joins[i], sub[i]);
+      cudaStreamWaitEvent(parent, joins[i], 0);
+      if (!pooled) {
+        cudaEventDestroy(joins[i]);
+        cudaStreamDestroy(sub[i]);
       }
-      cudaStreamDestroy(sub[i]);
     }
-    if (fork) cudaEventDestroy(fork);
+    if (!pooled && fork) cudaEventDestroy(fork);
     n = 0;
-    fork = nullptr;
+    fork = pooled ? fork : nullptr;
     used_parent = false;
   }
 };
@@ -652,7 +688,11 @@ static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_l
       while (ntier < 3 && lead_max > edge[ntier - 1]) ++ntier;
       const size_t big_warp = (size_t)((cpk::kGreedyTableWords + 2 * (1 << lg2_ceil(lead_max)) * 32 + 3) & ~3) * 4;
       bool ok = big_warp <= kMaxSmemPerBlock;
-      for (int tier = 0; tier < ntier && ok; ++tier) {
+      // the tier holding the largest leads (and the longest tasks: m up to 128 with large budgets) is
+      // launched first, so its tasks start at once instead of queueing behind the persistent grids of
+      // the short tiers (measured on one 1/8 rank shard of config 5: the last-enqueued long tier ended
+      // the shard)
+      for (int tier = ntier - 1; tier >= 0 && ok; --tier) {
         cpk::Args ag = a;
         ag.grid.cand_mask = greedy_mask;
         ag.sweep_counter = counters + 4 * c + 1 + tier;

@@ -79,6 +79,9 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
   const long long n_items = A.from_list ? (long long)*(volatile int32_t*)A.ovf_count : (long long)A.n_items;
   auto item_of = [&](long long t) -> long long { return A.from_list ? (long long)A.ovf_list[t] : t; };
 
+  // second pass over the overflow list: warps beyond the list leave before touching shared memory
+  // (an empty list then costs one short launch)
+  if (A.from_list && gwarp >= n_items) return;
   long long t_it = gwarp;
   // the rings never written by a producer (stage 0's F ring) and the zero row read by W entries
   // must hold 0: clear both ring blocks and the zero row once

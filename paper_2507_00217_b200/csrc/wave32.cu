@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(kFastThreads, kFastMinBlocks) k_chunk32(const 
   const int iF0 = rb0 + lane, iD1 = iF0 + RW, iF1 = iD1 + RW, iD0 = iF1 + RW;
   const int iZ = iD0 + RW;                             // zero row: inputs of W and of missing producers
   const int iP = iZ + 32;
+  if (A.from_list && gwarp >= *(volatile int32_t*)A.ovf_count) return;   // beyond the overflow list
   for (int k = lane; k < 4 * RW + 32; k += 32) smem[rb0 + k] = 0;
   __syncwarp();
 
