@@ -226,7 +226,11 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
       const long long segs = (long long)(32 / Wd) * wpb;
       const long long need = (n + segs - 1) / segs;
       const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
+      // instances from a counter in the workspace control block (zeroed above): segments that finish
+      // early take more, instead of a static stride leaving a tail
+      a.work_counter = std::getenv("CP_GREEDY_STATIC") ? nullptr : reinterpret_cast<int32_t*>(base + 128);
       if (cpk::launch_greedy_fast(Wd, false, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      a.work_counter = nullptr;
       a.from_list = 1;
       a.tma = 0;
       a.plan_words = sc->words <= kPlanCapWords ? sc->words : 0;

@@ -101,6 +101,11 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
           t = __shfl_sync(segmask, t, seg * W);
           item = sweep_task(A.grid.cand_mask & ((1u << CP_N_CAND) - 1u), SweepSet{A.pt_lo, A.pt_hi, A.blk_inner, A.own_lo, A.own_hi},
                         t, cand);
+        } else if (A.work_counter) {                     // dynamic: instances handed out by a counter
+          long long t = 0;
+          if (s == 0) t = atomicAdd(A.work_counter, 1);
+          t = __shfl_sync(segmask, t, seg * W);
+          item = t < A.n_items ? t : -1;
         } else {
           item = task < A.n_items ? task : -1;
           task += tstride;
