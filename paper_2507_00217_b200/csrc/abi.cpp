@@ -187,7 +187,12 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
       if (const char* v = std::getenv("CP_SIM32_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
       const long long need = (n + wpb - 1) / wpb;
       const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
-      if (!first_done && cpk::launch_sim32(tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+      if (!first_done) {
+        // the timeline first pass takes its items from the workspace counter (zeroed above)
+        a.work_counter = std::getenv("CP_SIM32_STATIC") ? nullptr : reinterpret_cast<int32_t*>(base + 128);
+        if (cpk::launch_sim32(tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+        a.work_counter = nullptr;
+      }
       // Items that stalled on a full 8-slot ring (cyclic backpressure) are re-run from the
       // overflow list by the same kernel with rings of R > n_mb slots, where no ring can fill (every
       // producer -> consumer lead is <= n_mb); only when such rings exceed shared memory does the

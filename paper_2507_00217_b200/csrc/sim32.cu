@@ -82,7 +82,16 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
   // second pass over the overflow list: warps beyond the list leave before touching shared memory
   // (an empty list then costs one short launch)
   if (A.from_list && gwarp >= n_items) return;
-  long long t_it = gwarp;
+  // items: a static stride, or (A.work_counter) handed out by a counter, fetched two items ahead
+  // because the plan of the next item is prefetched while the current one runs
+  const bool dyn = A.work_counter != nullptr && !A.from_list;
+  const auto fetch = [&]() -> long long {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(A.work_counter, 1);
+    return (long long)__shfl_sync(FULLM, t, 0);
+  };
+  long long t_it = dyn ? fetch() : gwarp;
+  long long t_nx = dyn ? fetch() : gwarp + nwarps;
   // the rings never written by a producer (stage 0's F ring) and the zero row read by W entries
   // must hold 0: clear both ring blocks and the zero row once
   for (int k = lane; k < 2 * RW; k += 32) smem[rbase + k] = 0;
@@ -93,8 +102,10 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
   uint32_t phase = 0;
   int buf = 0;
 
-  for (; t_it < n_items; t_it += nwarps) {
+  int t_req = 0;                                   // the item after next (dynamic), in flight
+  for (; t_it < n_items; t_it = t_nx, t_nx = dyn ? (long long)__shfl_sync(FULLM, t_req, 0) : t_nx + nwarps) {
     const long long item = item_of(t_it);
+    if (dyn && lane == 0) t_req = atomicAdd(A.work_counter, 1);
     // ------------------------------------------------------------------ load (warp-uniform)
     const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
     const cp_inst_v1* I = A.inst + ii;
@@ -128,8 +139,8 @@ __global__ void __launch_bounds__(SIM32_LB) k_sim32(const __grid_constant__ Args
     // this item's rows were prefetched into plan[buf]: wait, then prefetch the next item's
     mbar_wait(&bars[buf], (phase >> buf) & 1u);
     phase ^= 1u << buf;
-    if (lane == 0 && t_it + nwarps < n_items)
-      tma_load_1d(plan + (buf ^ 1) * PWr * 32, A.ops + item_of(t_it + nwarps) * A.words * 32, plan_bytes,
+    if (lane == 0 && t_nx < n_items)
+      tma_load_1d(plan + (buf ^ 1) * PWr * 32, A.ops + item_of(t_nx) * A.words * 32, plan_bytes,
                   &bars[buf ^ 1]);
     buf ^= 1;
     if (st0) {
