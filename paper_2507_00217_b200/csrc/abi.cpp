@@ -348,10 +348,29 @@ size_t sweep_class_ring_bytes(const cp_grid* g, int ip) {
   return align256((size_t)cpk::kFixWarps * ring_bytes_per_warp(slots));
 }
 
+// The static candidates (GPipe / 1F1B / ZB-H1) run on k_chunk32f<UD, grid> when every n_mb of the
+// grid fits its count bytes; their plans come from a library built per call, after the ring regions.
+constexpr unsigned kStaticCands = (1u << CP_PLAN_GPIPE) | (1u << CP_PLAN_1F1B) | (1u << CP_PLAN_ZBH1);
+bool sweep_static_fast(const cp_grid* g) {
+  if (!(g->cand_mask & kStaticCands) || getenv_nofast() || std::getenv("CP_SWEEP_STATIC_ENGINE")) return false;
+  for (int i = 0; i < g->n_mb_n; ++i)
+    if (g->n_mb_vals[i] > 255) return false;
+  return true;
+}
+int plan_lib_words(const cp_grid* g) {
+  int mx = 1;
+  for (int i = 0; i < g->n_mb_n; ++i) mx = std::max(mx, g->n_mb_vals[i]);
+  return (3 * mx + 15) / 16;                   // ZB-H1 rows (3m) are the longest
+}
+size_t plan_lib_bytes(const cp_grid* g) {
+  // 8 task counters (one per p-class), then the plans
+  return sweep_static_fast(g) ? align256(64 + (size_t)3 * g->n_pp_n * g->n_mb_n * plan_lib_words(g) * 32 * 4) : 0;
+}
+
 size_t sweep_ws_bytes(const cp_grid* g) {
   size_t b = kCtrlBytes;
   for (int ip = 0; ip < g->n_pp_n; ++ip) b += sweep_class_ring_bytes(g, ip);
-  return b;
+  return b + plan_lib_bytes(g);
 }
 
 long long point_cost(const cp_grid* g, int i_pp, int i_mb) {
@@ -652,6 +671,25 @@ static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_l
                              own_lo, own_hi, stream) != cudaSuccess)
     return CP_ECUDA;
   if (cudaMemsetAsync(counters, 0, sizeof(unsigned long long) * 32, st) != cudaSuccess) return CP_ECUDA;
+  // static candidates on k_chunk32f: their plan library (every (kind, n_pp, n_mb) block of the grid)
+  const bool static_fast = sweep_static_fast(g);
+  uint32_t* plan_lib = nullptr;
+  unsigned long long* static_counters = nullptr;
+  if (static_fast) {
+    size_t off = kCtrlBytes;
+    for (int q = 0; q < g->n_pp_n; ++q) off += sweep_class_ring_bytes(g, q);
+    static_counters = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + off);
+    plan_lib = reinterpret_cast<uint32_t*>(static_cast<char*>(ws) + off + 64);
+    if (cudaMemsetAsync(static_counters, 0, 64, st) != cudaSuccess) return CP_ECUDA;
+    cpk::PlanLibDims d;
+    std::memset(&d, 0, sizeof(d));
+    for (int i = 0; i < g->n_pp_n; ++i) d.pp[i] = g->n_pp_vals[i];
+    for (int i = 0; i < g->n_mb_n; ++i) d.mb[i] = g->n_mb_vals[i];
+    d.n_pp = g->n_pp_n;
+    d.n_mb = g->n_mb_n;
+    d.words = plan_lib_words(g);
+    if (cpk::launch_plan_library(d, plan_lib, stream) != cudaSuccess) return CP_ECUDA;
+  }
   // p is the slowest axis: one contiguous block of points per p-class; each class gets its own
   // segment width W and ring size, and the classes run concurrently on forked streams
   const long long per_pp = np / g->n_pp_n;
@@ -719,6 +757,25 @@ static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_l
         if (cpk::launch_greedy_fast(Wd, true, ag, blocks, threads, smem, fk.next()) != cudaSuccess) rc = CP_ECUDA;
       }
       if (ok) engine_mask &= ~greedy_mask;
+    }
+    if (!rc && static_fast && (engine_mask & kStaticCands)) {
+      // GPipe / 1F1B / ZB-H1 of this class on k_chunk32f<UD, grid> (8-slot rings: the static families
+      // never lead by more than two messages), plans from the library, one task per warp
+      cpk::Args as = a;
+      as.grid.cand_mask = engine_mask & kStaticCands;
+      as.sweep_counter = static_counters + c;
+      as.ops = plan_lib;
+      as.words = plan_lib_words(g);
+      as.ring_slots = 8;
+      as.shared_tab = 0;
+      const cpk::ChunkFLayout L = cpk::chunkf_layout(as.ring_slots, as.words, false, 2);
+      const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;
+      const size_t smem = (size_t)wpb * L.per_warp * 4;
+      const int bps = smsp_balanced(cpk::chunkf_grid_blocks_per_sm(threads, smem), wpb);
+      const long long need = (npts * __builtin_popcount(as.grid.cand_mask) + wpb - 1) / wpb;
+      const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
+      if (cpk::launch_chunkf_grid(as, blocks, threads, smem, fk.next()) != cudaSuccess) rc = CP_ECUDA;
+      engine_mask &= ~kStaticCands;
     }
     if (!rc && engine_mask) {
       a.grid.cand_mask = engine_mask;

@@ -174,5 +174,13 @@ __host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool sha
 }
 int launch_chunkf(int pattern, bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream);
 int chunkf_blocks_per_sm(int pattern, int threads, size_t smem);
+// the sweep's static candidates (GPipe / 1F1B / ZB-H1) on k_chunk32f<UD, grid>: plans from a library
+// of [3 kinds][n_pp][n_mb] plans of `words` words built per sweep call (k_plan_library)
+struct PlanLibDims {
+  int pp[8], mb[8], n_pp, n_mb, words;
+};
+int launch_plan_library(const PlanLibDims& d, uint32_t* lib, void* stream);
+int launch_chunkf_grid(const Args& a, int blocks, int threads, size_t smem, void* stream);
+int chunkf_grid_blocks_per_sm(int threads, size_t smem);
 
 }  // namespace cpk
