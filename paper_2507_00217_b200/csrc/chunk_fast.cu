@@ -3,14 +3,16 @@
 // Items it does not finish (a stall, which may be an artefact of its 8-slot rings, n_sub > 1,
 // n_mb > 127, anything invalid) go to the overflow list and are evaluated exactly by the second pass
 // with rings of n_mb slots: k_sim32 (sim32.cu) for UD, k_chunk32 (wave32.cu) for Wave / Loop.
+// Grid mode (UD): the sweep's static candidates, with plans from a per-call plan library.
 //
 // What makes the round short:
-//  * Block counts are bytes.  c = {F0, F1, D0, D1} counts + 128 (UD: {F, D, -, -}; every byte has its
-//    top bit set), one register; one shuffle per direction hands a lane its neighbours' counts.
+//  * Block counts are bytes.  Two-chunk: c = {F0, F1, D0, D1} counts + 128 (every byte has its top bit
+//    set).  UD: c = {F, D, 128 - W deficit, 0x80}, plain counts up to 255.  One register; one shuffle
+//    per direction hands a lane its neighbours' counts.
 //  * Readiness of the entry's own stream in three PRMTs and three compares: the producer count X,
 //    the consumer count Y and the own count n are byte-selected into the top byte (X from the left /
 //    right neighbour, or the own count at a turn-around / the loss, or 0xFF = "no producer" by sign
-//    replication of a biased byte), and the entry is ready iff X > n and n - Y < R.  The selectors
+//    replication of a byte with its top bit set), and the entry is ready iff X > n and n - Y < R.  The selectors
 //    come from per-lane 8-entry byte tables held in registers, indexed by the entry code with one
 //    more PRMT each.  W entries use the same test: their n is the sign of the chunk's W deficit byte
 //    w = 128 - (#D - #W) (0x00 when a D is owed its W, else 0xFF) against X = Y = 0xFF.
