@@ -3,16 +3,14 @@
 // Items it does not finish (a stall, which may be an artefact of its 8-slot rings, n_sub > 1,
 // n_mb > 127, anything invalid) go to the overflow list and are evaluated exactly by the second pass
 // with rings of n_mb slots: k_sim32 (sim32.cu) for UD, k_chunk32 (wave32.cu) for Wave / Loop.
-// Grid mode (UD): the sweep's static candidates, with plans from a per-call plan library.
 //
 // What makes the round short:
-//  * Block counts are bytes.  Two-chunk: c = {F0, F1, D0, D1} counts + 128 (every byte has its top bit
-//    set).  UD: c = {F, D, 128 - W deficit, 0x80}, plain counts up to 255.  One register; one shuffle
-//    per direction hands a lane its neighbours' counts.
+//  * Block counts are bytes.  c = {F0, F1, D0, D1} counts + 128 (UD: {F, D, -, -}; every byte has its
+//    top bit set), one register; one shuffle per direction hands a lane its neighbours' counts.
 //  * Readiness of the entry's own stream in three PRMTs and three compares: the producer count X,
 //    the consumer count Y and the own count n are byte-selected into the top byte (X from the left /
 //    right neighbour, or the own count at a turn-around / the loss, or 0xFF = "no producer" by sign
-//    replication of a byte with its top bit set), and the entry is ready iff X > n and n - Y < R.  The selectors
+//    replication of a biased byte), and the entry is ready iff X > n and n - Y < R.  The selectors
 //    come from per-lane 8-entry byte tables held in registers, indexed by the entry code with one
 //    more PRMT each.  W entries use the same test: their n is the sign of the chunk's W deficit byte
 //    w = 128 - (#D - #W) (0x00 when a D is owed its W, else 0xFF) against X = Y = 0xFF.
@@ -27,8 +25,6 @@
 #include <stdint.h>
 
 #include "engine.h"
-#include "grid_synth.cuh"
-#include "plan_codes.cuh"
 #include "ptx.cuh"
 
 #ifndef CHUNKF_UD_LKREG
@@ -69,48 +65,35 @@ __device__ __forceinline__ void pack_sel(const int (&ix)[8], uint32_t& lo, uint3
   }
 }
 
-// One lane's (stage's) costs: durations, memory deltas, and its right (s -> s+1; Loop: forward,
-// with the wrap at p-1) and left (s -> s-1; Loop: backward, with the wrap at 0) links.
-struct LaneVals {
-  int p, tf, td, tw, mf, md, mw, latR, bwR, latL, bwL;
-};
-template <bool kLoop>
-__device__ __forceinline__ LaneVals lane_vals(const cp_inst_v1* I, int s) {
-  LaneVals v = {};
-  v.p = I->n_pp < 1 ? 1 : (I->n_pp > CP_MAX_STAGES ? CP_MAX_STAGES : I->n_pp);   // (other p: not run here)
-  const int p = v.p;
-  if (s < p) {
-    v.tf = I->t_f[s]; v.td = I->t_d[s]; v.tw = I->t_w[s];
-    v.mf = I->m_f[s]; v.md = I->m_d[s]; v.mw = I->m_w[s];
-    // boundary s = link s -> s+1; Loop also uses index p-1, the wrap links p-1 -> 0 / 0 -> p-1 (Q33)
-    if (s < p - 1 || kLoop) { v.latR = I->lat_f[s]; v.bwR = I->bw_f[s]; }
-    if (s > 0) { v.latL = I->lat_b[s - 1]; v.bwL = I->bw_b[s - 1]; }
-    else if (kLoop) { v.latL = I->lat_b[p - 1]; v.bwL = I->bw_b[p - 1]; }
-  }
-  return v;
-}
-
-// Per-lane table rows (entry x = type | chunk << 2).  T0/T1 point at [x = 0][lane], rows 32 int4
-// apart; U at [0] (16-B rows).  Addresses are byte offsets from the warp region.
+// Per-lane table rows of instance I (entry x = type | chunk << 2).  T0/T1 point at [x = 0][lane],
+// rows 32 int4 apart; U at [0] (16-B rows).  Addresses are byte offsets from the warp region.
 template <int kPat>   // CP_PATTERN_UD / _WAVE / _LOOP
-__device__ void chunkf_tables(const LaneVals& v, int s, int R, const ChunkFLayout& Ly, int4* T0, int4* T1, int* U) {
+__device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLayout& Ly, int4* T0, int4* T1, int* U) {
   constexpr bool kUD = kPat == CP_PATTERN_UD, kLoop = kPat == CP_PATTERN_LOOP;
-  const int p = v.p;
+  const int p = I->n_pp < 1 ? 1 : (I->n_pp > CP_MAX_STAGES ? CP_MAX_STAGES : I->n_pp);   // (other p: not run here)
   const bool live = s < p, first = s == 0, last = s == p - 1;
-  const int tf = v.tf, td = v.td, tw = v.tw, mf = v.mf, md = v.md, mw = v.mw;
-  const int latR = v.latR, bwR = v.bwR, latL = v.latL, bwL = v.bwL;
+  int tf = 0, td = 0, tw = 0, mf = 0, md = 0, mw = 0, latR = 0, bwR = 0, latL = 0, bwL = 0;
+  if (live) {
+    tf = I->t_f[s]; td = I->t_d[s]; tw = I->t_w[s];
+    mf = I->m_f[s]; md = I->m_d[s]; mw = I->m_w[s];
+    // boundary s = link s -> s+1; Loop also uses index p-1, the wrap links p-1 -> 0 / 0 -> p-1 (Q33)
+    if (s < p - 1 || kLoop) { latR = I->lat_f[s]; bwR = I->bw_f[s]; }
+    if (s > 0) { latL = I->lat_b[s - 1]; bwL = I->bw_b[s - 1]; }
+    else if (kLoop) { latL = I->lat_b[p - 1]; bwL = I->bw_b[p - 1]; }
+  }
   const int RB = R * 128, col = 4 * s;
   const int rF0 = Ly.rings * 4 + col, rF1 = rF0 + RB, rD0 = rF0 + 2 * RB, rD1 = rF0 + 3 * RB;
   const int z = Ly.zero * 4 + col, lkR = Ly.lk * 4 + col, lkL = lkR + 128;
   const auto L = [&](int lat) { return live ? lat : -1; };   // latency -1: the entry sends nothing
   if (kUD) {
     // rings F (0) and D (1); F goes right, D / B left; entry x = code, rows 4..7 repeat 0..3.  One
-    // count register c = {F, D, 128 - (#D - #W), 0x80}: F +1; B: D +1; D: D +1 and byte 2 -1; W: byte 2 +1
+    // count register c = {F, D, W deficit, #B} (+128 each): F +1; B: D +1, #B +1; D: D +1, deficit -1;
+    // W: deficit +1
     for (int h = 0; h < 256; h += 128) {
       T0[h] = make_int4(tf, mf, bwR, L(last ? -1 : latR));
       T1[h] = make_int4(rF0, rF0 + 4, lkR, 1);
       T0[h + 32] = make_int4(td + tw, md + mw, bwL, L(first ? -1 : latL));
-      T1[h + 32] = make_int4(rF1, rF1 - 4, lkL, 1 << 8);
+      T1[h + 32] = make_int4(rF1, rF1 - 4, lkL, (1 << 8) + (1 << 24));
       T0[h + 64] = make_int4(td, md, bwL, L(first ? -1 : latL));
       T1[h + 64] = make_int4(rF1, rF1 - 4, lkL, (1 << 8) - (1 << 16));
       T0[h + 96] = make_int4(tw, mw, 0, -1);
@@ -153,11 +136,7 @@ __device__ void chunkf_tables(const LaneVals& v, int s, int R, const ChunkFLayou
 }
 }  // namespace
 
-// kPat: CP_PATTERN_UD / _WAVE / _LOOP; kTL: per-entry start ticks (A.t_start).  kGrid (UD only): the
-// sweep's static candidates -- (point, candidate) tasks of A.grid from A.sweep_counter, instances
-// synthesized per lane (grid_synth.cuh), the candidate's plan from the per-sweep plan library at
-// A.ops ([kind][n_pp][n_mb] plans of A.words words, build_plan_library), makespan and argmin key out.
-template <int kPat, bool kTL, bool kGrid = false>
+template <int kPat, bool kTL>   // kPat: CP_PATTERN_UD / _WAVE / _LOOP; kTL: per-entry start ticks (A.t_start)
 __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF_UD_MINB : kChunkFMinBlocks) k_chunk32f(const __grid_constant__ Args A) {
   constexpr bool kUD = kPat == CP_PATTERN_UD, kLoop = kPat == CP_PATTERN_LOOP;
   constexpr int kRings = kUD ? 2 : 4, kEPW = kUD ? 16 : 8, kStep = 32 / kEPW;   // entries per word, bits per entry
@@ -182,7 +161,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
   for (int k = lane; k < (kRings * R + Ly.zrows) * 32; k += 32) smem[wbase + Ly.rings + k] = 0;   // rings, zero block
   if (lane == 0) mbar_init(bar);
   if (A.shared_tab) {                               // every item uses instance 0 (host guarantees)
-    if (wib == 0) chunkf_tables<kPat>(lane_vals<kLoop>(A.inst, lane), lane, R, Ly, T0, T1, U);
+    if (wib == 0) chunkf_tables<kPat>(A.inst, lane, R, Ly, T0, T1, U);
     __syncthreads();
   }
   __syncwarp();
@@ -193,56 +172,26 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
   const uint32_t opq = (uint32_t)A.words >> 30;
   const uint32_t fifteen = 15u | (opq << 20);       // (bits >= 16 of a PRMT selector are ignored)
 
-  // items (tasks) are handed out by a counter (A.work_counter; the sweep's A.sweep_counter), the next
-  // index fetched one item ahead; without a counter, warp w takes items w, w + warps, ...
-  const bool dyn = kGrid || A.work_counter != nullptr;
-  const auto grab = [&]() -> long long {           // lane 0
-    if (kGrid) return (long long)atomicAdd(A.sweep_counter, 1ull);
-    return (long long)atomicAdd(A.work_counter, 1);
-  };
-  const unsigned smask = A.grid.cand_mask & ((1u << CP_N_CAND) - 1u);
-  const SweepSet sset{A.pt_lo, A.pt_hi, A.blk_inner, A.own_lo, A.own_hi};
-  const long long inner = (long long)A.grid.n_lat * A.grid.n_bw * A.grid.n_mem * A.grid.n_dp;
-  const long long nblk = (long long)A.grid.n_pp_n * A.grid.n_mb_n;
-  long long tsk = gwarp, tnx = 0;
+  // items are handed out by a counter (A.work_counter), the next index fetched one item ahead; without
+  // a counter, warp w takes items w, w + warps, ...
+  const bool dyn = A.work_counter != nullptr;
+  long long item = gwarp, nxt = 0;
   if (dyn) {
-    long long t0 = 0;
-    if (lane == 0) t0 = grab();
-    tsk = __shfl_sync(FMASK, t0, 0);
+    int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(A.work_counter, 1);
+    item = __shfl_sync(FMASK, t0, 0);
   }
-  for (;; tsk = dyn ? __shfl_sync(FMASK, tnx, 0) : tsk + nwarps) {
-    int cand = 0;
-    long long item;
-    if (kGrid) {
-      item = sweep_task(smask, sset, tsk, cand);
-      if (item < 0) break;
-    } else {
-      if (tsk >= A.n_items) break;
-      item = tsk;
-    }
-    if (dyn && lane == 0) tnx = grab();
+  for (; item < A.n_items; item = dyn ? (long long)__shfl_sync(FMASK, (int)nxt, 0) : item + nwarps) {
+    if (dyn && lane == 0) nxt = atomicAdd(A.work_counter, 1);
     // the previous item's generic-proxy writes to the plan rows are ordered before the bulk copy
     if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    if (lane == 0) {
-      const long long pi = kGrid ? (cand == CP_PLAN_GPIPE ? 0 : (cand == CP_PLAN_1F1B ? 1 : 2)) * nblk + item / inner : item;
-      tma_load_1d(plan, A.ops + pi * PW * 32, (uint32_t)PW * 128u, bar);
-    }
-    const long long ii = kGrid ? 0 : (A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item));
+    if (lane == 0) tma_load_1d(plan, A.ops + item * PW * 32, (uint32_t)PW * 128u, bar);
+    const long long ii = A.inst_of ? (long long)A.inst_of[item] : (A.n_inst == 1 ? 0 : item);
     const cp_inst_v1* I = A.inst + ii;
-    GridLane g = {};
-    if (kGrid) g = grid_lane(A.grid, item, s);
-    const int p = kGrid ? g.p : I->n_pp, m = kGrid ? g.m : I->n_mb, ns = kGrid ? 1 : I->n_sub;
+    const int p = I->n_pp, m = I->n_mb, ns = I->n_sub;
     int tf = 0, td = 0, tw = 0, mf = 0, md = 0, mw = 0, mlim = 0, tdp = 0, tag = 0;
     int latR = 0, bwR = 0, latL = 0, bwL = 0, lat_b_s = 0, bw_b_s = 0, plen = 0;
-    if (kGrid) {
-      if (s < p) {
-        tf = g.tf; td = g.td; tw = g.tw; mf = g.mf; md = g.md; mw = g.mw; mlim = g.mlim;
-        tdp = g.tdp; tag = g.zero1 ? g.tag : 0;
-        latR = g.latF; bwR = g.bwF; latL = g.latB; bwL = g.bwB;
-        lat_b_s = latR; bw_b_s = bwR;
-        plen = plan_row_len(cand, m);
-      }
-    } else if (s < p && p <= CP_MAX_STAGES) {
+    if (s < p && p <= CP_MAX_STAGES) {
       tf = I->t_f[s]; td = I->t_d[s]; tw = I->t_w[s];
       mf = I->m_f[s]; md = I->m_d[s]; mw = I->m_w[s]; mlim = I->m_lim[s];
       tdp = I->t_dp[s]; tag = (I->flags & 1) ? I->t_ag[s] : 0;
@@ -252,12 +201,10 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
       plen = A.len[item * 32 + s];
     }
     // the shapes this pass takes; everything else is classified by the exact pass
-    // (grid: GPipe / 1F1B have no W and ZB-H1 owes at most s + 1 W blocks, so n_mb up to 255 fits the
-    // UD count bytes and the W deficit byte)
-    bool ok = p >= (kLoop ? 2 : 1) && p <= CP_MAX_STAGES && m >= 1 && m <= (kGrid ? 255 : 127) && ns == 1;
+    bool ok = p >= (kLoop ? 2 : 1) && p <= CP_MAX_STAGES && m >= 1 && m <= 127 && ns == 1;
     if (ok && s < p)
       ok = tf >= 1 && td >= 1 && tw >= 1 && mf > 0 && md <= 0 && mw <= 0 && (long long)mf + md + mw == 0 &&
-           mlim >= mf && tdp >= 0 && (kGrid ? g.tag : I->t_ag[s]) >= 0 && latR >= 0 && bwR >= 0 && lat_b_s >= 0 && bw_b_s >= 0 &&
+           mlim >= mf && tdp >= 0 && I->t_ag[s] >= 0 && latR >= 0 && bwR >= 0 && lat_b_s >= 0 && bw_b_s >= 0 &&
            plen <= kEPW * PW;
     long long u = (s < p && ok) ? kChunks * (long long)m * ((long long)tf + td + tw) + tag + tdp +
                                       kChunks * (long long)m * ((long long)latR + bwR + latL + bwL)
@@ -266,54 +213,29 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
     ok = __all_sync(FMASK, ok) && u < (long long)CINF;
     mbar_wait(bar, phase);
     phase ^= 1u;
-    if (kGrid) {
-      // statically infeasible candidates are skipped (GPipe peak m m_f, 1F1B peak min(p - s, m) m_f
-      // over M_L, Z5; their cand_ms stays -1, no key); ZB-H1 is evaluated and excluded if over M_L.
-      // n_mb beyond the count bytes is left to the engine pass; the int32 horizon guard marks the
-      // point unevaluated (KEY_OVER), as the engine does.
-      const bool skip = s < p && (cand == CP_PLAN_GPIPE ? (long long)m * mf > mlim
-                                                          : (cand == CP_PLAN_1F1B ? (long long)min(p - s, m) * mf > mlim : false));
-      if (__any_sync(FMASK, skip) || m > 255) { __syncwarp(); continue; }
-      if (!ok) {
-        if (lane == 0) atomicMin(A.keys + item, KEY_OVER);
-        __syncwarp();
-        continue;
-      }
-    }
     // stage the row: codes < 8, pad past the end with D0, pre-rotate by one entry.  Q29's count and
     // mixing rules are checked on the final counts of a completed row (below); the W-prefix rule is
     // dynamic (a W ahead of its D never becomes ready).  No count can wrap its byte: an entry runs
     // only while its own count is below its producer's (<= 255), and a W only while a D is owed.
     if (ok) {
-      bool bplan = false, anyB = false, anyD = false;
+      bool bplan = false;
       for (int k = 0; k <= PW; ++k) {
         uint32_t w = (uint32_t)plan[(k << 5) + lane];
         const int n = s < p ? min(max(plen - kEPW * k, 0), kEPW) : 0;
         const uint32_t keep = n == kEPW ? 0xffffffffu : ((1u << (kStep * n)) - 1u);
         if (!kUD) bplan |= ((w & keep & 0x88888888u) != 0u);
-        if (kUD) {                                 // Q29: B blocks and D / W blocks not mixed on a stage
-          const uint32_t lo = w & keep & 0x55555555u, hi = (w >> 1) & keep & 0x55555555u;
-          anyB |= (lo & ~hi) != 0u;
-          anyD |= hi != 0u;
-        }
         w = (w & keep) | (kPad & ~keep);
         plan[(k << 5) + lane] = (int32_t)((w << 4) | (w >> 28));
       }
-      ok = !__any_sync(FMASK, bplan || (anyB && anyD));
+      ok = !__any_sync(FMASK, bplan);
     }
     if (!ok) {                                      // the exact pass takes it
-      if (kGrid) { if (lane == 0) atomicMin(A.keys + item, KEY_OVER); }
-      else if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
+      if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
       __syncwarp();
       continue;
     }
-    if (kGrid) {
-      LaneVals v = {};
-      v.p = p; v.tf = tf; v.td = td; v.tw = tw; v.mf = mf; v.md = md; v.mw = mw;
-      v.latR = latR; v.bwR = bwR; v.latL = latL; v.bwL = bwL;
-      chunkf_tables<kPat>(v, lane, R, Ly, T0, T1, U);
-    } else if (!A.shared_tab && ii != tab_inst) {
-      chunkf_tables<kPat>(lane_vals<kLoop>(I, lane), lane, R, Ly, T0, T1, U);
+    if (!A.shared_tab && ii != tab_inst) {
+      chunkf_tables<kPat>(I, lane, R, Ly, T0, T1, U);
       tab_inst = ii;
     }
     // ring columns read without a producer in this item but written by a larger previous one
@@ -336,11 +258,8 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
     {
       int ix[8], iy[8];
       if (kUD) {
-        // counts are plain bytes (0..255); "no producer" and the W tests take the sign of byte 3 (0x80);
-        // a block without a consumer compares with its own count (stage 0 / the last stage see their own
-        // counts in the left / right view), so n - Y = 0
-        const int tx[8] = {first ? 11 : 0, last ? 4 : 5, last ? 4 : 5, 11, first ? 11 : 0, last ? 4 : 5, last ? 4 : 5, 11};
-        const int ty[8] = {4, 1, 1, 11, 4, 1, 1, 11};
+        const int tx[8] = {first ? 8 : 0, last ? 4 : 5, last ? 4 : 5, 8, first ? 8 : 0, last ? 4 : 5, last ? 4 : 5, 8};
+        const int ty[8] = {last ? 8 : 4, first ? 8 : 1, first ? 8 : 1, 8, last ? 8 : 4, first ? 8 : 1, first ? 8 : 1, 8};
         for (int x = 0; x < 8; ++x) { ix[x] = tx[x]; iy[x] = ty[x]; }
       } else if (kLoop) {
         const int tx[8] = {first ? 8 : 0, 6, 6, 8, first ? 0 : 1, 7, 7, 8};
@@ -365,9 +284,8 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
     const uint32_t fixR = (kLoop && last) ? 0x5310u : 0x3210u;
     __syncwarp();
 
-    // UD: {F, D, 128 - W deficit, 0x80}; two-chunk: counts + 128, and W deficits (bytes 0, 1), #B (byte 2),
-    // sign byte 3 in w
-    uint32_t c = kUD ? 0x80800000u : 0x80808080u, w = 0x80008080u;
+    // counts + 128; two-chunk: W deficits (bytes 0, 1), #B (byte 2), sign byte 3 in w
+    uint32_t c = 0x80808080u, w = 0x80008080u;
     int clk = tag, mem = 0, peak = 0, pos4 = 0, lkR = 0, lkL = 0;
     const unsigned tab0m = sb + 4u * (unsigned)tbase + 16u * (unsigned)lane - 480u;   // T0[x][lane] - 15*32
     const unsigned ubm = sb + 4u * (unsigned)(tbase + 2048) - 15u;                    // U[x] - 15
@@ -433,8 +351,10 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
     // completed, with Q29's counts: F, D + B of each chunk m (c), as many W as D per chunk (deficit
     // bytes back at 128), B and D not mixed on a stage (#B, byte 2 of w, is 0 or kChunks m)
     bool rowok;
-    if (kUD) {   // c = {F, D, 128 - deficit, 0x80} (B / D mixing was checked when the row was staged)
-      rowok = s >= p || (pos == plen && c == 0x80800000u + 0x0101u * (uint32_t)m);
+    if (kUD) {   // c = {F, D, deficit, #B} + 128
+      const uint32_t bcnt = c >> 24;
+      rowok = s >= p || (pos == plen && (c & 0xffffffu) == 0x808080u + 0x0101u * (uint32_t)m &&
+                         (bcnt == 128u || bcnt == 128u + (uint32_t)m));
     } else {
       const uint32_t bcnt = (w >> 16) & 0xffu;
       rowok = s >= p || (pos == plen && c == 0x01010101u * (uint32_t)(128 + m) && (w & 0xffffu) == 0x8080u &&
@@ -442,10 +362,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
     }
     const bool complete = __all_sync(FMASK, rowok);
     if (!complete) {                                // stalled or invalid: the exact pass classifies it
-      // (grid: the static families cannot stall on 8-slot rings -- a producer leads its consumer by
-      // at most two messages -- so this is the engine's "never happens" path: point unevaluated)
-      if (kGrid) { if (lane == 0) atomicMin(A.keys + item, KEY_OVER); }
-      else if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
+      if (lane == 0) { const int slot = atomicAdd(A.ovf_count, 1); A.ovf_list[slot] = (int32_t)item; }
       __syncwarp();
       continue;
     }
@@ -454,14 +371,6 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
     for (int d = 16; d > 0; d >>= 1) {
       ms = cmax(ms, __shfl_xor_sync(FMASK, ms, d));
       pk = cmax(pk, __shfl_xor_sync(FMASK, pk, d));
-    }
-    if (kGrid) {                                    // one (point, candidate) task
-      if (lane == 0 && st == 0) {
-        if (A.cand_ms) A.cand_ms[item * CP_N_CAND + cand] = ms;
-        atomicMin(A.keys + item, ((unsigned long long)ms << 8) | (unsigned)cand);
-      }
-      __syncwarp();
-      continue;
     }
     if (lane == 0) {
       A.makespan[item] = (long long)ms;
@@ -489,27 +398,6 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
   }
 }
 
-// The sweep's static-candidate plans: one per (kind in GPipe / 1F1B / ZB-H1, n_pp, n_mb) block of the
-// grid, in the simulate layout [words][32 stages]; lane = stage, entries from plan_code (plan_codes.cuh).
-__global__ void k_plan_library(PlanLibDims d, uint32_t* lib) {
-  const int b = blockIdx.x, s = threadIdx.x;
-  const int nblk = d.n_pp * d.n_mb;
-  const int kind = b / nblk == 0 ? CP_PLAN_GPIPE : (b / nblk == 1 ? CP_PLAN_1F1B : CP_PLAN_ZBH1);
-  const int p = d.pp[(b % nblk) / d.n_mb], m = d.mb[(b % nblk) % d.n_mb];
-  const int len = s < p ? plan_row_len(kind, m) : 0;
-  uint32_t* out = lib + (long long)b * d.words * 32 + s;
-  for (int k = 0; k < d.words; ++k) {
-    uint32_t w = 0;
-    for (int e = 0; e < 16 && 16 * k + e < len; ++e) w |= (uint32_t)plan_code(kind, s, p, m, 16 * k + e) << (2 * e);
-    out[k * 32] = w;
-  }
-}
-
-int launch_plan_library(const PlanLibDims& d, uint32_t* lib, void* stream) {
-  k_plan_library<<<3 * d.n_pp * d.n_mb, 32, 0, (cudaStream_t)stream>>>(d, lib);
-  return (int)cudaGetLastError();
-}
-
 namespace {
 const void* chunkf_fn(int pat, bool tl) {
   switch (pat) {
@@ -519,24 +407,6 @@ const void* chunkf_fn(int pat, bool tl) {
   }
 }
 }  // namespace
-
-int launch_chunkf_grid(const Args& a, int blocks, int threads, size_t smem, void* stream) {
-  const void* fn = (const void*)k_chunk32f<CP_PATTERN_UD, false, true>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-  }
-  void* params[] = {(void*)&a};
-  return (int)cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
-}
-
-int chunkf_grid_blocks_per_sm(int threads, size_t smem) {
-  const void* fn = (const void*)k_chunk32f<CP_PATTERN_UD, false, true>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;
-  return n > 0 ? n : 1;
-}
 
 int launch_chunkf(int pattern, bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream) {
   const void* fn = chunkf_fn(pattern, timeline);

@@ -214,3 +214,18 @@ def test_sweep_workspace_covers_global_rings():
     big = cp.api.to_cp_grid(_grid(pp=(2, 4), mb=(1024,), mlim=(600000,)))
     nb = lib.cp_workspace_bytes(2, C.byref(big), 0)
     assert nb >= 256 + 2 * 148 * 4 * 2 * 1024 * 32 * 4, nb
+
+
+def test_bench_kernel_register_budget():
+    """The bench kernel k_chunk32f<UD> keeps 7 resident 4-warp blocks per SM only at <= 72 registers
+    per thread; small source changes have pushed it to 78 (6 blocks, -5% on config 4),
+    so the built library is checked here (cuobjdump, no GPU needed)."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "--dump-resource-usage", L.LIB_PATH], capture_output=True, text=True).stdout
+    m = re.search(r"Function _ZN3cpk10k_chunk32fILi0ELb0EEEvNS_4ArgsE:\s*\n\s*REG:(\d+)", out)
+    assert m, "k_chunk32f<UD, no timeline> not found in the library"
+    assert int(m.group(1)) <= 72, f"k_chunk32f<UD> uses {m.group(1)} registers (> 72: 6 instead of 7 blocks per SM)"
