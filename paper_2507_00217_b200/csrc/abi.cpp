@@ -155,23 +155,24 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
     // fast path (sim32.cu): warp = one item, TMA double-buffered plan rows with a spare row.  When every
     // item uses instance 0, a 4-warp block shares one cost / increment table (24 resident warps).
     const bool tl = res->t_start != nullptr;
-    // Without a timeline the first pass is k_chunk32f (chunk_fast.cu, byte-count readiness, dynamic item
-    // counter); with one, k_sim32 (its start ticks are staged in shared memory and written 32 B per lane).
-    // Either lists the items it does not finish for the exact second pass below.
+    // The first pass is k_chunk32f (chunk_fast.cu, byte-count readiness, dynamic item counter; with a
+    // timeline its start ticks are staged in shared memory and written 32 B per lane); it lists the
+    // items it does not finish for the exact second pass below (k_sim32).  CP_CHUNKF_OFF=1: k_sim32 for
+    // both passes.
     bool first_done = false;
-    if (!tl && !std::getenv("CP_CHUNKF_OFF")) {
+    if (!std::getenv("CP_CHUNKF_OFF")) {
       a.ring_slots = std::max(2, fast_ring_slots(in));   // W readiness needs R >= 2
       a.shared_tab = (!sc->inst_of && in->n == 1) ? 1 : 0;
-      const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0, 2);
+      const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0, 2, tl);
       const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;
       const size_t smem = ((size_t)L.hdr + (size_t)wpb * L.per_warp) * 4;
       if (smem <= kMaxSmemPerBlock) {
-        int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(CP_PATTERN_UD, threads, smem), wpb);
+        int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(CP_PATTERN_UD, threads, smem, tl), wpb);
         if (const char* v = std::getenv("CP_CHUNKF_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
         const long long need = (n + wpb - 1) / wpb;
         const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
         a.work_counter = std::getenv("CP_CHUNKF_STATIC") ? nullptr : reinterpret_cast<int32_t*>(base + 128);
-        if (cpk::launch_chunkf(CP_PATTERN_UD, false, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
+        if (cpk::launch_chunkf(CP_PATTERN_UD, tl, a, blocks, threads, smem, stream) != cudaSuccess) return CP_ECUDA;
         a.work_counter = nullptr;
         first_done = true;
       }
@@ -461,7 +462,7 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
     const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;
     const size_t smem = ((size_t)L.hdr + (size_t)wpb * L.per_warp) * 4;
     if (smem <= kMaxSmemPerBlock) {
-      int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(sc->pattern, threads, smem), wpb);
+      int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(sc->pattern, threads, smem, tl), wpb);
       if (const char* v = std::getenv("CP_CHUNKF_BPS")) bps = std::max(1, std::min(bps, std::atoi(v)));   // experiments
       const long long need = (n + wpb - 1) / wpb;
       const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)sms * bps));

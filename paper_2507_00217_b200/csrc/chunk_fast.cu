@@ -55,6 +55,14 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
   return d;
 }
+// timeline staging: the 8 start ticks in the lane's slots [k][lane], k < 8, -> two 16-B global stores
+__device__ __forceinline__ void tl_flush8(unsigned stg, int32_t* dst) {
+  int v[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v[k]) : "r"(stg + 128u * k));
+  __stcs(reinterpret_cast<int4*>(dst), make_int4(v[0], v[1], v[2], v[3]));
+  __stcs(reinterpret_cast<int4*>(dst) + 1, make_int4(v[4], v[5], v[6], v[7]));
+}
 // 8 selector bytes (source byte index in the top nibble, 0xF below) -> two registers
 __device__ __forceinline__ void pack_sel(const int (&ix)[8], uint32_t& lo, uint32_t& hi) {
   lo = hi = 0;
@@ -145,7 +153,8 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
   extern __shared__ __align__(128) int32_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, s = lane;
   const int R = A.ring_slots, Rm = R - 1, PW = A.words;
-  const ChunkFLayout Ly = chunkf_layout(R, PW, A.shared_tab != 0, kRings);
+  constexpr bool kStage = kTL && kUD;             // UD timelines: staged, written 8 ticks (32 B) per lane
+  const ChunkFLayout Ly = chunkf_layout(R, PW, A.shared_tab != 0, kRings, kStage);
   const int wbase = Ly.hdr + wib * Ly.per_warp;
   const int tbase = A.shared_tab ? 0 : wbase + Ly.tab;
   const unsigned sb = smem_u32(smem), wb = sb + 4u * (unsigned)wbase;
@@ -292,6 +301,8 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
     const unsigned iPb = wb + 4u * (unsigned)(Ly.plan + lane);
     const int R24 = R << 24, Rm7 = Rm << 7, lk_off_r = 4 * (Ly.lk + lane);
     int32_t* const trow = kTL ? A.t_start + (item * A.stage_stride + s) * (long long)A.len_stride : nullptr;
+    const unsigned stg = wb + 4u * (unsigned)(Ly.stage + lane);   // staging slot [0][lane]
+    int rr = 0, fg = 0;                              // (staged timeline) round counter, next group to write
     uint32_t wv;
     asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(iPb));
     for (;;) {
@@ -333,7 +344,10 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
         lkR = (snd & isF) ? nl : lkR;
         lkL = (snd & !isF) ? nl : lkL;
       }
-      if (kTL && go && pos4 / kStep < A.len_stride) trow[pos4 / kStep] = start;
+      if (kStage)   // start tick of entry pos4 / 2 into staging slot (entry & 15), predicated, no branch
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %2, 0;\n\t@q st.shared.b32 [%0], %1;\n\t}"
+                     :: "r"(stg + (((unsigned)pos4 & 30u) << 6)), "r"(start), "r"((int)go) : "memory");
+      else if (kTL && go && pos4 / kStep < A.len_stride) trow[pos4 / kStep] = start;
       const int gi = go ? 1 : 0;
       clk = cmadd(gi, end - clk, clk);
       mem = cmadd(gi, t0.y, mem);
@@ -344,9 +358,17 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
       unsigned wa;
       asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(wa) : "r"((unsigned)pos4 & ~31u), "r"(iPb));
       asm volatile("ld.shared.b32 %0, [%1];" : "=r"(wv) : "r"(wa));
+      if (kStage && (++rr & 7) == 0 && (pos4 >> 4) > fg) {
+        // warp-uniform every 8th round: a lane advances <= 8 entries in 8 rounds, so at most one aligned
+        // group of 8 has completed since the last flush and the 16-slot ring still holds it
+        tl_flush8(stg + ((unsigned)(fg & 1) << 10), trow + 8 * fg);
+        ++fg;
+      }
       __syncwarp();
       if (!__any_sync(FMASK, go)) break;
     }
+    if (kStage)                                     // entries not yet written (< 16)
+      for (int k = 8 * fg; k < pos4 / kStep; ++k) trow[k] = smem[wbase + Ly.stage + ((k & 15) << 5) + lane];
     const int pos = pos4 / kStep;
     // completed, with Q29's counts: F, D + B of each chunk m (c), as many W as D per chunk (deficit
     // bytes back at 128), B and D not mixed on a stage (#B, byte 2 of w, is 0 or kChunks m)
@@ -418,8 +440,8 @@ int launch_chunkf(int pattern, bool timeline, const Args& a, int blocks, int thr
   return (int)cudaLaunchKernel(fn, dim3(blocks), dim3(threads), params, smem, (cudaStream_t)stream);
 }
 
-int chunkf_blocks_per_sm(int pattern, int threads, size_t smem) {
-  const void* fn = chunkf_fn(pattern, false);
+int chunkf_blocks_per_sm(int pattern, int threads, size_t smem, bool timeline) {
+  const void* fn = chunkf_fn(pattern, timeline);
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) return 1;

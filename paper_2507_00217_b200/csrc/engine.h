@@ -155,9 +155,10 @@ constexpr int kChunkFTabWords = 2 * 8 * 32 * 4 + 8 * 4;
 constexpr int kChunkFThreads = 128;
 constexpr int kChunkFMinBlocks = 5;
 struct ChunkFLayout {
-  int hdr, bars, zero, zrows, lk, rings, plan, tab, per_warp;
+  int hdr, bars, zero, zrows, lk, rings, plan, stage, tab, per_warp;
 };
-__host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool shared_tab, int rings) {
+// timeline (UD): a [16][32] staging ring of start ticks after the plan rows
+__host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool shared_tab, int rings, bool timeline = false) {
   ChunkFLayout L;
   L.hdr = shared_tab ? kChunkFTabWords : 0;
   L.bars = 0;
@@ -167,13 +168,15 @@ __host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool sha
   L.lk = R >= 4 ? L.zero + 32 : L.zero + R * 32;
   L.plan = L.zero + L.zrows * 32;
   int w = L.plan + (words + 1) * 32;
+  L.stage = w;
+  if (timeline) w += 16 * 32;
   L.tab = shared_tab ? -1 : w;
   if (!shared_tab) w += kChunkFTabWords;
   L.per_warp = w;
   return L;
 }
 int launch_chunkf(int pattern, bool timeline, const Args& a, int blocks, int threads, size_t smem, void* stream);
-int chunkf_blocks_per_sm(int pattern, int threads, size_t smem);
+int chunkf_blocks_per_sm(int pattern, int threads, size_t smem, bool timeline = false);
 // the sweep's static candidates (GPipe / 1F1B / ZB-H1) on k_chunk32f<UD, grid>: plans from a library
 // of [3 kinds][n_pp][n_mb] plans of `words` words built per sweep call (k_plan_library)
 struct PlanLibDims {
