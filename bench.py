@@ -463,7 +463,7 @@ def run_ours(args):
                     "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                                  "frac": ach / hbm_peak, "traffic": traffic_per_launch("simulate_timeline_bytes_per_launch"),
                                  "peak_source": peak_src, "bytes_per_eval": tl_bytes,
-                                 "kernel": "k_sim32<timeline> (start ticks staged in smem, 32 B per lane store)"}}
+                                 "kernel": "k_chunk32f<UD, timeline> (start ticks staged in smem, 32 B per lane store)"}}
         del tl_out, r_tl
         torch.cuda.empty_cache()
 
