@@ -368,10 +368,12 @@ size_t plan_lib_bytes(const cp_grid* g) {
   return sweep_static_fast(g) ? align256(64 + (size_t)3 * g->n_pp_n * g->n_mb_n * plan_lib_words(g) * 32 * 4) : 0;
 }
 
+// Task counters of the long-task greedy launches (3 ring tiers per p-class), after the plan library.
+constexpr size_t kLongCtrBytes = 256;
 size_t sweep_ws_bytes(const cp_grid* g) {
   size_t b = kCtrlBytes;
   for (int ip = 0; ip < g->n_pp_n; ++ip) b += sweep_class_ring_bytes(g, ip);
-  return b + plan_lib_bytes(g);
+  return b + plan_lib_bytes(g) + kLongCtrBytes;
 }
 
 long long point_cost(const cp_grid* g, int i_pp, int i_mb) {
@@ -589,6 +591,10 @@ int32_t cp_greedy(const cp_instances* in, const cp_schedules* out, const cp_resu
 // The streams and events are created once per device and reused by later calls (a call that finds
 // the pool in use by another host thread creates its own and destroys them at the join).
 constexpr int kForkMax = 40;
+// Launches take one of three stream-priority bands (0 = the device's greatest priority, 2 = the
+// least): when SM resources free up, the block scheduler hands them to pending blocks of the
+// higher band first.  The pool holds kForkBand streams per band.
+constexpr int kForkBand = kForkMax / 3;
 struct ForkPool {
   std::mutex mu;
   int dev = -1;
@@ -597,14 +603,21 @@ struct ForkPool {
 };
 ForkPool g_fork_pool;
 
+inline int band_priority(int band) {
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  return band == 0 ? greatest : (band == 1 ? (least + greatest) / 2 : least);
+}
+
 struct Forker {
   cudaStream_t parent;
   std::unique_lock<std::mutex> lk;
   bool pooled = false;
   cudaEvent_t fork = nullptr, joins[kForkMax] = {};
   cudaStream_t sub[kForkMax] = {};
-  int n = 0;
-  bool used_parent = false;
+  int used[3] = {0, 0, 0}, n = 0;                  // pooled: per band; own streams: n
+  int own[kForkMax] = {};                          // own streams: indices in use
+  bool used_parent = false, forked = false;
   explicit Forker(cudaStream_t p) : parent(p), lk(g_fork_pool.mu, std::try_to_lock) {
     int dev = -1;
     cudaGetDevice(&dev);
@@ -614,7 +627,7 @@ struct Forker {
         g_fork_pool.dev = dev;
         cudaEventCreateWithFlags(&g_fork_pool.fork, cudaEventDisableTiming);
         for (int i = 0; i < kForkMax; ++i) {
-          cudaStreamCreateWithFlags(&g_fork_pool.sub[i], cudaStreamNonBlocking);
+          cudaStreamCreateWithPriority(&g_fork_pool.sub[i], cudaStreamNonBlocking, band_priority(std::min(2, i / kForkBand)));
           cudaEventCreateWithFlags(&g_fork_pool.joins[i], cudaEventDisableTiming);
         }
       }
@@ -623,39 +636,58 @@ struct Forker {
     }
   }
   ~Forker() { join(); }
-  // the first launch runs on the parent itself (a single-launch call forks nothing); the fork point
-  // is recorded before it, so later launches do not wait for it
-  cudaStream_t next() {
-    if (!used_parent) {
-      if (!fork && cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return parent;
-      cudaEventRecord(fork, parent);
+  // The fork point is recorded before the first launch, so no launch waits for another.  The first
+  // band-2 launch runs on the parent itself (a single-launch call forks nothing).
+  bool record_fork() {
+    if (forked) return true;
+    if (!fork && cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess) return false;
+    cudaEventRecord(fork, parent);
+    forked = true;
+    return true;
+  }
+  cudaStream_t next(int band = 2) {
+    if (!record_fork()) return parent;
+    if (band == 2 && !used_parent) {
       used_parent = true;
       return parent;
     }
-    if (n == kForkMax) return parent;
-    if (!pooled) {
-      if (cudaStreamCreateWithFlags(&sub[n], cudaStreamNonBlocking) != cudaSuccess) return parent;
-      if (cudaEventCreateWithFlags(&joins[n], cudaEventDisableTiming) != cudaSuccess) {
-        cudaStreamDestroy(sub[n]);
+    int i;
+    if (pooled) {
+      const int lim = band == 2 ? kForkMax - 2 * kForkBand : kForkBand;
+      if (used[band] == lim) return parent;
+      i = band * kForkBand + used[band]++;
+    } else {
+      if (n == kForkMax) return parent;
+      i = n;
+      if (cudaStreamCreateWithPriority(&sub[i], cudaStreamNonBlocking, band_priority(band)) != cudaSuccess) return parent;
+      if (cudaEventCreateWithFlags(&joins[i], cudaEventDisableTiming) != cudaSuccess) {
+        cudaStreamDestroy(sub[i]);
         return parent;
       }
+      own[n++] = i;
     }
-    cudaStreamWaitEvent(sub[n], fork, 0);
-    return sub[n++];
+    cudaStreamWaitEvent(sub[i], fork, 0);
+    return sub[i];
   }
   void join() {
-    for (int i = 0; i < n; ++i) {
+    auto join_one = [&](int i) {
       cudaEventRecord(joins[i], sub[i]);
       cudaStreamWaitEvent(parent, joins[i], 0);
       if (!pooled) {
         cudaEventDestroy(joins[i]);
         cudaStreamDestroy(sub[i]);
       }
+    };
+    if (pooled) {
+      for (int b = 0; b < 3; ++b)
+        for (int k = 0; k < used[b]; ++k) join_one(b * kForkBand + k);
+    } else {
+      for (int k = 0; k < n; ++k) join_one(own[k]);
     }
     if (!pooled && fork) cudaEventDestroy(fork);
-    n = 0;
+    used[0] = used[1] = used[2] = n = 0;
     fork = pooled ? fork : nullptr;
-    used_parent = false;
+    used_parent = forked = false;
   }
 };
 
@@ -699,16 +731,45 @@ static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_l
   // they are enqueued first and take the SMs before the cheaper classes fill them
   for (int ip = g->n_pp_n - 1; ip >= 0; --ip)
     if (blocked || std::max<long long>(lo, ip * per_pp) < std::min<long long>(hi, (ip + 1) * per_pp)) cls[ncls++] = ip;
+  // The longest tasks are the greedy candidates at the largest n_mb (up to ~2,700 rounds at p = 32,
+  // m = 128, n_sub = 4): a rank shard cannot end before they do, so they must start at once.  In a
+  // proper part of the grid (a shard of a multi-GPU sweep) the trailing mb blocks with
+  // n_mb >= max / CP_SWEEP_LONG_DIV (default 1: the largest) go to launches of their own --
+  // enqueued first on high-priority streams, the largest p first -- and the other points to the
+  // launches below.  The whole grid on one GPU is throughput-bound: there the split costs ~3%.
+  int mb_max = 0;
+  for (int i = 0; i < g->n_mb_n; ++i) mb_max = std::max(mb_max, g->n_mb_vals[i]);
+  int kcut = g->n_mb_n;                          // first mb block of the long part
+  const char* ldv = std::getenv("CP_SWEEP_LONG_DIV");
+  const int long_div = ldv ? std::max(1, std::atoi(ldv)) : 1;
+  while (kcut > 0 && long_div * g->n_mb_vals[kcut - 1] >= mb_max) --kcut;
+  const bool partial = blocked ? (long long)(own_hi - own_lo) < inner : hi - lo < np;
+  const bool split_long = partial && kcut > 0 && kcut < g->n_mb_n && !getenv_nofast() && !std::getenv("CP_SWEEP_NO_LONG");
+  unsigned long long* long_counters =
+      reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + sweep_ws_bytes(g) - kLongCtrBytes);
+  if (split_long && cudaMemsetAsync(long_counters, 0, kLongCtrBytes, st) != cudaSuccess) return CP_ECUDA;
   // every launch (greedy tier or static-candidate engine pass) gets its own stream forked from, and
   // joined back to, the caller's: a launch ends on its longest task, so launches that queue behind
   // each other would add those tails up
   Forker fk(st);
-  for (int c = 0; c < ncls; ++c) {
-    const int ip = cls[c];
-    // this class's point set: its points within [lo, hi), or its blocks with the owned slice
-    const long long a0 = blocked ? (long long)ip * g->n_mb_n : std::max<long long>(lo, ip * per_pp);
-    const long long a1 = blocked ? (long long)(ip + 1) * g->n_mb_n : std::min<long long>(hi, (ip + 1) * per_pp);
-    const long long npts = blocked ? (a1 - a0) * (long long)(own_hi - own_lo) : a1 - a0;
+  // this class's point set [a0, a1) (points, or mb blocks with the owned slice when blocked) and
+  // its size; part 0 = all, 1 = mb blocks [kcut, n_mb) only, 2 = blocks [0, kcut)
+  auto class_set = [&](int ip, int part, long long& a0, long long& a1) -> long long {
+    if (blocked) {
+      a0 = (long long)ip * g->n_mb_n;
+      a1 = (long long)(ip + 1) * g->n_mb_n;
+      if (part == 1) a0 += kcut;
+      if (part == 2) a1 = a0 + kcut;
+      return (a1 - a0) * (long long)(own_hi - own_lo);
+    }
+    a0 = std::max<long long>(lo, ip * per_pp);
+    a1 = std::min<long long>(hi, (ip + 1) * per_pp);
+    const long long cut = std::min(a1, std::max(a0, ip * per_pp + (long long)kcut * inner));
+    if (part == 1) a0 = cut;
+    if (part == 2) a1 = cut;
+    return std::max(0LL, a1 - a0);
+  };
+  auto base_args = [&](long long a0, long long a1) {
     cpk::Args a;
     std::memset(&a, 0, sizeof(a));
     a.grid = *g;
@@ -719,43 +780,79 @@ static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_l
     a.own_hi = own_hi;
     a.keys = ukeys;
     a.cand_ms = cand_ms;
+    return a;
+  };
+  // greedy candidates (n_sub 1/2/4): k_greedy_fast on synthesized instances, rings sized to the
+  // lead bound (rounded to a power of two) so they cannot fill.  Ring size sets residency, so
+  // tasks whose own bound is <= 32 run in a launch with 32-slot rings and only the rest in one
+  // sized to the class maximum.  Returns false if the class's rings do not fit shared memory.
+  const unsigned greedy_mask = g->cand_mask & 0x1cu;
+  // Stream priorities (Forker bands): the long-task launches first (band 0); then, across several
+  // p-classes, the greedy tiers (band 1: the longer tasks) ahead of the static and engine passes
+  // (band 2), which fill in around them (config 5 on one GPU: 5.35 -> 5.1 ms).  A single class
+  // keeps one band: there the static pass would only queue behind the greedy grid and add its
+  // tail (config 2: 0.25 -> 0.37 ms).
+  const int greedy_band = ncls > 1 ? 1 : 2;
+  const bool greedy_fast = greedy_mask && !getenv_nofast();
+  auto greedy_launches = [&](int ip, long long a0, long long a1, long long npts, unsigned long long* ctr,
+                             bool high) -> bool {
     const int p = g->n_pp_vals[ip];
-    // greedy candidates (n_sub 1/2/4): k_greedy_fast on synthesized instances, rings sized to the
-    // lead bound (rounded to a power of two) so they cannot fill.  Ring size sets residency, so
-    // tasks whose own bound is <= 32 run in a launch with 32-slot rings and only the rest in one
-    // sized to the class maximum.  Static candidates (GPipe, 1F1B) and anything the fast path
-    // cannot hold in shared memory: the generic engine.
+    const int Wd = p <= 8 ? 8 : (p <= 16 ? 16 : 32);
+    const int lead_max = sweep_ring_slots(g, p);
+    // tiers of lead bound: [0, 32], (32, 64], (64, lead_max]
+    const int edge[3] = {32, 64, CP_MAX_MB};
+    int ntier = 1;
+    while (ntier < 3 && lead_max > edge[ntier - 1]) ++ntier;
+    const size_t big_warp = (size_t)((cpk::kGreedyTableWords + 2 * (1 << lg2_ceil(lead_max)) * 32 + 3) & ~3) * 4;
+    if (big_warp > kMaxSmemPerBlock) return false;
+    // the tier holding the largest leads (and the longest tasks: m up to 128 with large budgets) is
+    // launched first, so its tasks start at once instead of queueing behind the persistent grids of
+    // the short tiers (measured on one 1/8 rank shard of config 5: the last-enqueued long tier ended
+    // the shard)
+    for (int tier = ntier - 1; tier >= 0; --tier) {
+      cpk::Args ag = base_args(a0, a1);
+      ag.grid.cand_mask = greedy_mask;
+      ag.sweep_counter = ctr + tier;
+      ag.tier_lo = tier == 0 ? 0 : edge[tier - 1] + 1;
+      ag.tier_hi = tier == ntier - 1 ? CP_MAX_MB : edge[tier];
+      ag.ring_slots = 1 << lg2_ceil(std::min(lead_max, ag.tier_hi));
+      ag.smem_words_per_warp = (cpk::kGreedyTableWords + 2 * ag.ring_slots * 32 + 3) & ~3;
+      const size_t per_warp = (size_t)ag.smem_words_per_warp * 4;
+      const int wpb = per_warp * 2 <= kMaxSmemPerBlock ? 2 : 1, threads = 32 * wpb;
+      const size_t smem = per_warp * wpb;
+      const int bps = cpk::greedy_fast_blocks_per_sm(Wd, true, threads, smem);
+      const long long segs = (long long)(32 / Wd) * wpb;
+      const long long need = (npts * __builtin_popcount(greedy_mask) + segs - 1) / segs;
+      const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
+      if (cpk::launch_greedy_fast(Wd, true, ag, blocks, threads, smem, fk.next(high ? 0 : greedy_band)) != cudaSuccess)
+        rc = CP_ECUDA;
+    }
+    return true;
+  };
+  bool long_done[8] = {};
+  if (split_long && greedy_fast)
+    for (int c = 0; c < ncls && !rc; ++c) {
+      long long a0, a1;
+      const long long npts = class_set(cls[c], 1, a0, a1);
+      if (npts > 0) long_done[c] = greedy_launches(cls[c], a0, a1, npts, long_counters + 3 * c, true);
+    }
+  for (int c = 0; c < ncls && !rc; ++c) {
+    const int ip = cls[c];
+    long long a0, a1;
+    const long long npts = class_set(ip, 0, a0, a1);
+    cpk::Args a = base_args(a0, a1);
+    const int p = g->n_pp_vals[ip];
+    // Static candidates (GPipe, 1F1B) and anything the fast path cannot hold in shared memory: the
+    // generic engine.
     unsigned engine_mask = g->cand_mask & ((1u << CP_N_CAND) - 1u);
-    const unsigned greedy_mask = engine_mask & 0x1cu;
-    if (greedy_mask && !getenv_nofast()) {
-      const int Wd = p <= 8 ? 8 : (p <= 16 ? 16 : 32);
-      const int lead_max = sweep_ring_slots(g, p);
-      // tiers of lead bound: [0, 32], (32, 64], (64, lead_max]
-      const int edge[3] = {32, 64, CP_MAX_MB};
-      int ntier = 1;
-      while (ntier < 3 && lead_max > edge[ntier - 1]) ++ntier;
-      const size_t big_warp = (size_t)((cpk::kGreedyTableWords + 2 * (1 << lg2_ceil(lead_max)) * 32 + 3) & ~3) * 4;
-      bool ok = big_warp <= kMaxSmemPerBlock;
-      // the tier holding the largest leads (and the longest tasks: m up to 128 with large budgets) is
-      // launched first, so its tasks start at once instead of queueing behind the persistent grids of
-      // the short tiers (measured on one 1/8 rank shard of config 5: the last-enqueued long tier ended
-      // the shard)
-      for (int tier = ntier - 1; tier >= 0 && ok; --tier) {
-        cpk::Args ag = a;
-        ag.grid.cand_mask = greedy_mask;
-        ag.sweep_counter = counters + 4 * c + 1 + tier;
-        ag.tier_lo = tier == 0 ? 0 : edge[tier - 1] + 1;
-        ag.tier_hi = tier == ntier - 1 ? CP_MAX_MB : edge[tier];
-        ag.ring_slots = 1 << lg2_ceil(std::min(lead_max, ag.tier_hi));
-        ag.smem_words_per_warp = (cpk::kGreedyTableWords + 2 * ag.ring_slots * 32 + 3) & ~3;
-        const size_t per_warp = (size_t)ag.smem_words_per_warp * 4;
-        const int wpb = per_warp * 2 <= kMaxSmemPerBlock ? 2 : 1, threads = 32 * wpb;
-        const size_t smem = per_warp * wpb;
-        const int bps = cpk::greedy_fast_blocks_per_sm(Wd, true, threads, smem);
-        const long long segs = (long long)(32 / Wd) * wpb;
-        const long long need = (npts * __builtin_popcount(greedy_mask) + segs - 1) / segs;
-        const int blocks = (int)std::max(1LL, std::min<long long>(need, (long long)cpk::device_sm_count() * bps));
-        if (cpk::launch_greedy_fast(Wd, true, ag, blocks, threads, smem, fk.next()) != cudaSuccess) rc = CP_ECUDA;
+    if (greedy_fast) {
+      bool ok = true;
+      if (long_done[c]) {
+        long long b0, b1;
+        const long long nrest = class_set(ip, 2, b0, b1);
+        if (nrest > 0) ok = greedy_launches(ip, b0, b1, nrest, counters + 4 * c + 1, false);
+      } else {
+        ok = greedy_launches(ip, a0, a1, npts, counters + 4 * c + 1, false);
       }
       if (ok) engine_mask &= ~greedy_mask;
     }
@@ -793,7 +890,6 @@ static int32_t sweep_run(const cp_grid* g, long long lo, long long hi, int own_l
         rc = launch_pass(cpk::MODE_SWEEP, true, a, npts * __builtin_popcount(engine_mask), 32 >> a.seg_lg, es);
       }
     }
-    if (rc) break;
   }
   fk.join();
   if (rc) return rc;

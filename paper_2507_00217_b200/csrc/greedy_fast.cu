@@ -15,6 +15,13 @@
 #include "engine.h"
 #include "grid_synth.cuh"
 
+// Debug builds only (make variant V=... DEFS=-DGREEDY_DBG_ROUNDS=N; tools/greedy_rounds.py,
+// greedy_task_times.py, greedy_task_starts.py): a sweep task's cand_ms gets, instead of its
+// makespan, 1 = its round count, 2 = its duration (0.1 us), 3 = its start time (globaltimer / 100).
+#ifndef GREEDY_DBG_ROUNDS
+#define GREEDY_DBG_ROUNDS 0
+#endif
+
 namespace cpk {
 
 namespace {
@@ -88,6 +95,10 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
   long long item = -1;
   int cand = 0;                                        // sweep: candidate id (2/3/4 = greedy n_sub 1/2/4)
   bool need = true, done = false;
+#if GREEDY_DBG_ROUNDS
+  int dbg_rounds = 0;
+  unsigned long long dbg_t0 = 0;
+#endif
 
   for (;;) {
     // ------------------------------------------------------------------ rare: (re)load instances
@@ -154,6 +165,10 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
           sendD = s > 0 && s < p;
           clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = pos = last_fd = 0;
           emitw = 0;
+#if GREEDY_DBG_ROUNDS
+          dbg_rounds = 0;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
+#endif
           // the last stage's D ring may hold a larger instance's arrivals: it must read 0
           if (lastS && s < W - 1)
             for (int k = 0; k < R; ++k) smem[iD + (k << 5)] = 0;
@@ -220,6 +235,9 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
     const bool onS = hasItem && s < p;
     for (;;) {
       __syncwarp();                                        // last round's ring stores -> these reads
+#if GREEDY_DBG_ROUNDS
+      ++dbg_rounds;
+#endif
 
       // ------------------------------------------------------------------ one round
       const bool live = onS & (nW < m);
@@ -237,11 +255,15 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s.
       // Width-W shuffles return the lane's own value past the segment edge, so the scans need no
       // lane predicates (min with itself).
+      // Radix-3 steps (two shuffles, one 3-input min each; ceil(log3 W) steps): fewer ALU-pipe mins
+      // than log2 W min steps and a shorter dependency chain.
       int x = tstar - P, y = tstar + Q;
   #pragma unroll
-      for (int d = 1; d < W; d <<= 1) {
-        x = gmin(x, __shfl_up_sync(GFULL, x, d, W));
-        y = gmin(y, __shfl_down_sync(GFULL, y, d, W));
+      for (int d = 1; d < W; d *= 3) {
+        const int a1 = __shfl_up_sync(GFULL, x, d, W), a2 = __shfl_up_sync(GFULL, x, 2 * d, W);
+        const int b1 = __shfl_down_sync(GFULL, y, d, W), b2 = __shfl_down_sync(GFULL, y, 2 * d, W);
+        x = gmin(gmin(x, a1), a2);
+        y = gmin(gmin(y, b1), b2);
       }
       const int xe = __shfl_up_sync(GFULL, x, 1, W);
       const int ye = __shfl_down_sync(GFULL, y, 1, W);
@@ -319,7 +341,14 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
             if (s == 0) {
               if (!complete) atomicMin(A.keys + item, KEY_OVER);
               else if (!(b_mem & segmask)) {
+#if GREEDY_DBG_ROUNDS
+                unsigned long long t1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                if (A.cand_ms) A.cand_ms[item * CP_N_CAND + cand] = GREEDY_DBG_ROUNDS == 2 ? (int)((t1 - dbg_t0) / 100)
+                                 : GREEDY_DBG_ROUNDS == 3 ? (int)((dbg_t0 / 100) & 0x3fffffff) : dbg_rounds;
+#else
                 if (A.cand_ms) A.cand_ms[item * CP_N_CAND + cand] = ms;
+#endif
                 atomicMin(A.keys + item, ((unsigned long long)ms << 8) | (unsigned)cand);
               }
             }

@@ -209,12 +209,13 @@ def test_sweep_workspace_covers_global_rings():
     """A grid whose in-flight bound min(m, M_L / m_f) exceeds what one block's shared memory holds
     gets global-memory rings per p-class in the sweep workspace (cp_workspace_bytes(2, grid)).
     Grids with static candidates and n_mb <= 255 also hold the per-call plan library: 64 B of task
-    counters, then 3 kinds x n_pp x n_mb plans of ceil(3 max_m / 16) words x 32 rows (256-B aligned)."""
+    counters, then 3 kinds x n_pp x n_mb plans of ceil(3 max_m / 16) words x 32 rows (256-B aligned);
+    every sweep workspace ends with 256 B of task counters for the long-task launches."""
     lib = cp._lib.load()
     small = cp.api.to_cp_grid(_grid())
     words = (3 * 8 + 15) // 16
     lib_bytes = (64 + 3 * 1 * 1 * words * 32 * 4 + 255) // 256 * 256
-    assert lib.cp_workspace_bytes(2, C.byref(small), 0) == 256 + lib_bytes
+    assert lib.cp_workspace_bytes(2, C.byref(small), 0) == 256 + lib_bytes + 256
     big = cp.api.to_cp_grid(_grid(pp=(2, 4), mb=(1024,), mlim=(600000,)))
     nb = lib.cp_workspace_bytes(2, C.byref(big), 0)
     assert nb >= 256 + 2 * 148 * 4 * 2 * 1024 * 32 * 4, nb
