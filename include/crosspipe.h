@@ -193,9 +193,13 @@ int32_t cp_greedy(const cp_instances* inst, const cp_schedules* out, const cp_re
  * (the caller fills the rest with INT64_MAX; cp_sweep in python = fill + shard + all_reduce(MIN)).
  * Work is (point, candidate) tasks taken from a device counter (most expensive first) and combined
  * with a 64-bit atomicMin per point; p-classes run concurrently on streams forked from `stream`
- * and joined back to it.  ws: cp_workspace_bytes(2, grid, 0) bytes (256 B of task counters, plus
- * global-memory arrival rings for any p-class whose in-flight bound min(m, M_L/m_f) does not fit
- * one block's shared memory, about 900 microbatches).  Errors: CP_EINVAL for a malformed grid --
+ * and joined back to it (stream priorities: the largest-n_mb greedy tasks of a proper part of the
+ * grid first, then greedy before static candidates across p-classes).  ws: cp_workspace_bytes(2,
+ * grid, 0) bytes: 256 B of task counters; global-memory arrival rings for any p-class whose
+ * in-flight bound min(m, M_L/m_f) does not fit one block's shared memory (about 900 microbatches);
+ * for grids with static candidates and every n_mb <= 255, the per-call plan library (64 B of
+ * counters + 3 x n_pp x n_mb plans of ceil(3 max_m / 16) words x 32 rows, 256-B aligned); and
+ * 256 B of counters for the long-task launches.  Errors: CP_EINVAL for a malformed grid --
  * axis sizes, negative axis values, or any point whose synthesized instance violates the record
  * invariants (e.g. a p beyond the base record's stages, M_L < m_f or beyond int32) --,
  * CP_EUNSUPPORTED (p > 32, m > 1024), CP_EWORKSPACE, CP_ECUDA.
