@@ -124,6 +124,7 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
         need = false;
         fresh = item >= 0;
         p = m = 0;
+        if (!fresh) { mlim = -1; nF = nD = nW = lmF = 0; }   // no instance: nothing eligible (see the round)
         if (fresh) {
           bool zero1;
           tf = td = tw = mf = md = mw = mlim = tdp = tag = latF = bwF = latB = bwB = 0;
@@ -153,13 +154,13 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
                     (long long)mf + md + mw == 0 && mlim >= mf && tdp >= 0 && tag >= 0 && latF >= 0 &&
                     bwF >= 0 && lat_b_s >= 0 && bw_b_s >= 0);
           if (!zero1) tag = 0;
+          if (s >= p) mlim = -1;                // lanes past the last stage: no F can fit (see the round)
           st0 = bad ? CPI_BAD_INSTANCE : 0;
           if (!kGrid && !st0 && (long long)(2 + nsub) * m > 16LL * A.words) st0 = CPI_BAD_PLAN;
           if (!st0 && (p > W || m > CP_MAX_MB || nsub > CP_MAX_SUB)) st0 = CPI_OVERFLOW;
           wq = tw / (nsub > 0 ? nsub : 1);
           wr = tw % (nsub > 0 ? nsub : 1);
-          lmF = s == 0 ? 0x7fff : 0;            // stage 0 has no F producer: always available
-          asm("mov.b32 %0, %0;" : "+r"(lmF));   // opaque: (x | m) stays one LOP3
+          lmF = s == 0 ? m : 0;                 // stage 0 has no F producer: all m available
           lastS = s == p - 1;
           sendF = s < p - 1;
           sendD = s > 0 && s < p;
@@ -240,16 +241,18 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
 #endif
 
       // ------------------------------------------------------------------ one round
-      const bool live = onS & (nW < m);
-      const int leftF = __shfl_up_sync(GFULL, nF, 1, W) | lmF;
+      // Eligibility without a liveness term: F needs leftF > nF, and leftF <= m (stage 0: leftF = m);
+      // D needs rightD > nD with rightD <= m; W needs nW < nD <= m.  Lanes past the last stage (and
+      // segments without an instance) hold m_lim = -1, so their F never fits, and no D / W counts.
+      const int leftF = gmax(__shfl_up_sync(GFULL, nF, 1, W), lmF);
       const int rD0 = __shfl_down_sync(GFULL, nD, 1, W);
       const int rightD = lastS ? nF : rD0;                // the last stage's D follows its own F
       const int adF = iF + ((nF & Rm) << 5), adD = iD + ((nD & Rm) << 5);   // ring heads
       const int availF = gmax(smem[adF], tag);
       const int availD = smem[adD];
-      const bool hasF = live & (nF < m) & (leftF > nF) & (mem + mf <= mlim);   // Q15
-      const bool hasD = live & (nD < m) & (rightD > nD);
-      const bool hasW = live & (nW < nD);
+      const bool hasF = (leftF > nF) & (mem + mf <= mlim);   // Q15
+      const bool hasD = rightD > nD;
+      const bool hasW = nW < nD;
       const int mnv = gmin(gmin(hasF ? availF : GINF, hasD ? availD : GINF), hasW ? clk : GINF);
       const int tstar = gmax(clk, mnv);                   // §4.2.2 :419 (GINF when nothing is eligible)
       // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s.
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       const unsigned bgo = __ballot_sync(GFULL, go);
       const bool idle = hasItem && !(bgo & segmask);
       if (__any_sync(GFULL, idle)) {
-        const unsigned b_unfin = __ballot_sync(GFULL, live);
+        const unsigned b_unfin = __ballot_sync(GFULL, onS && nW < m);
         const unsigned b_ring = __ballot_sync(GFULL, item >= 0 && s < p && nF < m && nF - nD >= R);
         const unsigned b_mem = __ballot_sync(GFULL, item >= 0 && s < p && peak > mlim);
         const bool complete = idle && !(b_unfin & segmask);
