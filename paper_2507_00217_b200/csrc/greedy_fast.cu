@@ -83,10 +83,11 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
   // per-lane instance constants
   int p = 0, m = 0, nsub = 1, tf = 0, td = 0, tw = 0, wq = 0, wr = 0, mf = 0, md = 0, mw = 0, mlim = 0;
   int tdp = 0, tag = 0, latF = 0, bwF = 0, latB = 0, bwB = 0, P = 0, Q = 0, lmF = 0;
+  int PL = 0, QR = 0;                                  // horizon offsets (P, Q; +-GINF at the segment edges)
   bool sendF = false, sendD = false, lastS = false;
   // per-lane state
   int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0;
-  int linkF = 0, linkB = 0, pos = 0, last_fd = 0;
+  int linkF = 0, linkB = 0, pos = 0, lastF = 0;       // lastF: the last full F/D block was an F
   uint32_t emitw = 0;
   // (out of line: inlined, this rare-path code changed the round's register allocation)
   auto finish_rows = [&](long long it, int used, bool stats_own) {
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
           lastS = s == p - 1;
           sendF = s < p - 1;
           sendD = s > 0 && s < p;
-          clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = pos = last_fd = 0;
+          clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = pos = lastF = 0;
           emitw = 0;
 #if GREEDY_DBG_ROUNDS
           dbg_rounds = 0;
@@ -212,6 +213,10 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       if (fresh) {
         P = pf - cf;
         Q = qd;
+        // At the segment edges the width-W shuffles return the lane's own scan value, so L_0 and
+        // R_{W-1} would come out as t*; offsetting them by GINF makes them exceed any t* < GINF.
+        PL = s == 0 ? P + GINF : P;
+        QR = s == W - 1 ? Q - GINF : Q;
         int st = (b_inst & segmask) ? CPI_BAD_INSTANCE
                  : (b_plan & segmask) ? CPI_BAD_PLAN
                  : (b_over & segmask) ? CPI_OVERFLOW : 0;
@@ -233,6 +238,8 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
     }                                                    // (failed items load again)
     if (done) break;
     const bool hasItem = item >= 0;                      // fixed until the next reload
+    unsigned segmaskH = hasItem ? segmask : 0u;          // this segment's lanes if it holds an instance
+    asm("mov.b32 %0, %0;" : "+r"(segmaskH));             // kept in a register (not re-derived per round)
     const bool onS = hasItem && s < p;
     for (;;) {
       __syncwarp();                                        // last round's ring stores -> these reads
@@ -270,11 +277,11 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       }
       const int xe = __shfl_up_sync(GFULL, x, 1, W);
       const int ye = __shfl_down_sync(GFULL, y, 1, W);
-      const int Lh = (s == 0) ? GINF : P + xe;
-      const int Rh = (s == W - 1) ? GINF : ye - Q;
+      const int Lh = PL + xe;                              // (lanes with t* = GINF cannot go: overflow is harmless)
+      const int Rh = ye - QR;
       // operation selection (Q13): opposite of the last full F/D block, then the other, then W
       const bool cF = hasF & (availF <= tstar), cD = hasD & (availD <= tstar);
-      const bool pD = cD & ((last_fd == 1) | !cF);
+      const bool pD = cD & ((lastF != 0) | !cF);
       const bool pF = !pD & cF;
       // an F whose consumer ring is full (lead would exceed R: undersized ring hint) is not executed:
       // the lane stalls and the item is re-run by the global-ring fix-up pass (decisions unchanged)
@@ -309,12 +316,12 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       nD = gmadd(gDi, 1, nD);
       wsub = gW ? (wfin ? 0 : wsub + 1) : wsub;
       nW = gmadd((gW & wfin) ? 1 : 0, 1, nW);
-      last_fd = gFi ? 1 : (gDi ? 2 : last_fd);
+      lastF = gmadd(lastF, gmadd(gFi, -1, gmadd(gDi, -1, 1)), gFi);   // F -> 1, D -> 0, else kept
       pos = gmadd(gi, 1, pos);
 
       // ------------------------------------------------------------------ rare: a segment went idle
       const unsigned bgo = __ballot_sync(GFULL, go);
-      const bool idle = hasItem && !(bgo & segmask);
+      const bool idle = (segmaskH != 0u) & ((bgo & segmaskH) == 0u);
       if (__any_sync(GFULL, idle)) {
         const unsigned b_unfin = __ballot_sync(GFULL, onS && nW < m);
         const unsigned b_ring = __ballot_sync(GFULL, item >= 0 && s < p && nF < m && nF - nD >= R);
