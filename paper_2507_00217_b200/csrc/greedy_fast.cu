@@ -84,7 +84,8 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
   int p = 0, m = 0, nsub = 1, tf = 0, td = 0, tw = 0, wq = 0, wr = 0, mf = 0, md = 0, mw = 0, mlim = 0;
   int tdp = 0, tag = 0, latF = 0, bwF = 0, latB = 0, bwB = 0, P = 0, Q = 0, lmF = 0;
   int PL = 0, QR = 0;                                  // horizon offsets (P, Q; +-GINF at the segment edges)
-  bool sendF = false, sendD = false, lastS = false;
+  bool lastS = false;
+  int offF = 1, offD = -1;                             // F / D send target relative to the ring head
   // per-lane state
   int clk = 0, mem = 0, peak = 0, nF = 0, nD = 0, nW = 0, wsub = 0;
   int linkF = 0, linkB = 0, pos = 0, lastF = 0;       // lastF: the last full F/D block was an F
@@ -163,16 +164,21 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
           wr = tw % (nsub > 0 ? nsub : 1);
           lmF = s == 0 ? m : 0;                 // stage 0 has no F producer: all m available
           lastS = s == p - 1;
-          sendF = s < p - 1;
-          sendD = s > 0 && s < p;
+          // Sends without a consumer need no test: stage 0's D goes into the D slot it has just
+          // consumed (message nD + R is sent only after this round: the ring bound nF - nD < R orders
+          // it after this op), the last stage's F into its own D ring at slot nF -- its D follows its
+          // own F, and the F's end (<= clk when that D is considered) reads like the cleared 0.
+          offF = lastS ? RW : 1;
+          offD = s == 0 ? 0 : -1;
           clk = mem = peak = nF = nD = nW = wsub = linkF = linkB = pos = lastF = 0;
           emitw = 0;
 #if GREEDY_DBG_ROUNDS
           dbg_rounds = 0;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dbg_t0));
 #endif
-          // the last stage's D ring may hold a larger instance's arrivals: it must read 0
-          if (lastS && s < W - 1)
+          // the last stage's D ring may hold a larger instance's arrivals or an earlier instance's F
+          // ends: it must read 0
+          if (lastS)
             for (int k = 0; k < R; ++k) smem[iD + (k << 5)] = 0;
           // parameter table: 0 = F, 1 = D (W sub-blocks are computed from wq, wr, m_w in the round)
           tab[0 * 32] = make_int4(tf, mf, bwF, latF);
@@ -295,17 +301,21 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       const int dmv = pW ? (wfin ? mw : 0) : ta.y;
       const int end = tstar + dur;
       const int nl = gmax(end, pF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
-      if (go & (pF ? sendF : (pD & sendD))) smem[pF ? adF + 1 : adD - 1] = nl + ta.w;
+      if (go & !pW) smem[pF ? adF + offF : adD + offD] = nl + ta.w;
       // emit the 2-bit entry into a shift register (the newest entry enters at bits 30-31, so after
       // 16 entries entry k sits at bits 2k); a full word goes straight to global memory
-      const uint32_t code = pF ? CP_OP_F : (pD ? CP_OP_D : CP_OP_W);
+      const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
       if (!kGrid) {
-        const uint32_t w1 = (emitw >> 2) | (code << 30);
+        // (integer multiply-adds: the FMA pipe has room, the ALU pipe binds)
+        // code << 30 = W - gFi (W - F) - gDi (W - D), valid when go
+        static_assert(CP_OP_F == 0u && CP_OP_D == 2u && CP_OP_W == 3u, "op codes");
+        const int code30 = gmadd(gFi, 0x40000000, gmadd(gDi, (int)0xC0000000u, (int)0xC0000000u));
+        uint32_t w1;                                       // (emitw >> 2) + code30 in one IMAD.HI
+        asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(w1) : "r"(emitw), "r"(0x40000000u), "r"(code30));
         const bool flush = go & ((pos & 15) == 15);
         if (flush) A.ops[(item * A.words + (pos >> 4)) * A.stage_stride + s] = w1;
-        emitw = go ? w1 : emitw;
+        emitw = (uint32_t)gmadd(gi, (int)(w1 - emitw), (int)emitw);
       }
-      const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
       const bool gW = go & pW;
       clk = gmadd(gi, end - clk, clk);
       mem = gmadd(gi, dmv, mem);
