@@ -264,9 +264,11 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       const int availF = gmax(smem[adF], tag);
       const int availD = smem[adD];
       const bool hasF = (leftF > nF) & (mem + mf <= mlim);   // Q15
-      const bool hasD = rightD > nD;
-      const bool hasW = nW < nD;
-      const int mnv = gmin(gmin(hasF ? availF : GINF, hasD ? availD : GINF), hasW ? clk : GINF);
+      // D / W: rightD >= nD and nD >= nW always, so max(n - bound + 1, 0) is 1 exactly when the op is
+      // not eligible, and a multiply-add lifts its time past GINF (times stay below 2^30)
+      const int fD = gmadd(gmax(nD - rightD + 1, 0), GINF, availD);
+      const int fW = gmadd(gmax(nW - nD + 1, 0), GINF, clk);
+      const int mnv = gmin(gmin(hasF ? availF : GINF, fD), fW);
       const int tstar = gmax(clk, mnv);                   // §4.2.2 :419 (GINF when nothing is eligible)
       // causal horizon: L_s = P_s + min_{k<s}(t*_k - P_k), R_s = min_{k>s}(t*_k + Q_k) - Q_s.
       // Width-W shuffles return the lane's own value past the segment edge, so the scans need no
@@ -286,7 +288,7 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       const int Lh = PL + xe;                              // (lanes with t* = GINF cannot go: overflow is harmless)
       const int Rh = ye - QR;
       // operation selection (Q13): opposite of the last full F/D block, then the other, then W
-      const bool cF = hasF & (availF <= tstar), cD = hasD & (availD <= tstar);
+      const bool cF = hasF & (availF <= tstar), cD = fD <= tstar;
       const bool pD = cD & ((lastF != 0) | !cF);
       const bool pF = !pD & cF;
       // an F whose consumer ring is full (lead would exceed R: undersized ring hint) is not executed:
