@@ -12,3 +12,6 @@ ncu --set full --clock-control none --import-source on -k regex:k_chunk32f -s 2 
     python tools/prof_sim.py sim 1000000 > gpurun_out/ncu_full_ud_$tag.log 2>&1; echo "ncu ud rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:k_chunk32f -s 2 -c 1 -f -o gpurun_out/chunkf_wave_$tag \
     python tools/prof_wave.py 200000 > gpurun_out/ncu_full_wave_$tag.log 2>&1; echo "ncu wave rc=$?"
+ncu --set full --clock-control none --import-source on -k regex:k_greedy_fast -s 2 -c 1 -f -o gpurun_out/greedy_c3_$tag \
+    python tools/prof_sim.py greedy 100000 > gpurun_out/ncu_full_greedy_$tag.log 2>&1; echo "ncu greedy rc=$?"
+python tools/shard8.py > gpurun_out/shard8_$tag.txt 2>&1; echo "shard8 rc=$?"
