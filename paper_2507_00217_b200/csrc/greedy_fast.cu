@@ -278,10 +278,15 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       int x = tstar - P, y = tstar + Q;
   #pragma unroll
       for (int d = 1; d < W; d *= 3) {
-        const int a1 = __shfl_up_sync(GFULL, x, d, W), a2 = __shfl_up_sync(GFULL, x, 2 * d, W);
-        const int b1 = __shfl_down_sync(GFULL, y, d, W), b2 = __shfl_down_sync(GFULL, y, 2 * d, W);
-        x = gmin(gmin(x, a1), a2);
-        y = gmin(gmin(y, b1), b2);
+        const int a1 = __shfl_up_sync(GFULL, x, d, W), b1 = __shfl_down_sync(GFULL, y, d, W);
+        if (2 * d < W) {                                   // (a shift of W or more returns x itself)
+          const int a2 = __shfl_up_sync(GFULL, x, 2 * d, W), b2 = __shfl_down_sync(GFULL, y, 2 * d, W);
+          x = gmin(gmin(x, a1), a2);
+          y = gmin(gmin(y, b1), b2);
+        } else {
+          x = gmin(x, a1);
+          y = gmin(y, b1);
+        }
       }
       const int xe = __shfl_up_sync(GFULL, x, 1, W);
       const int ye = __shfl_down_sync(GFULL, y, 1, W);
@@ -332,9 +337,16 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       pos = gmadd(gi, 1, pos);
 
       // ------------------------------------------------------------------ rare: a segment went idle
-      const unsigned bgo = __ballot_sync(GFULL, go);
-      const bool idle = (segmaskH != 0u) & ((bgo & segmaskH) == 0u);
-      if (__any_sync(GFULL, idle)) {
+      bool idle, any_idle;
+      if constexpr (W == 32) {                             // one segment: idle is warp-uniform
+        idle = (segmaskH != 0u) & !__any_sync(GFULL, go);
+        any_idle = idle;
+      } else {
+        const unsigned bgo = __ballot_sync(GFULL, go);
+        idle = (segmaskH != 0u) & ((bgo & segmaskH) == 0u);
+        any_idle = __any_sync(GFULL, idle);
+      }
+      if (any_idle) {
         const unsigned b_unfin = __ballot_sync(GFULL, onS && nW < m);
         const unsigned b_ring = __ballot_sync(GFULL, item >= 0 && s < p && nF < m && nF - nD >= R);
         const unsigned b_mem = __ballot_sync(GFULL, item >= 0 && s < p && peak > mlim);
