@@ -299,7 +299,9 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       // an F whose consumer ring is full (lead would exceed R: undersized ring hint) is not executed:
       // the lane stalls and the item is re-run by the global-ring fix-up pass (decisions unchanged)
       // (t* < GINF matters: an idle neighbour's horizon term can exceed GINF)
-      const bool go = (tstar < GINF) & (tstar < gmin(Lh, Rh)) & !(pF & (nF - nD >= R));
+      // (sweep: rings hold the lead bound min(m, floor(M_L / m_f)), and memory caps nF - nD at it --
+      // mem >= (nF - nD) m_f since m_d, m_w <= 0 and m_f + m_d + m_w = 0 -- so they cannot fill)
+      const bool go = (tstar < GINF) & (tstar < gmin(Lh, Rh)) & (kGrid || !(pF & (nF - nD >= R)));
       const bool pW = !pD & !pF;
       const bool wfin = wsub + 1 == nsub;
       const int4 ta = tab[pF ? 0 : 32];                    // F or D row: {duration, memory delta, link bw, latency}
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       const bool gW = go & pW;
       clk = gmadd(gi, end - clk, clk);
       mem = gmadd(gi, dmv, mem);
-      peak = gmax(peak, mem);
+      if (!kGrid) peak = gmax(peak, mem);                 // (sweep: F's memory test keeps mem <= M_L)
       linkF = gmadd(gFi, nl - linkF, linkF);
       linkB = gmadd(gDi, nl - linkB, linkB);
       nF = gmadd(gFi, 1, nF);
