@@ -72,6 +72,8 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
   // per-warp smem (words): [params 6*32 int4][ringF R*32][ringD R*32]
   const int wbase = wib * A.smem_words_per_warp;
   const int iF = wbase + kGreedyTableWords + lane, iD = iF + RW;
+  int* const ringF = smem + iF;                        // this lane's ring columns (slot k at [k << 5])
+  int* const ringD = smem + iD;
   int4* const tab = reinterpret_cast<int4*>(smem + wbase) + lane;    // [entry][lane]
   // stage 0's F ring is never written by a producer: it must read 0 (cleared once)
   for (int k = lane; k < 2 * RW; k += 32) smem[wbase + kGreedyTableWords + k] = 0;
@@ -260,9 +262,11 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       const int leftF = gmax(__shfl_up_sync(GFULL, nF, 1, W), lmF);
       const int rD0 = __shfl_down_sync(GFULL, nD, 1, W);
       const int rightD = lastS ? nF : rD0;                // the last stage's D follows its own F
-      const int adF = iF + ((nF & Rm) << 5), adD = iD + ((nD & Rm) << 5);   // ring heads
-      const int availF = gmax(smem[adF], tag);
-      const int availD = smem[adD];
+      // ring heads (byte offsets: one mask and one multiply-add each)
+      int* const hF = reinterpret_cast<int*>(reinterpret_cast<char*>(ringF) + ((nF & Rm) << 7));
+      int* const hD = reinterpret_cast<int*>(reinterpret_cast<char*>(ringD) + ((nD & Rm) << 7));
+      const int availF = gmax(*hF, tag);
+      const int availD = *hD;
       const bool hasF = (leftF > nF) & (mem + mf <= mlim);   // Q15
       // D / W: rightD >= nD and nD >= nW always, so max(n - bound + 1, 0) is 1 exactly when the op is
       // not eligible, and a multiply-add lifts its time past GINF (times stay below 2^30)
@@ -306,11 +310,13 @@ __global__ void __launch_bounds__(kFastThreads, kGreedyMinBlocks) k_greedy_fast(
       const bool wfin = wsub + 1 == nsub;
       const int4 ta = tab[pF ? 0 : 32];                    // F or D row: {duration, memory delta, link bw, latency}
       // a W sub-block (Q12): duration wq + (sub-block index < t_w mod n_sub), memory delta m_w at the last
-      const int dur = pW ? wq + (wsub < wr ? 1 : 0) : ta.x;
+      int wdur;                                            // wq + (wsub < wr): the borrow bit of wsub - wr, by IMAD.HI
+      asm("mad.hi.u32 %0, %1, 2, %2;" : "=r"(wdur) : "r"(wsub - wr), "r"(wq));
+      const int dur = pW ? wdur : ta.x;
       const int dmv = pW ? (wfin ? mw : 0) : ta.y;
       const int end = tstar + dur;
       const int nl = gmax(end, pF ? linkF : linkB) + ta.z;   // FIFO link clock (App. X1)
-      if (go & !pW) smem[pF ? adF + offF : adD + offD] = nl + ta.w;
+      if (go & !pW) *(pF ? hF + offF : hD + offD) = nl + ta.w;
       // emit the 2-bit entry into a shift register (the newest entry enters at bits 30-31, so after
       // 16 entries entry k sits at bits 2k); a full word goes straight to global memory
       const int gi = go ? 1 : 0, gFi = (go & pF) ? 1 : 0, gDi = (go & pD) ? 1 : 0;
