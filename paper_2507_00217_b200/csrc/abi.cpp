@@ -161,7 +161,8 @@ int run_engine(cpk::Mode mode, const cp_instances* in, const cp_schedules* sc, c
     // both passes.
     bool first_done = false;
     if (!std::getenv("CP_CHUNKF_OFF")) {
-      a.ring_slots = std::max(2, fast_ring_slots(in));   // W readiness needs R >= 2
+      // W readiness needs R >= 2; the UD kernel's base | slot addressing needs R <= 8 (CHUNKF_WBS)
+      a.ring_slots = std::max(2, CHUNKF_WBS ? std::min(8, fast_ring_slots(in)) : fast_ring_slots(in));
       a.shared_tab = (!sc->inst_of && in->n == 1) ? 1 : 0;
       const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0, 2, tl);
       const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;

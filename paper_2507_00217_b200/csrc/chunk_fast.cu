@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
   constexpr int kRings = kUD ? 2 : 4, kEPW = kUD ? 16 : 8, kStep = 32 / kEPW;   // entries per word, bits per entry
   constexpr int kChunks = kUD ? 1 : 2;
   constexpr uint32_t kPad = kUD ? 0xaaaaaaaau : 0x22222222u;   // D (UD) / D0 entries: never ready at the end
-  extern __shared__ __align__(128) int32_t smem[];
+  extern __shared__ __align__(1024) int32_t smem[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, s = lane;
   const int R = A.ring_slots, Rm = R - 1, PW = A.words;
   constexpr bool kStage = kTL && kUD;             // UD timelines: staged, written 8 ticks (32 B) per lane
@@ -327,9 +327,22 @@ __global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF
       const uint32_t sX = prmt(kxl, kxh, x4), sY = prmt(kyl, kyh, x4), sN = prmt(knl, knh, x4);
       const uint32_t X = prmt(Lv, Rv, sX), Y = prmt(Lv, Rv, sY), n = prmt(c, kUD ? c : w, sN);
       const bool go = (X > n) & ((int)(n - Y) < R24);
-      const unsigned slot = (n >> 17) & (unsigned)Rm7;
       const bool isF = kUD ? (x4 & 0xF0u) == 0u : t1.z == lk_off_r;   // the message takes the right link
-      const unsigned ia = wb + (unsigned)t1.x + slot, oa = wb + (unsigned)t1.y + slot, la = wb + (unsigned)t1.z;
+      unsigned ia, oa;
+      const unsigned la = wb + (unsigned)t1.z;
+      if (kUD && CHUNKF_WBS) {
+        // UD warp regions are 1 KB-aligned (chunkf_layout, __align__(1024)) and a slot offset is below
+        // 1 KB (R <= 8), so base | slot = base + slot: one LOP3, and the two adds become 2-input
+        // (FMA-pipe) adds -- this loop is ALU-pipe bound (config 4: 79.4 -> 83.1 M evals/s)
+        unsigned wbs;
+        asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(wbs) : "r"(n >> 17), "r"((unsigned)Rm7), "r"(wb));
+        ia = wbs + (unsigned)t1.x;
+        oa = wbs + (unsigned)t1.y;
+      } else {
+        const unsigned slot = (n >> 17) & (unsigned)Rm7;
+        ia = wb + (unsigned)t1.x + slot;
+        oa = wb + (unsigned)t1.y + slot;
+      }
       int arr, lk;
       asm volatile("ld.shared.b32 %0, [%1];" : "=r"(arr) : "r"(ia));
       constexpr bool kLkReg = kUD ? CHUNKF_UD_LKREG : CHUNKF_2C_LKREG;

@@ -158,6 +158,9 @@ struct ChunkFLayout {
   int hdr, bars, zero, zrows, lk, rings, plan, stage, tab, per_warp;
 };
 // timeline (UD): a [16][32] staging ring of start ticks after the plan rows
+#ifndef CHUNKF_WBS
+#define CHUNKF_WBS 1   // UD: 1 KB-aligned warp regions, ring slot offsets OR-ed into the warp base (R <= 8)
+#endif
 __host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool shared_tab, int rings, bool timeline = false) {
   ChunkFLayout L;
   L.hdr = shared_tab ? kChunkFTabWords : 0;
@@ -172,6 +175,10 @@ __host__ __device__ inline ChunkFLayout chunkf_layout(int R, int words, bool sha
   if (timeline) w += 16 * 32;
   L.tab = shared_tab ? -1 : w;
   if (!shared_tab) w += kChunkFTabWords;
+  if (CHUNKF_WBS && rings == 2) {                 // UD (chunk_fast.cu: warp base | slot offset)
+    L.hdr = (L.hdr + 255) & ~255;
+    w = (w + 255) & ~255;
+  }
   L.per_warp = w;
   return L;
 }
