@@ -462,7 +462,7 @@ int run_wave(const cp_instances* in, const cp_schedules* sc, const cp_results* r
     a.plan_words = sc->words;
     a.shared_tab = (!sc->inst_of && in->n == 1) ? 1 : 0;
     const cpk::ChunkFLayout L = cpk::chunkf_layout(a.ring_slots, sc->words, a.shared_tab != 0, 4);
-    const int wpb = cpk::kChunkFThreads / 32, threads = cpk::kChunkFThreads;
+    const int wpb = cpk::kChunkF2CThreads / 32, threads = cpk::kChunkF2CThreads;
     const size_t smem = ((size_t)L.hdr + (size_t)wpb * L.per_warp) * 4;
     if (smem <= kMaxSmemPerBlock) {
       int bps = smsp_balanced(cpk::chunkf_blocks_per_sm(sc->pattern, threads, smem, tl), wpb);

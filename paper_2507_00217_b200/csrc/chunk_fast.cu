@@ -36,7 +36,7 @@
 #define CHUNKF_2C_LKREG 0   // the same for Wave / Loop (the link is the one the table's link address names)
 #endif
 #ifndef CHUNKF_2C_MINB
-#define CHUNKF_2C_MINB kChunkFMinBlocks   // Wave / Loop
+#define CHUNKF_2C_MINB 2   // Wave / Loop (with CHUNKF_2C_THREADS = 384)
 #endif
 #ifndef CHUNKF_UD_MINB
 #define CHUNKF_UD_MINB 6   // UD: 24 resident warps at <= 80 registers (measured +0.6% over 20 warps; 28, 32: no further gain)
@@ -148,7 +148,8 @@ __device__ void chunkf_tables(const cp_inst_v1* I, int s, int R, const ChunkFLay
 }  // namespace
 
 template <int kPat, bool kTL>   // kPat: CP_PATTERN_UD / _WAVE / _LOOP; kTL: per-entry start ticks (A.t_start)
-__global__ void __launch_bounds__(kChunkFThreads, kPat == CP_PATTERN_UD ? CHUNKF_UD_MINB : CHUNKF_2C_MINB) k_chunk32f(const __grid_constant__ Args A) {
+__global__ void __launch_bounds__(kPat == CP_PATTERN_UD ? kChunkFThreads : kChunkF2CThreads,
+                                  kPat == CP_PATTERN_UD ? CHUNKF_UD_MINB : CHUNKF_2C_MINB) k_chunk32f(const __grid_constant__ Args A) {
   constexpr bool kUD = kPat == CP_PATTERN_UD, kLoop = kPat == CP_PATTERN_LOOP;
   constexpr int kRings = kUD ? 2 : 4, kEPW = kUD ? 16 : 8, kStep = 32 / kEPW;   // entries per word, bits per entry
   constexpr int kChunks = kUD ? 1 : 2;

@@ -153,6 +153,12 @@ __host__ __device__ inline Sim32Layout sim32_layout(int R, int plan_words, bool 
 // holds them.
 constexpr int kChunkFTabWords = 2 * 8 * 32 * 4 + 8 * 4;
 constexpr int kChunkFThreads = 128;
+#ifndef CHUNKF_2C_THREADS
+// Wave / Loop: 12-warp blocks, 2 per SM (the shared table amortized over 12 warps; 24 resident warps
+// at <= 80 registers): +1.6% Wave, +0.7% Loop over 4-warp blocks; 6-warp blocks: -11%
+#define CHUNKF_2C_THREADS 384
+#endif
+constexpr int kChunkF2CThreads = CHUNKF_2C_THREADS;
 constexpr int kChunkFMinBlocks = 5;
 struct ChunkFLayout {
   int hdr, bars, zero, zrows, lk, rings, plan, stage, tab, per_warp;
