@@ -298,7 +298,9 @@ def test_sweep_config2_every_point(O):
 
 def test_sweep_config5_sample_and_shards(O):
     """Config 5 (4 DCs, p 8-32, m 8-128, memory grid): 400 sampled points; shards over 1/2/4/8
-    cost-balanced ranges assembled with MIN give byte-identical keys."""
+    cost-balanced ranges assembled with MIN give byte-identical keys, and so do the rank shards --
+    whose largest-n_mb greedy tasks run in launches of their own (DESIGN.md §7 Sweep) -- together
+    with every candidate's makespan."""
     grid = K.full_sweep_grid()
     full, cm = cp.sweep_shard(grid, cand=True)
     torch.cuda.synchronize()
@@ -310,13 +312,16 @@ def test_sweep_config5_sample_and_shards(O):
         b = cp.sweep_partition(grid, world)
         acc = torch.full((grid.n_points,), cp.KEY_NONE, dtype=torch.int64, device="cuda")
         acc_r = acc.clone()
+        acc_c = torch.full_like(cm, -1)
         for rk in range(world):
             kr, _ = cp.sweep_shard(grid, b[rk], b[rk + 1])
             acc = torch.minimum(acc, kr)
-            kb, _ = cp.sweep_shard_rank(grid, rk, world)          # blocked ownership
+            kb, cb = cp.sweep_shard_rank(grid, rk, world, cand=True)   # blocked ownership
             acc_r = torch.minimum(acc_r, kb)
+            acc_c = torch.maximum(acc_c, cb)                          # (not owned: -1)
         assert torch.equal(acc.cpu(), torch.from_numpy(full_h)), world
         assert torch.equal(acc_r.cpu(), torch.from_numpy(full_h)), ("rank shards", world)
+        assert torch.equal(acc_c, cm), ("rank-shard candidate makespans", world)
 
 
 def test_sweep_global_ring_fallback(O):
